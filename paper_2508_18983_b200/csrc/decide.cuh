@@ -1,0 +1,798 @@
+// decide.cuh — one (iteration, layer) decision step on the device.
+//
+// decide_step() restates Simulator::run_layer (pipeline.cpp:128-286) and
+// Simulator::schedule_prefetch (pipeline.cpp:293-344) with the policies they
+// call: route (router.cpp:97-152), coalesce_for_batching (router.cpp:154-260),
+// plain_top_k (router.cpp:35-39), CacheState (cache.cpp:58-156), balance
+// (balancer.cpp:8-38), predict_scores / build_queue (prefetch.cpp:34-115).
+// Called by the whole decision CTA (kThreads threads).
+#pragma once
+
+#include "engine.cuh"
+
+namespace moeb {
+
+struct StepCtx {
+  const DevCfg* cfg;
+  EngineState* st;       // global
+  LayerState* layers;    // global [L]
+  double* hist;          // global [L][window][E]
+  const Logs* logs;      // nullable
+  uint64_t it;
+  uint32_t layer;
+  uint32_t has_target;   // prefetch target exists (pipeline.cpp:401-409)
+  uint32_t target_layer;
+  uint64_t target_it;
+};
+
+// Extra shared state for the prefetch target's classification.
+struct NextSmem {
+  uint8_t order[kMaxB][kMaxE];
+  uint64_t act[kMaxB], top[kMaxB];
+};
+
+// ------------------------------------------------------- cache helpers
+// cache.cpp:69-79: sum oldest -> newest, then divide by the window size.
+__device__ __forceinline__ double window_average(const LayerState* ls, const double* hist_l,
+                                                 uint32_t window, uint32_t E, uint32_t e) {
+  if (ls->h_size == 0) return 0.0;
+  double sum = 0.0;
+  uint32_t slot = ls->h_head;
+  for (uint32_t i = 0; i < ls->h_size; ++i) {
+    sum += hist_l[(size_t)slot * E + e];
+    slot = (slot + 1 == window) ? 0 : slot + 1;
+  }
+  return sum / (double)ls->h_size;
+}
+
+// cache.cpp:81-106 (warp-collective; every lane returns the victim or -1).
+__device__ inline int try_evict_warp(const LayerState* ls, const double* hist_l, const DevCfg& cfg) {
+  const int lane = lane_id();
+  const uint64_t cand = ls->mask & ~ls->shield;
+  if (cfg.policy == 0) {
+    double key = 0.0;
+    uint32_t idx = 0xffffffffu;
+    for (uint32_t e = lane; e < cfg.E; e += 32) {
+      if (!has(cand, e)) continue;
+      const double a = window_average(ls, hist_l, cfg.window, cfg.E, e);
+      if (idx == 0xffffffffu || a < key) { key = a; idx = e; }
+    }
+    warp_argmin_d(key, idx);
+    return idx == 0xffffffffu ? -1 : (int)idx;
+  }
+  uint64_t key = 0;
+  uint32_t idx = 0xffffffffu;
+  for (uint32_t e = lane; e < cfg.E; e += 32) {
+    if (!has(cand, e)) continue;
+    const uint64_t a = ls->last_access[e];
+    if (idx == 0xffffffffu || a < key) { key = a; idx = e; }
+  }
+  warp_argmin_u(key, idx);
+  return idx == 0xffffffffu ? -1 : (int)idx;
+}
+
+// cache.cpp:136-156. Returns 0 ok, 3 CacheError (all shielded), 4 already
+// resident. victim/slot are -1 when none. Warp-collective.
+__device__ inline int admit_warp(LayerState* ls, const double* hist_l, const DevCfg& cfg,
+                                 uint32_t e, uint64_t now, int& victim, int& slot) {
+  const int lane = lane_id();
+  victim = -1;
+  slot = -1;
+  if (has(ls->mask, e)) return 4;
+  if (cfg.slots == 0) return 0;  // zero-slot cache: loads pass through
+  if (ls->n_res >= cfg.slots) {
+    const int v = try_evict_warp(ls, hist_l, cfg);
+    if (v < 0) return 3;
+    victim = v;
+    slot = ls->slot_of[v];
+    __syncwarp();
+    if (lane == 0) {
+      ls->mask &= ~bit(v);
+      ls->n_res -= 1;
+      ls->slot_of[v] = -1;
+      if (slot >= 0) ls->expert_of_slot[slot] = -1;
+    }
+    __syncwarp();
+  }
+  if (slot < 0) {
+    const uint32_t nslot = cfg.slots < (uint32_t)kMaxSlots ? cfg.slots : (uint32_t)kMaxSlots;
+    const bool f0 = (uint32_t)lane < nslot && ls->expert_of_slot[lane] < 0;
+    const bool f1 = (uint32_t)lane + 32 < nslot && ls->expert_of_slot[lane + 32] < 0;
+    const uint64_t free_mask = ballot64(f0, f1);
+    slot = free_mask ? __ffsll((long long)free_mask) - 1 : -1;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    ls->mask |= bit(e);
+    ls->n_res += 1;
+    ls->last_access[e] = now;
+    ls->slot_of[e] = (int8_t)slot;
+    if (slot >= 0) ls->expert_of_slot[slot] = (int8_t)e;
+  }
+  __syncwarp();
+  return 0;
+}
+
+// cache.cpp:58-67: push one score vector into the ring (warp-collective).
+__device__ inline void record_scores_warp(LayerState* ls, double* hist_l, uint32_t window,
+                                          uint32_t E, const double* v) {
+  uint32_t slot;
+  const uint32_t head = ls->h_head, size = ls->h_size;
+  if (size < window) {
+    slot = head + size;
+    if (slot >= window) slot -= window;
+  } else {
+    slot = head;
+  }
+  for (uint32_t e = lane_id(); e < E; e += 32) hist_l[(size_t)slot * E + e] = v[e];
+  __syncwarp();
+  if (lane_id() == 0) {
+    if (size < window) {
+      ls->h_size = size + 1;
+    } else {
+      ls->h_head = (head + 1 == window) ? 0 : head + 1;
+    }
+  }
+  __syncwarp();
+}
+
+// --------------------------------------------------------- router parts
+// router.cpp:114-149: pass 2 for token t (executed by one lane).
+__device__ inline void route_token(DecideSmem* sm, uint32_t t, uint64_t resident, uint32_t E,
+                                   uint32_t k) {
+  const uint64_t free_set = resident | sm->C;
+  const uint8_t* order = sm->order[t];
+  const uint64_t top = sm->top[t], low = sm->low[t], alt = sm->alt[t];
+  uint32_t n = 0, nk = 0, ns = 0;
+  for (uint32_t r = 0; r < k; ++r) {
+    const uint32_t e = order[r];
+    if (has(top, e)) sm->sel[t][n++] = (uint8_t)e;
+  }
+  uint8_t blow[kMaxK];
+  uint32_t m = 0;
+  for (uint32_t r = 0; r < k; ++r) {
+    const uint32_t e = order[r];
+    if (!has(low, e)) continue;
+    if (has(free_set, e)) sm->sel[t][n++] = (uint8_t)e;
+    else blow[m++] = (uint8_t)e;
+  }
+  uint8_t alts[kMaxK];
+  uint32_t na = 0;
+  for (uint32_t r = k; r < E && na < m; ++r) {
+    const uint32_t e = order[r];
+    if (has(alt, e) && has(free_set, e)) alts[na++] = (uint8_t)e;
+  }
+  const uint32_t covered = m < na ? m : na;
+  const uint32_t kept = m - covered;
+  for (uint32_t i = 0; i < kept; ++i) {
+    sm->sel[t][n++] = blow[i];
+    sm->kept[t][nk++] = blow[i];
+  }
+  for (uint32_t i = 0; i < covered; ++i) {
+    sm->sel[t][n++] = alts[i];
+    sm->sub_d[t][ns] = blow[kept + i];
+    sm->sub_c[t][ns] = alts[i];
+    ++ns;
+  }
+  sm->nsel[t] = (uint8_t)n;
+  sm->nkept[t] = (uint8_t)nk;
+  sm->nsub[t] = (uint8_t)ns;
+}
+
+// router.cpp:154-248: fixed-point coalescing, warp 0. The candidate scan
+// (ascending x, replace on more others, or equal others with higher score)
+// is the lexicographic max of (others, score, -x) over candidates whose
+// count beats the occupant's, reduced across lanes.
+__device__ inline void coalesce_warp(DecideSmem* sm, uint32_t B, uint32_t E, uint32_t k,
+                                     uint64_t resident, uint16_t* cnt) {
+  const int lane = lane_id();
+  for (uint32_t e = lane; e < E; e += 32) cnt[e] = 0;
+  __syncwarp();
+  if (lane == 0)
+    for (uint32_t t = 0; t < B; ++t)
+      for (uint32_t i = 0; i < sm->nsel[t]; ++i) cnt[sm->sel[t][i]]++;
+  __syncwarp();
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (uint32_t t = 0; t < B; ++t) {
+      const double* s = sm->s[t];
+      uint64_t selm = 0;
+      for (uint32_t i = 0; i < sm->nsel[t]; ++i) selm |= bit(sm->sel[t][i]);
+      const uint64_t actm = sm->act[t];
+      const double beta = sm->beta[t], thR = sm->thR[t], thL = sm->thL[t];
+      for (uint32_t r = 0; r < k; ++r) {
+        const uint32_t orig = sm->order[t][r];
+        if (!has(sm->low[t], orig)) continue;
+        int kept_pos = -1, sub_pos = -1;
+        for (uint32_t i = 0; i < sm->nkept[t]; ++i)
+          if (sm->kept[t][i] == orig) { kept_pos = (int)i; break; }
+        uint32_t occupant;
+        if (kept_pos >= 0) {
+          occupant = orig;
+        } else {
+          for (uint32_t i = 0; i < sm->nsub[t]; ++i)
+            if (sm->sub_d[t][i] == orig) { sub_pos = (int)i; break; }
+          if (sub_pos < 0) continue;
+          occupant = sm->sub_c[t][sub_pos];
+        }
+        const uint32_t occ_others = cnt[occupant] - 1u;
+        // lane-parallel candidate search
+        uint32_t b_oth = 0, b_x = 0xffffffffu;
+        double b_s = 0.0;
+        for (uint32_t x = lane; x < E; x += 32) {
+          const double sx = s[x];
+          if (!(beta > 0.0 && sx >= thR && sx < thL)) continue;
+          if (has(actm, x) || has(selm, x)) continue;
+          const uint32_t others = cnt[x];
+          if (!(has(resident, x) || has(sm->C, x) || others > 0)) continue;
+          if (others <= occ_others) continue;
+          if (b_x == 0xffffffffu || others > b_oth || (others == b_oth && sx > b_s)) {
+            b_oth = others; b_s = sx; b_x = x;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint32_t o2 = __shfl_xor_sync(0xffffffffu, b_oth, o);
+          const double s2 = __shfl_xor_sync(0xffffffffu, b_s, o);
+          const uint32_t x2 = __shfl_xor_sync(0xffffffffu, b_x, o);
+          const bool take = x2 != 0xffffffffu &&
+                            (b_x == 0xffffffffu || o2 > b_oth ||
+                             (o2 == b_oth && (s2 > b_s || (s2 == b_s && x2 < b_x))));
+          if (take) { b_oth = o2; b_s = s2; b_x = x2; }
+        }
+        if (b_x == 0xffffffffu) continue;  // best == occupant
+        const uint32_t best = b_x;
+        __syncwarp();
+        if (lane == 0) {
+          for (uint32_t i = 0; i < sm->nsel[t]; ++i)
+            if (sm->sel[t][i] == occupant) { sm->sel[t][i] = (uint8_t)best; break; }
+          cnt[occupant] -= 1;
+          cnt[best] += 1;
+          if (sub_pos >= 0) {
+            sm->sub_c[t][sub_pos] = (uint8_t)best;
+          } else {
+            for (uint32_t i = (uint32_t)kept_pos; i + 1 < sm->nkept[t]; ++i)
+              sm->kept[t][i] = sm->kept[t][i + 1];
+            sm->nkept[t] -= 1;
+            const uint32_t ns = sm->nsub[t];
+            sm->sub_d[t][ns] = (uint8_t)orig;
+            sm->sub_c[t][ns] = (uint8_t)best;
+            sm->nsub[t] = (uint8_t)(ns + 1);
+          }
+        }
+        __syncwarp();
+        selm = (selm & ~bit(occupant)) | bit(best);
+        changed = true;
+      }
+    }
+  }
+}
+
+// balancer.cpp:8-38 on warp 0. uid/batch ascending by uid on entry.
+__device__ inline void balance_warp(const uint8_t* uid, const uint16_t* batch, uint32_t n,
+                                    uint64_t t_cpu_token, uint64_t t_load, uint8_t* load,
+                                    uint32_t& n_load, uint8_t* cpu, uint32_t& n_cpu) {
+  __shared__ uint8_t sorted[kMaxE];
+  const int lane = lane_id();
+  for (uint32_t i = lane; i < n; i += 32) {
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < n; ++j)
+      r += batch[j] > batch[i] || (batch[j] == batch[i] && uid[j] < uid[i]);
+    sorted[r] = (uint8_t)i;
+  }
+  __syncwarp();
+  n_load = n_cpu = 0;
+  uint64_t c_load = 0, c_cpu = 0;
+  if (n > 0) {
+    int l = 0, r = (int)n - 1;
+    while (l <= r) {
+      if (c_load <= c_cpu) {
+        c_load += t_load;
+        load[n_load++] = uid[sorted[l]];
+        ++l;
+      } else {
+        c_cpu += (uint64_t)batch[sorted[r]] * t_cpu_token;
+        cpu[n_cpu++] = uid[sorted[r]];
+        if (r == 0) break;
+        --r;
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// --------------------------------------------------------------- step
+struct StepScratch {
+  uint64_t attn_end, route_end;
+  uint16_t cnt[kMaxE];
+  uint8_t duid[kMaxE];
+  uint16_t dbat[kMaxE];
+  uint32_t ndm;
+};
+
+__device__ inline void log_eviction(const Logs* lg, StepOut* out, uint64_t now, uint32_t layer,
+                                    uint32_t e) {
+  if (lane_id() == 0) {
+    if (lg && lg->evs) {
+      const unsigned long long i = atomicAdd(&lg->counts[2], 1ULL);
+      if (i < lg->cap_evs) {
+        EvRec r;
+        r.time = now; r.layer = layer; r.e = e;
+        lg->evs[i] = r;
+      } else {
+        *lg->overflow = 1;
+      }
+    }
+    if (out->n_evict < 2 * kMaxE) {
+      // ev_layer/ev_e live in the StepRec; StepOut keeps only the count
+    }
+    out->n_evict++;
+  }
+}
+
+// admit_or_defer (pipeline.cpp:93-108), warp-collective. Returns the slot
+// (>= 0), -1 when nothing was inserted, -2 when the admission was deferred.
+__device__ inline int admit_or_defer(const StepCtx& cx, DecideSmem* sm, LayerState* ls,
+                                     uint32_t layer, uint32_t e, uint64_t now, bool shield_it,
+                                     uint8_t* ev_layer, uint8_t* ev_e) {
+  const DevCfg& cfg = *cx.cfg;
+  if (has(ls->mask, e)) return ls->slot_of[e];
+  int victim, slot;
+  const int rc = admit_warp(ls, cx.hist + (size_t)layer * cfg.window * cfg.E, cfg, e, now,
+                            victim, slot);
+  if (rc == 3) {
+    if (lane_id() == 0) sm->def_e[sm->n_def++] = e;
+    __syncwarp();
+    return -2;
+  }
+  if (rc == 4) {
+    if (lane_id() == 0) cx.st->err = 4;
+    return -1;
+  }
+  if (victim >= 0) {
+    if (lane_id() == 0 && sm->out.n_evict < 2 * kMaxE) {
+      ev_layer[sm->out.n_evict] = (uint8_t)layer;
+      ev_e[sm->out.n_evict] = (uint8_t)victim;
+    }
+    __syncwarp();
+    log_eviction(cx.logs, &sm->out, now, layer, (uint32_t)victim);
+    __syncwarp();
+  }
+  if (shield_it && lane_id() == 0) ls->shield |= bit(e);
+  __syncwarp();
+  return slot;
+}
+
+// The step. Caller fills sm->s (and sm->ns / sm->np / sm->next_has_pred when
+// cx.has_target && cfg.pre) and __syncthreads() before the call.
+__device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* nx,
+                                   StepScratch* sc, StepRec* rec_out, TokRec* tok_out) {
+  const DevCfg& cfg = *cx.cfg;
+  EngineState* st = cx.st;
+  const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
+  const uint32_t E = cfg.E, B = cfg.B, k = cfg.k, layer = cx.layer;
+  const uint64_t it = cx.it;
+
+  // stage the executing layer's state
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&cx.layers[layer]);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(&sm->ls);
+    for (uint32_t i = tid; i < sizeof(LayerState) / 8; i += blockDim.x) dst[i] = src[i];
+  }
+  if (tid == 0) {
+    const uint64_t start = st->now;
+    // attention + gate (pipeline.cpp:133-145)
+    const uint64_t attn_end = start + cfg.t_attn;
+    log_task(cx.logs, R_GPU, K_ATTN, -1, 0, start, attn_end, layer, it);
+    st->gpu_free = attn_end;
+    if (st->q_valid && st->q_layer == layer && st->q_it == it) {
+      const uint64_t all = st->q_n >= 64 ? ~0ULL : ((1ULL << st->q_n) - 1ULL);
+      st->c.cancelled += __popcll(all & ~st->q_issued);
+      st->q_valid = 0;
+    }
+    // routing on CPU (pipeline.cpp:147-152)
+    const uint64_t route_start = attn_end > st->cpu_free ? attn_end : st->cpu_free;
+    const uint64_t route_end = route_start + cfg.t_route;
+    log_task(cx.logs, R_CPU, K_ROUTE, -1, 0, route_start, route_end, layer, it);
+    st->cpu_free = route_end;
+    sc->attn_end = attn_end;
+    sc->route_end = route_end;
+    sm->n_def = 0;
+    sm->out.n_load = sm->out.n_cpu = sm->out.n_pref = sm->out.n_def = sm->out.n_evict = 0;
+    sm->out.n_res = 0;
+  }
+  __syncthreads();
+  const uint64_t mask = sm->ls.mask;  // snapshot the router sees (pipeline.cpp:154-155)
+
+  // classify every token (and the prefetch target's tokens) — warp per token
+  const bool want_next = cfg.pre && cx.has_target;
+  for (uint32_t t = warp; t < B; t += kWarps) {
+    uint64_t a, tp, lw, al;
+    double b, T, L, R;
+    classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R);
+    if (lane == 0) {
+      sm->act[t] = a; sm->top[t] = tp; sm->low[t] = lw; sm->alt[t] = al;
+      sm->beta[t] = b; sm->thT[t] = T; sm->thL[t] = L; sm->thR[t] = R;
+    }
+    if (want_next) {
+      classify_warp(sm->ns[t], E, k, cfg.alpha, nx->order[t], a, tp, lw, al, b, T, L, R);
+      if (lane == 0) { nx->act[t] = a; nx->top[t] = tp; }
+    }
+  }
+  __syncthreads();
+
+  if (cfg.er) {
+    if (tid == 0) {
+      uint64_t C = 0;
+      for (uint32_t t = 0; t < B; ++t) C |= sm->top[t];
+      sm->C = C;
+    }
+    __syncthreads();
+    for (uint32_t t = warp; t < B; t += kWarps)
+      if (lane == 0) route_token(sm, t, mask, E, k);
+    __syncthreads();
+    if (warp == 0) coalesce_warp(sm, B, E, k, mask, sc->cnt);
+    __syncthreads();
+  } else {
+    // plain_top_k (router.cpp:35-39)
+    for (uint32_t t = warp; t < B; t += kWarps) {
+      if (lane == 0) {
+        for (uint32_t r = 0; r < k; ++r) sm->sel[t][r] = sm->order[t][r];
+        sm->nsel[t] = (uint8_t)k;
+        sm->nsub[t] = 0;
+        sm->nkept[t] = 0;
+      }
+    }
+    __syncthreads();
+  }
+
+  if (warp != 0) return;  // the rest is order-dependent: warp 0 in lock-step
+
+  // ---- hit accounting + batch_of (pipeline.cpp:176-189)
+  for (uint32_t e = lane; e < E; e += 32) sc->cnt[e] = 0;
+  __syncwarp();
+  uint64_t n_sel_total = 0, n_hits = 0, n_subs = 0, n_kept = 0;
+  for (uint32_t t = 0; t < B; ++t) {
+    for (uint32_t i = 0; i < sm->nsel[t]; ++i) {
+      const uint32_t e = sm->sel[t][i];
+      n_sel_total++;
+      n_hits += has(mask, e);
+    }
+    n_subs += sm->nsub[t];
+    n_kept += sm->nkept[t];
+  }
+  for (uint32_t e = lane; e < E; e += 32) {
+    uint32_t c = 0;
+    for (uint32_t t = 0; t < B; ++t)
+      for (uint32_t i = 0; i < sm->nsel[t]; ++i) c += sm->sel[t][i] == e;
+    sc->cnt[e] = (uint16_t)c;
+  }
+  // mean over tokens in token order (pipeline.cpp:79-91)
+  for (uint32_t e = lane; e < E; e += 32) {
+    double m = 0.0;
+    for (uint32_t t = 0; t < B; ++t) m += sm->s[t][e];
+    sm->mean[e] = m / (double)B;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    Counters& c = st->c;
+    if (cfg.er) { c.subs += n_subs; c.kept_low += n_kept; }
+    c.selections += n_sel_total;
+    c.hits += n_hits;
+    c.misses += n_sel_total - n_hits;
+  }
+  LayerState* ls = &sm->ls;
+  double* hist_l = cx.hist + (size_t)layer * cfg.window * E;
+  record_scores_warp(ls, hist_l, cfg.window, E, sm->mean);  // pipeline.cpp:191
+
+  // residents: shield + touch; misses -> demand set (pipeline.cpp:196-205)
+  const uint64_t route_end = sc->route_end, attn_end = sc->attn_end;
+  const bool c0 = (uint32_t)lane < E && sc->cnt[lane] > 0;
+  const bool c1 = (uint32_t)lane + 32 < E && sc->cnt[lane + 32] > 0;
+  const uint64_t distinct = ballot64(c0, c1);
+  const uint64_t res_sel = distinct & mask;
+  const uint64_t miss = distinct & ~mask;
+  for (uint32_t e = lane; e < E; e += 32)
+    if (has(res_sel, e)) ls->last_access[e] = route_end;
+  if (lane == 0) {
+    ls->shield |= res_sel;
+    uint32_t n = 0;
+    for (uint64_t m = miss; m; m &= m - 1) {
+      const uint32_t e = __ffsll((long long)m) - 1;
+      sc->duid[n] = (uint8_t)e;
+      sc->dbat[n] = sc->cnt[e];
+      ++n;
+    }
+    sc->ndm = n;
+    uint32_t nr = 0;
+    for (uint64_t m = res_sel; m; m &= m - 1) sm->out.res[nr++] = (uint8_t)(__ffsll((long long)m) - 1);
+    sm->out.n_res = nr;
+    sm->out.mask_before = mask;
+    for (uint32_t e = 0; e < E; ++e) sm->out.cnt[e] = sc->cnt[e];
+  }
+  __syncwarp();
+
+  // BA split (pipeline.cpp:207-215)
+  uint32_t n_load = 0, n_cpu = 0;
+  if (cfg.ba) {
+    balance_warp(sc->duid, sc->dbat, sc->ndm, cfg.t_cpu_token, cfg.t_load, sm->out.load, n_load,
+                 sm->out.cpu, n_cpu);
+  } else {
+    if (lane == 0)
+      for (uint32_t i = 0; i < sc->ndm; ++i) sm->out.load[i] = sc->duid[i];
+    n_load = sc->ndm;
+    n_cpu = 0;
+  }
+  __syncwarp();
+
+  // the per-step record's eviction arrays double as scratch for StepOut
+  __shared__ uint8_t ev_layer[2 * kMaxE], ev_e[2 * kMaxE];
+
+  // CPU expert tasks (pipeline.cpp:217-227)
+  uint64_t cpu_t = route_end > st->cpu_free ? route_end : st->cpu_free;
+  for (uint32_t i = 0; i < n_cpu; ++i) {
+    const uint32_t e = sm->out.cpu[i];
+    const uint64_t dur = (uint64_t)sc->cnt[e] * cfg.t_cpu_token;
+    if (lane == 0) log_task(cx.logs, R_CPU, K_CPU, (int)layer, e, cpu_t, cpu_t + dur, layer, it);
+    cpu_t += dur;
+  }
+  if (lane == 0) { st->cpu_free = cpu_t; st->c.cpu_computed += n_cpu; }
+  __syncwarp();
+
+  // demand loads, serial on PCIe, admitted + shielded (pipeline.cpp:229-240)
+  uint64_t ready[kMaxE];
+  uint64_t pcie_t = route_end > st->pcie_free ? route_end : st->pcie_free;
+  for (uint32_t i = 0; i < n_load; ++i) {
+    const uint32_t e = sm->out.load[i];
+    if (lane == 0) log_task(cx.logs, R_PCIE, K_DEMAND, (int)layer, e, pcie_t, pcie_t + cfg.t_load, layer, it);
+    pcie_t += cfg.t_load;
+    const int slot = admit_or_defer(cx, sm, ls, layer, e, pcie_t, true, ev_layer, ev_e);
+    if (lane == 0) sm->out.load_slot[i] = (int8_t)(slot >= 0 ? slot : -1);
+    ready[i] = pcie_t;
+  }
+  if (lane == 0) { st->pcie_free = pcie_t; st->c.demand += n_load; }
+  __syncwarp();
+
+  // GPU expert compute (pipeline.cpp:242-266)
+  uint64_t gpu_t = st->gpu_free > route_end ? st->gpu_free : route_end;
+  uint64_t resident_done = attn_end > route_end ? attn_end : route_end;
+  const uint32_t nres = sm->out.n_res;
+  for (uint32_t i = 0; i < nres; ++i) {
+    if (lane == 0) log_task(cx.logs, R_GPU, K_RESIDENT, (int)layer, sm->out.res[i], gpu_t, gpu_t + cfg.t_gpu, layer, it);
+    gpu_t += cfg.t_gpu;
+  }
+  if (nres) resident_done = gpu_t;
+  for (uint32_t i = 0; i < n_load; ++i) {
+    const uint64_t s0 = gpu_t > ready[i] ? gpu_t : ready[i];
+    if (lane == 0) log_task(cx.logs, R_GPU, K_LOADED, (int)layer, sm->out.load[i], s0, s0 + cfg.t_gpu, layer, it);
+    gpu_t = s0 + cfg.t_gpu;
+  }
+  uint64_t completion = attn_end;
+  if (route_end > completion) completion = route_end;
+  if (cpu_t > completion) completion = cpu_t;
+  if ((nres || n_load) && gpu_t > completion) completion = gpu_t;
+  if (lane == 0) {
+    st->gpu_free = gpu_t;
+    const Logs* lg = cx.logs;
+    if (lg && lg->wins) {
+      const unsigned long long i = atomicAdd(&lg->counts[1], 1ULL);
+      if (i < lg->cap_wins) {
+        WinRec w;
+        w.it = it; w.layer = layer; w.pad = 0; w.attn_end = attn_end; w.route_end = route_end;
+        w.completion = completion; w.sel = distinct;
+        lg->wins[i] = w;
+      } else {
+        *lg->overflow = 1;
+      }
+    }
+    sm->out.n_load = n_load;
+    sm->out.n_cpu = n_cpu;
+    ls->shield = 0;  // unshield_layer (pipeline.cpp:276)
+  }
+  __syncwarp();
+
+  // deferred admissions, FIFO, unshielded, at completion (pipeline.cpp:277-280)
+  {
+    const uint32_t nd = sm->n_def;
+    uint32_t def_copy[2 * kMaxE];
+    for (uint32_t i = 0; i < nd; ++i) def_copy[i] = sm->def_e[i];
+    __syncwarp();
+    if (lane == 0) sm->n_def = 0;
+    __syncwarp();
+    for (uint32_t i = 0; i < nd; ++i) {
+      const int slot = admit_or_defer(cx, sm, ls, layer, def_copy[i], completion, false, ev_layer, ev_e);
+      if (lane == 0 && slot >= 0 && sm->out.n_def < kMaxE) {
+        sm->out.def_e[sm->out.n_def] = (uint8_t)def_copy[i];
+        sm->out.def_slot[sm->out.n_def] = (int8_t)slot;
+        sm->out.n_def++;
+      }
+      __syncwarp();
+    }
+  }
+
+  // prefetch for the next layer (pipeline.cpp:293-344)
+  uint32_t n_pref = 0;
+  if (want_next) {
+    const uint32_t tl = cx.target_layer;
+    const uint64_t tit = cx.target_it;
+    const uint64_t gate = completion + cfg.t_attn;
+    LayerState* tls = (tl == layer) ? ls : &cx.layers[tl];
+    for (uint32_t e = lane; e < E; e += 32) sm->merged[e] = 0.0;
+    __syncwarp();
+    uint64_t rs[4] = {st->rng[0], st->rng[1], st->rng[2], st->rng[3]};
+    for (uint32_t t = 0; t < B; ++t) {
+      const double* tn = sm->ns[t];
+      const bool supplied = (sm->next_has_pred >> t) & 1ULL;
+      // kind_of / argmax of the true vector
+      const uint64_t ntop = nx->top[t], nact = nx->act[t];
+      uint32_t head;
+      int kind;
+      // argmax_first (prefetch.cpp:12-20): max value, lowest index
+      auto argmax_first = [&](const double* v) -> uint32_t {
+        double bv = 0.0;
+        uint32_t bi = 0xffffffffu;
+        for (uint32_t e = lane; e < E; e += 32)
+          if (bi == 0xffffffffu || v[e] > bv) { bv = v[e]; bi = e; }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+          const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (i2 != 0xffffffffu && (bi == 0xffffffffu || v2 > bv || (v2 == bv && i2 < bi))) { bv = v2; bi = i2; }
+        }
+        return bi;
+      };
+      uint32_t tt = 0;
+      if (supplied) {
+        head = argmax_first(sm->np[t]);
+        kind = has(ntop, head) ? 0 : (has(nact, head) ? 1 : 2);
+        for (uint32_t e = lane; e < E; e += 32) {
+          const double v = sm->np[t][e];
+          if (sm->merged[e] < v) sm->merged[e] = v;
+        }
+      } else {
+        const uint32_t n_top = __popcll(ntop);
+        if (rng_double(rs) < cfg.p_top && n_top > 0) {
+          const uint32_t pick = (uint32_t)rng_below(rs, n_top);
+          uint32_t c = 0;
+          head = 0;
+          for (uint32_t r = 0; r < k; ++r) {
+            const uint32_t e = nx->order[t][r];
+            if (has(ntop, e)) { if (c == pick) { head = e; break; } ++c; }
+          }
+          kind = 0;
+        } else {
+          const uint64_t lows = nact & ~ntop;
+          const uint32_t n_low = __popcll(lows);
+          if (rng_double(rs) < cfg.p_active && n_low > 0) {
+            const uint32_t pick = (uint32_t)rng_below(rs, n_low);
+            uint32_t c = 0;
+            head = 0;
+            for (uint32_t r = 0; r < k; ++r) {
+              const uint32_t e = nx->order[t][r];
+              if (has(lows, e)) { if (c == pick) { head = e; break; } ++c; }
+            }
+            kind = 1;
+          } else {
+            const uint64_t allm = E >= 64 ? ~0ULL : ((1ULL << E) - 1ULL);
+            const uint64_t inact = allm & ~nact;
+            uint32_t pick = (uint32_t)rng_below(rs, __popcll(inact));
+            uint64_t m = inact;
+            for (uint32_t i = 0; i < pick; ++i) m &= m - 1;
+            head = __ffsll((long long)m) - 1;
+            kind = 2;
+          }
+        }
+        tt = argmax_first(tn);
+        for (uint32_t e = lane; e < E; e += 32) {
+          const double v = (e == head) ? tn[tt] : ((e == tt) ? tn[head] : tn[e]);
+          if (sm->merged[e] < v) sm->merged[e] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        Counters& c = st->c;
+        if (supplied) c.trace_supplied++; else c.draws++;
+        if (kind == 0) c.head_top++; else if (kind == 1) c.head_active++; else c.head_inactive++;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) { st->rng[0] = rs[0]; st->rng[1] = rs[1]; st->rng[2] = rs[2]; st->rng[3] = rs[3]; }
+    // build_queue (prefetch.cpp:85-115): rank merged, first `depth` non-resident
+    __shared__ uint8_t qorder[kMaxE];
+    for (uint32_t e = lane; e < E; e += 32) {
+      const double v = sm->merged[e];
+      uint32_t r = 0;
+      for (uint32_t j = 0; j < E; ++j) {
+        const double vj = sm->merged[j];
+        r += (vj > v) || (vj == v && j < e);
+      }
+      qorder[r] = (uint8_t)e;
+    }
+    __syncwarp();
+    const uint64_t tmask = tls->mask;
+    uint32_t qn = 0;
+    uint8_t qe[kMaxE];
+    if (cfg.depth > 0)
+      for (uint32_t r = 0; r < E && qn < cfg.depth; ++r) {
+        const uint32_t e = qorder[r];
+        if (!has(tmask, e)) qe[qn++] = (uint8_t)e;
+      }
+    uint64_t t = st->pcie_free > resident_done ? st->pcie_free : resident_done;
+    uint64_t issued = 0;
+    for (uint32_t i = 0; i < qn; ++i) {
+      if (t + cfg.t_load > gate) break;
+      const uint32_t e = qe[i];
+      if (has(tls->mask, e)) continue;
+      if (lane == 0) log_task(cx.logs, R_PCIE, K_PREFETCH, (int)tl, e, t, t + cfg.t_load, tl, tit);
+      t += cfg.t_load;
+      issued |= bit(i);
+      const int slot = admit_or_defer(cx, sm, tls, tl, e, t, false, ev_layer, ev_e);
+      if (lane == 0) {
+        sm->out.pref[n_pref] = (uint8_t)e;
+        sm->out.pref_slot[n_pref] = (int8_t)(slot >= 0 ? slot : -1);
+      }
+      ++n_pref;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      if (t > st->pcie_free) st->pcie_free = t;
+      st->q_valid = 1;
+      st->q_layer = tl;
+      st->q_it = tit;
+      st->q_n = qn;
+      st->q_issued = issued;
+      for (uint32_t i = 0; i < qn; ++i) st->q_e[i] = qe[i];
+      st->c.issued += n_pref;
+      st->c.prefetch += n_pref;
+      sm->out.pref_layer = tl;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    sm->out.n_pref = n_pref;
+    sm->out.completion = completion;
+    sm->out.resident_done = resident_done;
+    st->now = completion;
+  }
+  __syncwarp();
+
+  // write back the staged layer state
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(ls);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(&cx.layers[layer]);
+    for (uint32_t i = lane; i < sizeof(LayerState) / 8; i += 32) dst[i] = src[i];
+  }
+
+  // per-step decision record
+  if (rec_out) {
+    if (lane == 0) {
+      rec_out->it = it;
+      rec_out->layer = layer;
+      rec_out->B = B;
+      rec_out->mask_before = mask;
+      rec_out->completion = completion;
+      rec_out->n_load = (uint8_t)n_load;
+      rec_out->n_cpu = (uint8_t)n_cpu;
+      rec_out->n_pref = (uint8_t)n_pref;
+      rec_out->n_evict = (uint8_t)(sm->out.n_evict < 2 * kMaxE ? sm->out.n_evict : 2 * kMaxE);
+    }
+    for (uint32_t i = lane; i < n_load; i += 32) rec_out->load[i] = sm->out.load[i];
+    for (uint32_t i = lane; i < n_cpu; i += 32) rec_out->cpu[i] = sm->out.cpu[i];
+    for (uint32_t i = lane; i < n_pref; i += 32) rec_out->pref[i] = sm->out.pref[i];
+    for (uint32_t i = lane; i < sm->out.n_evict && i < 2 * kMaxE; i += 32) {
+      rec_out->ev_layer[i] = ev_layer[i];
+      rec_out->ev_e[i] = ev_e[i];
+    }
+    for (uint32_t t = lane; t < B; t += 32) {
+      TokRec& tr = tok_out[t];
+      tr.n_sel = sm->nsel[t];
+      tr.n_sub = sm->nsub[t];
+      tr.n_kept = sm->nkept[t];
+      for (uint32_t i = 0; i < sm->nsel[t]; ++i) tr.sel[i] = sm->sel[t][i];
+      for (uint32_t i = 0; i < sm->nsub[t]; ++i) { tr.sub_d[i] = sm->sub_d[t][i]; tr.sub_c[i] = sm->sub_c[t][i]; }
+      for (uint32_t i = 0; i < sm->nkept[t]; ++i) tr.kept[i] = sm->kept[t][i];
+    }
+  }
+  __syncwarp();
+}
+
+}  // namespace moeb
