@@ -271,3 +271,78 @@ def simulate(cfg: Config, scores, pred=None, has_pred=None, steps=False):
         return json.loads(_take_str(j))
     finally:
         lib().moeb_result_free(r)
+
+
+MODEL_LOG_STEPS = 1
+
+# Model presets (dimensions of the BASELINE.json configs)
+DSV2_LITE = dict(d_model=2048, ffn=1408, shared_ffn=2816, shared_gate=0, renormalize=0, routed_scale=1.0)
+QWEN15_MOE = dict(d_model=2048, ffn=1408, shared_ffn=5632, shared_gate=1, renormalize=0, routed_scale=1.0)
+MIXTRAL_8X7B = dict(d_model=4096, ffn=14336, shared_ffn=0, shared_gate=0, renormalize=1, routed_scale=1.0)
+
+
+class Stack:
+    """The MoE decode stack (moeb_create / moeb_step): bf16 device tensors in/out."""
+
+    def __init__(self, cfg: Config, d_model, ffn, shared_ffn=0, shared_gate=0, renormalize=0,
+                 routed_scale=1.0, weight_seed=7, log_steps=False, device=0, weights_host=None):
+        m = Model(d_model=d_model, ffn=ffn, shared_ffn=shared_ffn, shared_gate=shared_gate,
+                  renormalize=renormalize, routed_scale=routed_scale, weight_seed=weight_seed,
+                  max_batch=cfg.batch, flags=MODEL_LOG_STEPS if log_steps else 0)
+        h = C.c_void_p()
+        self._weights = weights_host  # keep alive
+        wp = None if weights_host is None else C.c_void_p(weights_host.ctypes.data)
+        check(lib().moeb_create(C.byref(cfg), C.byref(m), wp, C.c_int(device), C.byref(h)))
+        self.h, self.cfg, self.model = h, cfg, m
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().moeb_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def set_logits_trace(self, logits, total_iterations=0):
+        """logits: float32 [n_steps, L, B, E] numpy array or torch tensor (host or device)."""
+        if hasattr(logits, "data_ptr"):
+            ptr, n = logits.data_ptr(), logits.shape[0]
+        else:
+            logits = np.ascontiguousarray(logits, dtype=np.float32)
+            self._trace = logits
+            ptr, n = logits.ctypes.data, logits.shape[0]
+        check(lib().moeb_set_logits_trace(self.h, C.c_void_p(ptr), C.c_uint64(n), C.c_uint64(total_iterations)))
+
+    def step(self, x_ptr, y_ptr, B, stream=0):
+        check(lib().moeb_step(self.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_uint32(B), C.c_void_p(stream)))
+
+    def sync(self):
+        check(lib().moeb_sync(self.h))
+
+    def metrics(self):
+        m = Metrics()
+        check(lib().moeb_get_metrics(self.h, C.byref(m)))
+        return m.as_dict()
+
+    def decisions(self):
+        j = C.c_void_p()
+        check(lib().moeb_get_decisions_json(self.h, C.byref(j)))
+        return json.loads(_take_str(j))
+
+    def scores(self):
+        n = C.c_size_t()
+        check(lib().moeb_get_scores(self.h, None, C.c_size_t(0), C.byref(n)))
+        out = np.zeros(n.value, dtype=np.float32)
+        check(lib().moeb_get_scores(self.h, out.ctypes.data_as(C.POINTER(C.c_float)), C.c_size_t(n.value),
+                                    C.byref(n)))
+        return out
+
+    def io_stats(self):
+        s = IoStats()
+        check(lib().moeb_get_io_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in IoStats._fields_}
+
+    def layer_outputs(self):
+        L, B, d = self.cfg.num_layers, self.cfg.batch, self.model.d_model
+        out = np.zeros(L * B * d, dtype=np.float32)
+        check(lib().moeb_get_layer_outputs(self.h, out.ctypes.data_as(C.POINTER(C.c_float)), C.c_size_t(out.size)))
+        return out.reshape(L, B, d)

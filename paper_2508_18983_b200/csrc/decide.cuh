@@ -505,7 +505,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     }
     sc->ndm = n;
     uint32_t nr = 0;
-    for (uint64_t m = res_sel; m; m &= m - 1) sm->out.res[nr++] = (uint8_t)(__ffsll((long long)m) - 1);
+    for (uint64_t m = res_sel; m; m &= m - 1) {
+      const uint32_t e = __ffsll((long long)m) - 1;
+      sm->out.res_slot[nr] = ls->slot_of[e];
+      sm->out.res[nr++] = (uint8_t)e;
+    }
     sm->out.n_res = nr;
     sm->out.mask_before = mask;
     for (uint32_t e = 0; e < E; ++e) sm->out.cnt[e] = sc->cnt[e];

@@ -69,6 +69,8 @@ struct EngineState {
   Counters c;
   uint32_t next_copy;              // upload id allocator (stack mode)
   uint32_t err;                    // sticky device error (1 config, 4 logic)
+  uint64_t it;                     // decode iteration (stack mode)
+  uint64_t seq;                    // layer-step sequence number (stack mode)
 };
 
 // Log records (layouts == moeb_task / moeb_window / moeb_eviction).
@@ -126,6 +128,8 @@ struct StepOut {
   uint8_t def_e[kMaxE];
   int8_t def_slot[kMaxE];    // admitted at completion; staging -> slot copy
   uint8_t res[kMaxE];        // resident (hit) experts, ascending
+  int8_t res_slot[kMaxE];    // their slots at route time (a completion-time
+                             // deferred admission may evict a hit afterwards)
   uint32_t pref_layer;
   uint64_t mask_before, completion, resident_done;
   uint16_t cnt[kMaxE];       // tokens per distinct selected expert
