@@ -1,0 +1,512 @@
+#!/usr/bin/env python3
+"""Bench: MoE decode ms/token + expert cache hit rate, DeepSeek-V2-Lite shape.
+
+Workload (BASELINE.json configs[1]): the 26-layer DeepSeek-V2-Lite MoE stack
+(64 routed experts top-6 + 2 shared, d=2048, ffn=1408), batch-1 decode of a
+512-token synthetic stream, expert cache capped at 25% (16 of 64 experts per
+layer), full scheduler stages CE+ER+Pre+BA at alpha=0.25 — plus the same
+stream with substitution off (ER off) as an ablation.
+
+A "step" is one decoded token through all 26 layers: per layer the router
+gate kernel, the device decision kernel (routing / substitution / cache /
+prefetch / balance, bit-exact vs the reference), and the persistent grouped
+SwiGLU FFN kernel; expert misses are uploaded from pinned host memory over
+PCIe on the copy stream while resident experts compute.
+
+Data: synthetic. Router logits are ln(s) of the reference's generate_trace
+(trace.cpp:106, seed 7 + rank) so the softmax reproduces the reference's
+skewed, temporally persistent routing; hidden states are an AR(1) stream;
+weights are counter-based random (uniform +-sqrt(3/fan_in), bf16).
+
+Timed region: W warm-up tokens (untimed, positions 0..W-1), then exactly K
+tokens (positions W..W+K-1), bracketed by barrier + synchronize, CUDA events
+on the stack's stream, max over ranks. Every step streams ~140 MB of expert
+weights from HBM and hundreds of MB over PCIe, far above the 126 MB L2, so no
+L2 flush is needed ("l2": "inputs > L2").
+
+--impl reference: the reference's CPU path on this host (decisions by the
+reference library compiled from /root/reference into oracle/_ref, layer
+arithmetic by the CPU fp32 port oracle/cpu_moe.c over all host threads).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+# DeepSeek-V2-Lite MoE stack (configs[1]); CE+ER+Pre+BA, alpha 0.25, c = 25% of E
+CFG = dict(num_layers=26, experts=64, top_k=6, batch=1, alpha=0.25, slots=16, window=16, seed=7,
+           ce=1, er=1, pre=1, ba=1)
+MODEL = dict(d_model=2048, ffn=1408, shared_ffn=2816, shared_gate=0, renormalize=0, routed_scale=1.0)
+TOKENS = 512
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def ar1_hidden(T, B, d, seed):
+    rng = np.random.default_rng(seed)
+    x = np.zeros((T, B, d), dtype=np.float32)
+    prev = rng.standard_normal((B, d)).astype(np.float32)
+    for t in range(T):
+        prev = 0.9 * prev + np.float32(np.sqrt(0.19)) * rng.standard_normal((B, d)).astype(np.float32)
+        x[t] = prev
+    return x
+
+
+def measure_pcie_gbs(torch):
+    """Pinned H2D copy-engine bandwidth: 256 MB, best of 10 (the PCIe roofline)."""
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8).pin_memory()
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    best = 1e9
+    with torch.cuda.stream(s):
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            d.copy_(h, non_blocking=True)
+            b.record(s)
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+    del h, d
+    return n / best / 1e6
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2508_18983_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    W, K = args.warmup, args.steps
+    T = W + K
+    L, E, B, d = CFG["num_layers"], CFG["experts"], CFG["batch"], MODEL["d_model"]
+    seed = 7 + rank  # independent decode stream per GPU (stream partitioning, no collective)
+    scores = capi.generate_trace(L, E, B, T, seed)
+    logits = capi.trace_logits(scores)
+    x_host = ar1_hidden(T, B, d, seed)
+    x_dev = torch.from_numpy(x_host).to(torch.bfloat16).cuda()
+    x_pin = x_dev.cpu().pin_memory()
+    y_dev = torch.empty((B, d), dtype=torch.bfloat16, device="cuda")
+    y_pin = torch.empty((T, B, d), dtype=torch.bfloat16).pin_memory()
+
+    cfg = capi.Config.make(**CFG)
+    t0 = time.time()
+    stack = capi.Stack(cfg, weight_seed=7, time_kernels=True, device=local, **MODEL)
+    create_s = time.time() - t0
+    stack.set_logits_trace(logits, T)
+    s_ptr = stack.stream()
+    s = torch.cuda.ExternalStream(s_ptr)
+
+    def run_steps(lo, hi, e2e=False):
+        for i in range(lo, hi):
+            if e2e:
+                xi = x_dev[i]
+                xi.copy_(x_pin[i], non_blocking=True)  # H2D of this step's input
+                stack.step(xi.data_ptr(), y_dev.data_ptr(), B, stream=s_ptr)
+                y_pin[i].copy_(y_dev, non_blocking=True)  # D2H of this step's output
+            else:
+                stack.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s_ptr)
+
+    # ---- device-resident inputs (value)
+    with torch.cuda.stream(s):
+        run_steps(0, W)
+        stack.sync()
+        m0 = stack.metrics()
+        stack.reset_kernel_stats()
+        barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(s)
+        run_steps(W, T)
+        ev1.record(s)
+        ev1.synchronize()
+        stack.sync()
+        barrier()
+        clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    m1 = stack.metrics()
+    io = stack.io_stats()
+    ks = stack.kernel_stats()
+    ms_max = max_over_ranks(ms)
+
+    # ---- end to end through the C-ABI with host buffers (e2e)
+    stack.reset()
+    with torch.cuda.stream(s):
+        run_steps(0, W, e2e=True)
+        stack.sync()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        run_steps(W, T, e2e=True)
+        e1.record(s)
+        e1.synchronize()
+        stack.sync()
+        barrier()
+    e2e_ms_max = max_over_ranks(e0.elapsed_time(e1))
+
+    # ---- substitution off (ER off), same stream and weights (ablation)
+    abl = None
+    if not args.no_ablation:
+        cfg2 = capi.Config.make(**dict(CFG, er=0))
+        pool_ptr, _ = stack.host_pool()
+        st2 = capi.Stack(cfg2, weight_seed=7, device=local, weights_host=(pool_ptr, stack), **MODEL)
+        st2.set_logits_trace(logits, T)
+        s2p = st2.stream()
+        s2 = torch.cuda.ExternalStream(s2p)
+        with torch.cuda.stream(s2):
+            for i in range(W):
+                st2.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s2p)
+            st2.sync()
+            a0m = st2.metrics()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(s2)
+            for i in range(W, T):
+                st2.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s2p)
+            a1.record(s2)
+            a1.synchronize()
+            st2.sync()
+        a1m = st2.metrics()
+        sel = a1m["selections"] - a0m["selections"]
+        abl = {"er_off": {"ms_per_token": round(a0.elapsed_time(a1) / K, 4),
+                          "hit_rate": round((a1m["hits"] - a0m["hits"]) / max(sel, 1), 4),
+                          "demand_loads": a1m["demand_loads"] - a0m["demand_loads"],
+                          "streamed": a1m["cpu_computed"] - a0m["cpu_computed"]}}
+        st2.close()
+
+    # ---- FFN kernel roofline on the all-resident configuration (no uploads)
+    hbm_peak, peak_kind = peaks()
+    cfg3 = capi.Config.make(**dict(CFG, slots=E))
+    pool_ptr, _ = stack.host_pool()
+    st3 = capi.Stack(cfg3, weight_seed=7, device=local, weights_host=(pool_ptr, stack), time_kernels=True, **MODEL)
+    st3.set_logits_trace(logits, T)
+    s3p = st3.stream()
+    n3 = min(64, T)
+    for i in range(8):
+        st3.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
+    st3.sync()
+    st3.reset_kernel_stats()
+    h0 = time.time()
+    for i in range(8, 8 + n3):
+        st3.step(x_dev[i % T].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
+    st3.sync()
+    allhit_wall = time.time() - h0
+    k3 = st3.kernel_stats()
+    st3.close()
+    ffn_gbs = k3["ffn_bytes"] / (k3["ffn_ms"] * 1e-3) / 1e9
+    per_launch_bytes = k3["ffn_bytes"] / max(k3["ffn_launches"], 1)
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_ffn_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    allhit_ms_token = (k3["route_ms"] + k3["ffn_ms"]) / n3
+
+    # ---- path roofline: T_roof = max(B_hbm / BW_hbm, B_pcie / BW_pcie) per token
+    pcie_peak = measure_pcie_gbs(torch)
+    tokens = K
+    b_hbm = (ks["ffn_bytes"] + ks["route_bytes"]) / tokens
+    b_pcie = io["h2d_bytes"] / tokens
+    t_roof = max(b_hbm / (hbm_peak * 1e9), b_pcie / (pcie_peak * 1e9)) * 1e3
+    ms_tok = ms / K
+    sel = m1["selections"] - m0["selections"]
+    hit = (m1["hits"] - m0["hits"]) / max(sel, 1)
+
+    total_tokens = sum_over_ranks(float(K))
+    value = ms_max / (total_tokens / world) / world  # whole-job ms per token across all GPUs
+    result = {
+        "metric": "MoE decode ms/token + expert cache hit rate, DeepSeek-V2-Lite shape",
+        "value": round(value, 4),
+        "unit": "ms/token",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": round(ms_max / K, 4),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16 weights, fp32 accumulate; fp64 decisions",
+        "data": "synthetic: reference generate_trace router logits (seed 7+rank), AR(1) hidden states, "
+                "counter-based random bf16 weights",
+        "config": {"workload": "DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode, 512-token stream, "
+                               "cache 16/64 experts per layer, CE+ER+Pre+BA alpha=0.25",
+                   "layers": L, "experts": E, "top_k": CFG["top_k"], "shared_ffn": MODEL["shared_ffn"],
+                   "d_model": d, "ffn": MODEL["ffn"], "global_batch": B * world, "tokens_per_gpu": T,
+                   "slots_per_layer": CFG["slots"], "parallelism": f"stream-partitioned x{world} (no collective)",
+                   "l2": "inputs > L2 (>=140 MB weights per step)"},
+        "hit_rate": round(hit, 4),
+        "metrics_timed": {"demand_loads": m1["demand_loads"] - m0["demand_loads"],
+                          "streamed_ba": m1["cpu_computed"] - m0["cpu_computed"],
+                          "prefetch_loads": m1["prefetch_loads"] - m0["prefetch_loads"],
+                          "substitutions": m1["substitutions"] - m0["substitutions"],
+                          "substitution_ratio": round((m1["substitutions"] - m0["substitutions"]) /
+                                                      max(1, (m1["substitutions"] - m0["substitutions"]) +
+                                                          (m1["low_score_kept"] - m0["low_score_kept"])), 4)},
+        "e2e": {"value": round(e2e_ms_max / K, 4), "unit": "ms/token", "h2d_bytes_per_step": B * d * 2,
+                "d2h_bytes_per_step": B * d * 2},
+        "roofline": {"bound": "hbm", "kernel": "ffn_kernel (all-resident pass, no uploads)",
+                     "achieved": round(ffn_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(ffn_gbs / hbm_peak, 4), "traffic": traffic,
+                     "algorithmic_bytes_per_launch": int(per_launch_bytes), "peak_source": peak_kind,
+                     "allhit_ms_per_token": round(allhit_ms_token, 4)},
+        "path_roofline": {"t_roof_ms": round(t_roof, 4), "t_measured_ms": round(ms_tok, 4),
+                          "frac": round(t_roof / ms_tok, 4), "hbm_bytes_per_token": int(b_hbm),
+                          "pcie_bytes_per_token": int(b_pcie), "pcie_peak_gbs": round(pcie_peak, 2),
+                          "pcie_achieved_gbs_copy_stream": round(io["h2d_bytes"] / max(io["copy_ms"], 1e-9) / 1e6, 2),
+                          "pcie_busy_frac": round(io["copy_ms"] / ms, 4),
+                          "bound": "pcie" if b_pcie / pcie_peak > b_hbm / hbm_peak else "hbm"},
+        "kernel_ms_per_token": {"gate_decide": round(ks["route_ms"] / K, 4),
+                                "ffn_incl_upload_waits": round(ks["ffn_ms"] / K, 4),
+                                "allhit_gate_decide": round(k3["route_ms"] / n3, 4),
+                                "allhit_ffn": round(k3["ffn_ms"] / n3, 4)},
+        "gpu_launches": int(2 * L * K),
+        "clocks": clk,
+        "create_s": round(create_s, 2),
+    }
+    if abl:
+        result["ablation"] = abl
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(scores, x_host, args.cpu_sample_tokens)
+    stack.close()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- CPU path
+
+def cpu_path(scores, x_host, n_tokens, nthreads):
+    """The reference CPU path: reference-library decisions + CPU fp32 layer arithmetic.
+
+    Decisions: the reference's simulate() (oracle/_ref, compiled from
+    /root/reference) when present, else the oracle's C port; at batch 1 the
+    per-layer selections are the windows' selected sets. Arithmetic: oracle
+    cpu_moe.c over bf16 weights in host RAM, every host thread.
+    Returns (ms_per_token, kind, cores, sample).
+    """
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import pyoracle as po
+
+    L, E, B = CFG["num_layers"], CFG["experts"], CFG["batch"]
+    d, F, S = MODEL["d_model"], MODEL["ffn"], MODEL["shared_ffn"]
+    T = scores.shape[0]
+    cfg = po.SimCfg(**{k: v for k, v in CFG.items()})
+    use_ref = po.ref() is not None
+    t0 = time.perf_counter()
+    out = (po.ref_simulate if use_ref else po.simulate)(cfg, scores, timeline=True)
+    dec_s = time.perf_counter() - t0
+    dec_ms_token = dec_s * 1e3 / T
+    wins = {(w[0], w[1]): w[5] for w in out["windows"]}
+
+    cm = C.CDLL(os.path.join(REPO, "oracle", "libcpumoe.so"))
+    cm.cpu_synth.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int]
+    cm.cpu_moe_layer.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_int]
+    seed = 7
+
+    def tid(l, e, m):
+        return (l << 20) | (e << 4) | m
+
+    cache = {}
+
+    def tensor(key, tensor_id, n, fan_in):
+        if key not in cache:
+            a = np.empty(n, dtype=np.uint16)
+            cm.cpu_synth(seed, tensor_id, n, fan_in, a.ctypes.data, nthreads)
+            cache[key] = a
+        return cache[key]
+
+    def expert(l, e):
+        key = ("e", l, e)
+        if key not in cache:
+            a = np.empty(3 * F * d, dtype=np.uint16)
+            for m in range(3):
+                cm.cpu_synth(seed, tid(l, e, m), F * d, d if m < 2 else F, a[m * F * d:].ctypes.data, nthreads)
+            cache[key] = a
+        return cache[key]
+
+    # weights in host RAM before timing (the CPU path has no PCIe)
+    sample = list(range(T - n_tokens, T))
+    for l in range(L):
+        tensor(("r", l), (l << 20) | (0xFFFF << 4), E * d, d)
+        sh = np.empty(3 * S * d, dtype=np.uint16)
+        for m in range(3):
+            cm.cpu_synth(seed, (l << 20) | (0xFFFE << 4) | m, S * d, d if m < 2 else S, sh[m * S * d:].ctypes.data,
+                         nthreads)
+        cache[("s", l)] = sh
+        for it in sample:
+            for e in wins[(it, l)]:
+                expert(l, e)
+    logits = np.zeros(E, dtype=np.float32)
+    y = np.zeros(d, dtype=np.float32)
+    t0 = time.perf_counter()
+    for it in sample:
+        x = np.ascontiguousarray(x_host[it, 0]).astype(np.float32)
+        xb = (x.view(np.uint32) + np.uint32(0x7FFF) + ((x.view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
+        for l in range(L):
+            sel = wins[(it, l)]
+            ptrs = (C.c_void_p * len(sel))(*[expert(l, e).ctypes.data for e in sel])
+            wts = np.array([scores[it, l, 0, e] for e in sel], dtype=np.float32)
+            xn = np.empty(d, dtype=np.uint16)
+            cm.cpu_moe_layer(xb.ctypes.data, d, F, S, E, cache[("r", l)].ctypes.data, cache[("s", l)].ctypes.data,
+                             None, ptrs, wts.ctypes.data, len(sel), logits.ctypes.data, y.ctypes.data,
+                             xn.ctypes.data, nthreads)
+            xb = xn
+    arith_s = time.perf_counter() - t0
+    ms_token = arith_s * 1e3 / len(sample) + dec_ms_token
+    kind = "reference" if use_ref else "port"
+    sample_desc = (f"decisions: {'reference simulate() (oracle/_ref)' if use_ref else 'oracle C port'} over all "
+                   f"{T} tokens ({dec_ms_token:.3f} ms/token, 1 thread); arithmetic: oracle/cpu_moe.c fp32 over "
+                   f"bf16 host weights, last {len(sample)} tokens x {L} layers ({arith_s * 1e3 / len(sample):.1f} "
+                   f"ms/token, {nthreads} threads)")
+    return ms_token, kind, nthreads, sample_desc
+
+
+def cpu_baseline(scores, x_host, n_tokens):
+    nthreads = os.cpu_count() or 1
+    ms, kind, cores, sample = cpu_path(scores, x_host, n_tokens, nthreads)
+    return {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    L, E, B, d = CFG["num_layers"], CFG["experts"], CFG["batch"], MODEL["d_model"]
+    W, K = args.warmup, args.steps
+    T = W + K
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import pyoracle as po
+    scores = po.generate_trace(L, E, B, T, 7, use_ref=po.ref() is not None)
+    x_host = ar1_hidden(T, B, d, 7)
+    nthreads = os.cpu_count() or 1
+    ms, kind, cores, sample = cpu_path(scores, x_host, min(args.cpu_sample_tokens, K), nthreads)
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "MoE decode ms/token + expert cache hit rate, DeepSeek-V2-Lite shape",
+        "value": round(ms, 3), "unit": "ms/token", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": K, "warmup": W, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 compute over bf16 weights; fp64 decisions", "data": "synthetic",
+        "config": {"workload": "DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode, 512-token stream, "
+                               "cache 16/64 experts per layer, CE+ER+Pre+BA alpha=0.25"},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": round(ms, 3), "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=TOKENS - 16)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-ablation", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=12)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -66,7 +66,8 @@ typedef struct moeb_model {
   uint32_t flags;        /* MOEB_MODEL_* */
 } moeb_model;
 
-#define MOEB_MODEL_LOG_STEPS 1u /* record per-step decision records */
+#define MOEB_MODEL_LOG_STEPS 1u     /* record per-step decision records */
+#define MOEB_MODEL_TIME_KERNELS 2u  /* CUDA-event timing of every gate/decide/FFN launch */
 
 typedef struct moeb_engine moeb_engine; /* decision engine only (simulate path) */
 typedef struct moeb_stack moeb_stack;   /* full MoE decode stack */
@@ -218,6 +219,28 @@ typedef struct moeb_io_stats {
 int moeb_get_io_stats(moeb_stack* s, moeb_io_stats* st);
 /* Device buffers for tests: fp32 layer outputs of the last step ([L][B][d]) */
 int moeb_get_layer_outputs(moeb_stack* s, float* out, size_t cap);
+/* Reset the decision state and cache contents to the post-create state
+ * (iteration 0), keeping weights and the pinned pool. */
+int moeb_reset(moeb_stack* s);
+/* The stack's own compute stream (cudaStream_t). */
+void* moeb_stream(moeb_stack* s);
+/* Per-kernel CUDA-event totals (MOEB_MODEL_TIME_KERNELS) and algorithmic
+ * bytes (weights + activations each launch must move at least once). */
+typedef struct moeb_kernel_stats {
+  double route_ms, ffn_ms;        /* route = fused router gate + decision launch */
+  uint64_t route_launches, ffn_launches;
+  uint64_t route_bytes, ffn_bytes, ffn_planned;
+  uint64_t prof_ns[16];           /* device phase timers of the decision launch */
+} moeb_kernel_stats;
+int moeb_get_kernel_stats(moeb_stack* s, moeb_kernel_stats* out);
+int moeb_reset_kernel_stats(moeb_stack* s);
+
+/* generate_trace (trace.hpp:45 / trace.cpp:106-151): synthetic skewed gate
+ * scores, [iters][L][B][E] fp64 (workload synthesis, host side). */
+int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction, double hot_mass,
+                        double persistence, double concentration, uint64_t iters, uint64_t seed,
+                        double* out);
+
 /* Pinned host pool pointer and per-expert bytes (for the CPU oracle). */
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes);
 

@@ -285,13 +285,20 @@ class Stack:
     """The MoE decode stack (moeb_create / moeb_step): bf16 device tensors in/out."""
 
     def __init__(self, cfg: Config, d_model, ffn, shared_ffn=0, shared_gate=0, renormalize=0,
-                 routed_scale=1.0, weight_seed=7, log_steps=False, device=0, weights_host=None):
+                 routed_scale=1.0, weight_seed=7, log_steps=False, device=0, weights_host=None,
+                 time_kernels=False):
+        flags = (MODEL_LOG_STEPS if log_steps else 0) | (2 if time_kernels else 0)
         m = Model(d_model=d_model, ffn=ffn, shared_ffn=shared_ffn, shared_gate=shared_gate,
                   renormalize=renormalize, routed_scale=routed_scale, weight_seed=weight_seed,
-                  max_batch=cfg.batch, flags=MODEL_LOG_STEPS if log_steps else 0)
+                  max_batch=cfg.batch, flags=flags)
         h = C.c_void_p()
-        self._weights = weights_host  # keep alive
-        wp = None if weights_host is None else C.c_void_p(weights_host.ctypes.data)
+        self._weights = weights_host  # keep alive (numpy array, or (int pointer, owner))
+        if weights_host is None:
+            wp = None
+        elif isinstance(weights_host, tuple):
+            wp = C.c_void_p(weights_host[0])
+        else:
+            wp = C.c_void_p(weights_host.ctypes.data)
         check(lib().moeb_create(C.byref(cfg), C.byref(m), wp, C.c_int(device), C.byref(h)))
         self.h, self.cfg, self.model = h, cfg, m
 
@@ -346,3 +353,61 @@ class Stack:
         out = np.zeros(L * B * d, dtype=np.float32)
         check(lib().moeb_get_layer_outputs(self.h, out.ctypes.data_as(C.POINTER(C.c_float)), C.c_size_t(out.size)))
         return out.reshape(L, B, d)
+
+MODEL_TIME_KERNELS = 2
+
+
+class KernelStats(C.Structure):
+    _fields_ = [("route_ms", C.c_double), ("ffn_ms", C.c_double),
+                ("route_launches", C.c_uint64), ("ffn_launches", C.c_uint64),
+                ("route_bytes", C.c_uint64), ("ffn_bytes", C.c_uint64), ("ffn_planned", C.c_uint64),
+                ("prof_ns", C.c_uint64 * 16)]
+
+
+def generate_trace(L, E, B, iters, seed, hot_fraction=0.125, hot_mass=0.8, persistence=0.92, concentration=1.5):
+    """generate_trace (trace.cpp:106-151) via the product library -> float64 [iters, L, B, E]."""
+    out = np.zeros((iters, L, B, E), dtype=np.float64)
+    check(lib().moeb_generate_trace(C.c_uint32(L), C.c_uint32(E), C.c_uint32(B), C.c_double(hot_fraction),
+                                    C.c_double(hot_mass), C.c_double(persistence), C.c_double(concentration),
+                                    C.c_uint64(iters), C.c_uint64(seed), _d(out)))
+    return out
+
+
+def trace_logits(scores):
+    """Router logits whose softmax reproduces a score trace: ln(s) in fp32."""
+    with np.errstate(divide="ignore"):
+        return np.log(scores).astype(np.float32)
+
+
+def _stack_extra():
+    L = lib()
+    L.moeb_stream.restype = C.c_void_p
+
+
+class _StackExt:
+    def reset(self):
+        check(lib().moeb_reset(self.h))
+
+    def stream(self):
+        lib().moeb_stream.restype = C.c_void_p
+        return lib().moeb_stream(self.h) or 0
+
+    def kernel_stats(self):
+        s = KernelStats()
+        check(lib().moeb_get_kernel_stats(self.h, C.byref(s)))
+        d = {f: getattr(s, f) for f, _ in KernelStats._fields_}
+        d["prof_ns"] = list(s.prof_ns)
+        return d
+
+    def reset_kernel_stats(self):
+        check(lib().moeb_reset_kernel_stats(self.h))
+
+    def host_pool(self):
+        p, n = C.c_void_p(), C.c_size_t()
+        check(lib().moeb_get_host_pool(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+
+for _n, _f in vars(_StackExt).items():
+    if not _n.startswith("__"):
+        setattr(Stack, _n, _f)

@@ -12,18 +12,30 @@
 
 namespace moeb {
 
+// Pointers may be global or shared (callers stage hot state in smem). When
+// the prefetch target is the executing layer (L == 1), tls == ls and
+// thist == hist_l.
 struct StepCtx {
   const DevCfg* cfg;
-  EngineState* st;       // global
-  LayerState* layers;    // global [L]
-  double* hist;          // global [L][window][E]
+  EngineState* st;
+  LayerState* ls;        // executing layer
+  double* hist_l;        // its score ring [window][E]
+  LayerState* tls;       // prefetch target layer
+  double* thist;         // its score ring
   const Logs* logs;      // nullable
   uint64_t it;
   uint32_t layer;
   uint32_t has_target;   // prefetch target exists (pipeline.cpp:401-409)
   uint32_t target_layer;
   uint64_t target_it;
+  uint64_t* prof;        // nullable: phase timers (globaltimer deltas)
 };
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Extra shared state for the prefetch target's classification.
 struct NextSmem {
@@ -46,7 +58,10 @@ __device__ __forceinline__ double window_average(const LayerState* ls, const dou
 }
 
 // cache.cpp:81-106 (warp-collective; every lane returns the victim or -1).
-__device__ inline int try_evict_warp(const LayerState* ls, const double* hist_l, const DevCfg& cfg) {
+// avg: optional precomputed window averages of this layer (the history does
+// not change between a step's record_scores and its admissions).
+__device__ inline int try_evict_warp(const LayerState* ls, const double* hist_l, const DevCfg& cfg,
+                                     const double* avg = nullptr) {
   const int lane = lane_id();
   const uint64_t cand = ls->mask & ~ls->shield;
   if (cfg.policy == 0) {
@@ -54,7 +69,7 @@ __device__ inline int try_evict_warp(const LayerState* ls, const double* hist_l,
     uint32_t idx = 0xffffffffu;
     for (uint32_t e = lane; e < cfg.E; e += 32) {
       if (!has(cand, e)) continue;
-      const double a = window_average(ls, hist_l, cfg.window, cfg.E, e);
+      const double a = avg ? avg[e] : window_average(ls, hist_l, cfg.window, cfg.E, e);
       if (idx == 0xffffffffu || a < key) { key = a; idx = e; }
     }
     warp_argmin_d(key, idx);
@@ -74,14 +89,15 @@ __device__ inline int try_evict_warp(const LayerState* ls, const double* hist_l,
 // cache.cpp:136-156. Returns 0 ok, 3 CacheError (all shielded), 4 already
 // resident. victim/slot are -1 when none. Warp-collective.
 __device__ inline int admit_warp(LayerState* ls, const double* hist_l, const DevCfg& cfg,
-                                 uint32_t e, uint64_t now, int& victim, int& slot) {
+                                 uint32_t e, uint64_t now, int& victim, int& slot,
+                                 const double* avg = nullptr) {
   const int lane = lane_id();
   victim = -1;
   slot = -1;
   if (has(ls->mask, e)) return 4;
   if (cfg.slots == 0) return 0;  // zero-slot cache: loads pass through
   if (ls->n_res >= cfg.slots) {
-    const int v = try_evict_warp(ls, hist_l, cfg);
+    const int v = try_evict_warp(ls, hist_l, cfg, avg);
     if (v < 0) return 3;
     victim = v;
     slot = ls->slot_of[v];
@@ -333,13 +349,13 @@ __device__ inline void log_eviction(const Logs* lg, StepOut* out, uint64_t now, 
 // admit_or_defer (pipeline.cpp:93-108), warp-collective. Returns the slot
 // (>= 0), -1 when nothing was inserted, -2 when the admission was deferred.
 __device__ inline int admit_or_defer(const StepCtx& cx, DecideSmem* sm, LayerState* ls,
-                                     uint32_t layer, uint32_t e, uint64_t now, bool shield_it,
-                                     uint8_t* ev_layer, uint8_t* ev_e) {
+                                     const double* hist, uint32_t layer, uint32_t e, uint64_t now,
+                                     bool shield_it, uint8_t* ev_layer, uint8_t* ev_e,
+                                     const double* avg) {
   const DevCfg& cfg = *cx.cfg;
   if (has(ls->mask, e)) return ls->slot_of[e];
   int victim, slot;
-  const int rc = admit_warp(ls, cx.hist + (size_t)layer * cfg.window * cfg.E, cfg, e, now,
-                            victim, slot);
+  const int rc = admit_warp(ls, hist, cfg, e, now, victim, slot, avg);
   if (rc == 3) {
     if (lane_id() == 0) sm->def_e[sm->n_def++] = e;
     __syncwarp();
@@ -373,12 +389,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   const uint32_t E = cfg.E, B = cfg.B, k = cfg.k, layer = cx.layer;
   const uint64_t it = cx.it;
 
-  // stage the executing layer's state
-  {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(&cx.layers[layer]);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(&sm->ls);
-    for (uint32_t i = tid; i < sizeof(LayerState) / 8; i += blockDim.x) dst[i] = src[i];
-  }
+  const uint32_t nw = blockDim.x >> 5;
+  uint64_t tp = (cx.prof && tid == 0) ? gtimer() : 0;
+  auto mark = [&](int i) {
+    if (cx.prof && tid == 0) { const uint64_t n = gtimer(); cx.prof[i] += n - tp; tp = n; }
+  };
   if (tid == 0) {
     const uint64_t start = st->now;
     // attention + gate (pipeline.cpp:133-145)
@@ -402,24 +417,29 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     sm->out.n_res = 0;
   }
   __syncthreads();
-  const uint64_t mask = sm->ls.mask;  // snapshot the router sees (pipeline.cpp:154-155)
+  const uint64_t mask = cx.ls->mask;  // snapshot the router sees (pipeline.cpp:154-155)
 
   // classify every token (and the prefetch target's tokens) — warp per token
   const bool want_next = cfg.pre && cx.has_target;
-  for (uint32_t t = warp; t < B; t += kWarps) {
+  const uint32_t jobs = want_next ? 2 * B : B;
+  for (uint32_t j = warp; j < jobs; j += nw) {
     uint64_t a, tp, lw, al;
     double b, T, L, R;
-    classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R);
-    if (lane == 0) {
-      sm->act[t] = a; sm->top[t] = tp; sm->low[t] = lw; sm->alt[t] = al;
-      sm->beta[t] = b; sm->thT[t] = T; sm->thL[t] = L; sm->thR[t] = R;
-    }
-    if (want_next) {
+    if (j < B) {
+      const uint32_t t = j;
+      classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R);
+      if (lane == 0) {
+        sm->act[t] = a; sm->top[t] = tp; sm->low[t] = lw; sm->alt[t] = al;
+        sm->beta[t] = b; sm->thT[t] = T; sm->thL[t] = L; sm->thR[t] = R;
+      }
+    } else {
+      const uint32_t t = j - B;
       classify_warp(sm->ns[t], E, k, cfg.alpha, nx->order[t], a, tp, lw, al, b, T, L, R);
       if (lane == 0) { nx->act[t] = a; nx->top[t] = tp; }
     }
   }
   __syncthreads();
+  mark(4);
 
   if (cfg.er) {
     if (tid == 0) {
@@ -428,14 +448,16 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       sm->C = C;
     }
     __syncthreads();
-    for (uint32_t t = warp; t < B; t += kWarps)
+    for (uint32_t t = warp; t < B; t += nw)
       if (lane == 0) route_token(sm, t, mask, E, k);
     __syncthreads();
-    if (warp == 0) coalesce_warp(sm, B, E, k, mask, sc->cnt);
+    // coalescing is a no-op for a single token: every candidate's batch count
+    // is 0, never above the occupant's (router.cpp:203-228)
+    if (warp == 0 && B > 1) coalesce_warp(sm, B, E, k, mask, sc->cnt);
     __syncthreads();
   } else {
     // plain_top_k (router.cpp:35-39)
-    for (uint32_t t = warp; t < B; t += kWarps) {
+    for (uint32_t t = warp; t < B; t += nw) {
       if (lane == 0) {
         for (uint32_t r = 0; r < k; ++r) sm->sel[t][r] = sm->order[t][r];
         sm->nsel[t] = (uint8_t)k;
@@ -446,6 +468,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     __syncthreads();
   }
 
+  mark(5);
   if (warp != 0) return;  // the rest is order-dependent: warp 0 in lock-step
 
   // ---- hit accounting + batch_of (pipeline.cpp:176-189)
@@ -481,9 +504,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     c.hits += n_hits;
     c.misses += n_sel_total - n_hits;
   }
-  LayerState* ls = &sm->ls;
-  double* hist_l = cx.hist + (size_t)layer * cfg.window * E;
+  LayerState* ls = cx.ls;
+  double* hist_l = cx.hist_l;
   record_scores_warp(ls, hist_l, cfg.window, E, sm->mean);  // pipeline.cpp:191
+  if (cfg.policy == 0)
+    for (uint32_t e = lane; e < E; e += 32) sm->avg[e] = window_average(ls, hist_l, cfg.window, E, e);
 
   // residents: shield + touch; misses -> demand set (pipeline.cpp:196-205)
   const uint64_t route_end = sc->route_end, attn_end = sc->attn_end;
@@ -512,10 +537,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     }
     sm->out.n_res = nr;
     sm->out.mask_before = mask;
-    for (uint32_t e = 0; e < E; ++e) sm->out.cnt[e] = sc->cnt[e];
   }
+  for (uint32_t e = lane; e < E; e += 32) sm->out.cnt[e] = sc->cnt[e];
   __syncwarp();
 
+  mark(6);
   // BA split (pipeline.cpp:207-215)
   uint32_t n_load = 0, n_cpu = 0;
   if (cfg.ba) {
@@ -550,7 +576,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     const uint32_t e = sm->out.load[i];
     if (lane == 0) log_task(cx.logs, R_PCIE, K_DEMAND, (int)layer, e, pcie_t, pcie_t + cfg.t_load, layer, it);
     pcie_t += cfg.t_load;
-    const int slot = admit_or_defer(cx, sm, ls, layer, e, pcie_t, true, ev_layer, ev_e);
+    const int slot = admit_or_defer(cx, sm, ls, hist_l, layer, e, pcie_t, true, ev_layer, ev_e, sm->avg);
     if (lane == 0) sm->out.load_slot[i] = (int8_t)(slot >= 0 ? slot : -1);
     ready[i] = pcie_t;
   }
@@ -604,7 +630,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     if (lane == 0) sm->n_def = 0;
     __syncwarp();
     for (uint32_t i = 0; i < nd; ++i) {
-      const int slot = admit_or_defer(cx, sm, ls, layer, def_copy[i], completion, false, ev_layer, ev_e);
+      const int slot = admit_or_defer(cx, sm, ls, hist_l, layer, def_copy[i], completion, false, ev_layer, ev_e, sm->avg);
       if (lane == 0 && slot >= 0 && sm->out.n_def < kMaxE) {
         sm->out.def_e[sm->out.n_def] = (uint8_t)def_copy[i];
         sm->out.def_slot[sm->out.n_def] = (int8_t)slot;
@@ -614,13 +640,15 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     }
   }
 
+  mark(7);
   // prefetch for the next layer (pipeline.cpp:293-344)
   uint32_t n_pref = 0;
   if (want_next) {
     const uint32_t tl = cx.target_layer;
     const uint64_t tit = cx.target_it;
     const uint64_t gate = completion + cfg.t_attn;
-    LayerState* tls = (tl == layer) ? ls : &cx.layers[tl];
+    LayerState* tls = cx.tls;
+    const double* tavg = nullptr;  // computed on the first prefetch admission
     for (uint32_t e = lane; e < E; e += 32) sm->merged[e] = 0.0;
     __syncwarp();
     uint64_t rs[4] = {st->rng[0], st->rng[1], st->rng[2], st->rng[3]};
@@ -655,7 +683,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       } else {
         const uint32_t n_top = __popcll(ntop);
         if (rng_double(rs) < cfg.p_top && n_top > 0) {
-          const uint32_t pick = (uint32_t)rng_below(rs, n_top);
+          const uint32_t pick = rng_below_small(rs, n_top);
           uint32_t c = 0;
           head = 0;
           for (uint32_t r = 0; r < k; ++r) {
@@ -667,7 +695,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
           const uint64_t lows = nact & ~ntop;
           const uint32_t n_low = __popcll(lows);
           if (rng_double(rs) < cfg.p_active && n_low > 0) {
-            const uint32_t pick = (uint32_t)rng_below(rs, n_low);
+            const uint32_t pick = rng_below_small(rs, n_low);
             uint32_t c = 0;
             head = 0;
             for (uint32_t r = 0; r < k; ++r) {
@@ -678,7 +706,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
           } else {
             const uint64_t allm = E >= 64 ? ~0ULL : ((1ULL << E) - 1ULL);
             const uint64_t inact = allm & ~nact;
-            uint32_t pick = (uint32_t)rng_below(rs, __popcll(inact));
+            uint32_t pick = rng_below_small(rs, __popcll(inact));
             uint64_t m = inact;
             for (uint32_t i = 0; i < pick; ++i) m &= m - 1;
             head = __ffsll((long long)m) - 1;
@@ -729,7 +757,16 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       if (lane == 0) log_task(cx.logs, R_PCIE, K_PREFETCH, (int)tl, e, t, t + cfg.t_load, tl, tit);
       t += cfg.t_load;
       issued |= bit(i);
-      const int slot = admit_or_defer(cx, sm, tls, tl, e, t, false, ev_layer, ev_e);
+      if (!tavg && cfg.policy == 0) {
+        if (tl == layer) {
+          tavg = sm->avg;
+        } else {
+          for (uint32_t x = lane; x < E; x += 32) sm->tavg[x] = window_average(tls, cx.thist, cfg.window, E, x);
+          __syncwarp();
+          tavg = sm->tavg;
+        }
+      }
+      const int slot = admit_or_defer(cx, sm, tls, cx.thist, tl, e, t, false, ev_layer, ev_e, tavg);
       if (lane == 0) {
         sm->out.pref[n_pref] = (uint8_t)e;
         sm->out.pref_slot[n_pref] = (int8_t)(slot >= 0 ? slot : -1);
@@ -751,6 +788,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     }
     __syncwarp();
   }
+  mark(8);
   if (lane == 0) {
     sm->out.n_pref = n_pref;
     sm->out.completion = completion;
@@ -758,13 +796,6 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     st->now = completion;
   }
   __syncwarp();
-
-  // write back the staged layer state
-  {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(ls);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(&cx.layers[layer]);
-    for (uint32_t i = lane; i < sizeof(LayerState) / 8; i += 32) dst[i] = src[i];
-  }
 
   // per-step decision record
   if (rec_out) {

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace moeb {
@@ -71,6 +72,9 @@ struct EngineState {
   uint32_t err;                    // sticky device error (1 config, 4 logic)
   uint64_t it;                     // decode iteration (stack mode)
   uint64_t seq;                    // layer-step sequence number (stack mode)
+  uint64_t ffn_bytes;              // algorithmic FFN bytes planned (stack mode)
+  uint64_t ffn_launches;
+  uint64_t prof[16];               // phase timers of the decision launch (ns, summed)
 };
 
 // Log records (layouts == moeb_task / moeb_window / moeb_eviction).
@@ -142,6 +146,8 @@ struct DecideSmem {
   double np[kMaxB][kMaxE];   // supplied predictions (optional)
   double merged[kMaxE];
   double mean[kMaxE];
+  double avg[kMaxE];         // window averages of the executing layer (this step)
+  double tavg[kMaxE];        // ... of the prefetch target layer
   uint8_t order[kMaxB][kMaxE];
   uint64_t act[kMaxB], top[kMaxB], low[kMaxB], alt[kMaxB];
   double beta[kMaxB], thT[kMaxB], thL[kMaxB], thR[kMaxB];
@@ -180,6 +186,32 @@ __host__ __device__ __forceinline__ uint64_t rng_below(uint64_t* s, uint64_t n) 
   do { x = rng_u64(s); } while (x >= lim);
   return x % n;
 }
+// rng_below for n <= 64 without 64-bit division (identical results): the
+// rejection limit n * floor((2^64-1)/n) comes from a compile-time table and
+// x mod n is assembled from 32-bit halves.
+template <size_t... I>
+struct LimTable {
+  uint64_t v[sizeof...(I)];
+};
+template <size_t... I>
+constexpr LimTable<I...> make_lim_table(std::index_sequence<I...>) {
+  return {{(I == 0 ? 0ULL : (uint64_t)I * (~0ULL / (uint64_t)(I == 0 ? 1 : I)))...}};
+}
+using LimTableT = decltype(make_lim_table(std::make_index_sequence<kMaxE + 1>{}));
+static __constant__ const LimTableT kLim = make_lim_table(std::make_index_sequence<kMaxE + 1>{});
+
+__device__ __forceinline__ uint32_t mod64_small(uint64_t x, uint32_t n) {
+  const uint32_t hi = (uint32_t)(x >> 32), lo = (uint32_t)x;
+  const uint32_t p32 = (0xFFFFFFFFu % n + 1u) % n;  // 2^32 mod n
+  return ((hi % n) * p32 + lo % n) % n;
+}
+__device__ __forceinline__ uint32_t rng_below_small(uint64_t* s, uint32_t n) {
+  const uint64_t lim = kLim.v[n];
+  uint64_t x;
+  do { x = rng_u64(s); } while (x >= lim);
+  return mod64_small(x, n);
+}
+
 __host__ __device__ inline uint64_t splitmix_next(uint64_t* st) {
   *st += 0x9e3779b97f4a7c15ULL;
   uint64_t z = *st;
@@ -245,6 +277,7 @@ __device__ inline void classify_warp(const double* s, uint32_t E, uint32_t k, do
   const bool v0 = e0 < E, v1 = e1 < E;
   const double s0 = v0 ? s[e0] : 0.0, s1 = v1 ? s[e1] : 0.0;
   uint32_t r0 = 0, r1 = 0;
+#pragma unroll 16
   for (uint32_t j = 0; j < E; ++j) {
     const double sj = s[j];
     r0 += (sj > s0) || (sj == s0 && j < e0);

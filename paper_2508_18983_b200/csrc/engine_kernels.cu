@@ -68,14 +68,17 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(ReplayArgs a) {
       StepCtx cx;
       cx.cfg = &cfg;
       cx.st = a.st;
-      cx.layers = a.layers;
-      cx.hist = a.hist;
-      cx.logs = &a.logs;
-      cx.it = it;
-      cx.layer = layer;
       uint64_t tit = it;
       uint32_t tl = layer + 1;
       if (tl == L) { tl = 0; ++tit; }
+      cx.ls = &a.layers[layer];
+      cx.hist_l = a.hist + (size_t)layer * cfg.window * E;
+      cx.tls = &a.layers[tl];
+      cx.thist = a.hist + (size_t)tl * cfg.window * E;
+      cx.logs = &a.logs;
+      cx.prof = nullptr;
+      cx.it = it;
+      cx.layer = layer;
       cx.has_target = tit < a.iters;
       cx.target_layer = tl;
       cx.target_it = tit;

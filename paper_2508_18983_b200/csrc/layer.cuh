@@ -130,9 +130,8 @@ struct GateArgs {
 
 // grid = ceil(rows / 2) with rows = E (+1 for the shared gate); 8 warps:
 // warp w -> row 2*blockIdx + (w & 1), quarter (w >> 1) of d.
-__global__ void __launch_bounds__(kGateThreads) gate_kernel(GateArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint16_t* us = reinterpret_cast<uint16_t*>(smem_raw);  // [B][d]
+// us: [B][d] bf16 scratch in shared memory.
+__device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
   __shared__ float part[4][2][kMaxB];
   __shared__ float inv_rms[kMaxB];
   const int lane = lane_id(), warp = warp_id();

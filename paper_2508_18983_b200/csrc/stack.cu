@@ -35,7 +35,35 @@
 namespace moeb {
 
 constexpr int kMaxCmds = 3 * kMaxE + 8;
-constexpr uint32_t kRing = 256;
+constexpr uint32_t kRing = 1024;
+
+// Stream memory operations come from the driver API; resolve them through
+// the runtime so libmoeb.so itself does not link libcuda (it must load on
+// hosts without a driver, e.g. for the CPU-side ABI checks).
+using PFN_write32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using PFN_wait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_write32 p_write32 = nullptr;
+static PFN_wait32 p_wait32 = nullptr;
+
+static void load_stream_memops() {
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &f2, cudaEnableDefault, &q2) != cudaSuccess ||
+        q2 != cudaDriverEntryPointSuccess) {
+      err = "driver entry points cuStreamWriteValue32/cuStreamWaitValue32 unavailable";
+      return;
+    }
+    p_write32 = reinterpret_cast<PFN_write32>(f1);
+    p_wait32 = reinterpret_cast<PFN_wait32>(f2);
+  });
+  if (!p_write32 || !p_wait32) throw Error(5, err);
+}
 
 struct MailCmd {
   uint64_t src_off;   // byte offset into the pinned host pool
@@ -75,112 +103,69 @@ struct DecideArgs {
   StepRec* recs;
   TokRec* toks;
   uint64_t rec_cap;
+  uint64_t it;                // decode iteration of this launch (host-tracked)
+  uint64_t seq;               // 1-based layer-step sequence number (host-tracked)
 };
 
+struct GateDecideArgs {
+  GateArgs g;
+  DecideArgs d;
+  uint32_t* ticket;           // last-CTA election counter (self-resetting)
+};
+
+constexpr int kGdThreads = 256;
+constexpr uint32_t kMaxHistSmem = 32 * kMaxE;  // window * E doubles staged in smem
+
+// Shared state of the deciding CTA. Everything the decision step touches
+// lives here for the step: engine state, the executing and the prefetch
+// target layer (state + score ring), the plan and the upload commands.
 struct DecideKSmem {
   DecideSmem d;
   NextSmem n;
   StepScratch s;
   DevCfg cfg;
+  EngineState st;
+  LayerState ls, tls;
+  double hist[kMaxHistSmem], thist[kMaxHistSmem];
   float sc[kMaxB][kMaxE];
   float nsc[kMaxB][kMaxE];
   float sg[kMaxB];
   float denom[kMaxB];
+  Plan plan;
+  MailCmd cmd[kMaxCmds];
+  uint32_t n_cmds;
   uint64_t it, seq;
+  int last;
 };
+
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const volatile uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 __device__ __forceinline__ uint16_t* slot_ptr(const DecideArgs& a, uint32_t layer, int slot) {
   return a.slots + ((size_t)layer * a.slots_alloc + (uint32_t)slot) * a.expert_elems;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) decide_kernel(DecideArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  DecideKSmem* sm = reinterpret_cast<DecideKSmem*>(smem_raw);
-  const int warp = warp_id(), lane = lane_id();
-  if (threadIdx.x == 0) {
-    sm->cfg = a.cfg;
-    sm->it = a.st->it;
-    sm->seq = a.st->seq + 1;
-  }
-  __syncthreads();
+template <class T>
+__device__ __forceinline__ void cta_copy(T* dst, const T* src) {
+  static_assert(sizeof(T) % 8 == 0, "8-byte granular");
+  const uint64_t* s = reinterpret_cast<const uint64_t*>(src);
+  uint64_t* d = reinterpret_cast<uint64_t*>(dst);
+  for (uint32_t i = threadIdx.x; i < sizeof(T) / 8; i += blockDim.x) d[i] = s[i];
+}
+
+// Thread 0 builds the FFN plan and the upload commands in shared memory.
+__device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
   const DevCfg& cfg = sm->cfg;
-  const uint32_t B = cfg.B, E = cfg.E, L = cfg.L, layer = a.layer;
-  const uint64_t it = sm->it;
-  uint64_t tit = it;
-  uint32_t tl = layer + 1;
-  if (tl == L) { tl = 0; ++tit; }
-  const bool has_target = tit < a.total_iters;
-  const bool want_next = cfg.pre && has_target && a.trace;
-  for (uint32_t t = warp; t < B; t += kWarps) {
-    const float* lg = a.trace ? a.trace + (((it % a.trace_steps) * L + layer) * B + t) * E
-                              : a.logits + (size_t)t * (E + 1);
-    softmax_warp(lg, E, sm->sc[t]);
-    if (want_next) {
-      const float* nl = a.trace + (((tit % a.trace_steps) * L + tl) * B + t) * E;
-      softmax_warp(nl, E, sm->nsc[t]);
-    }
-    if (lane == 0 && a.shared_gate) {
-      const float z = a.logits[(size_t)t * (E + 1) + E];
-      sm->sg[t] = __fdiv_rn(1.0f, 1.0f + expf(-z));
-    }
-  }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < B * E; i += blockDim.x) {
-    const uint32_t t = i / E, e = i % E;
-    sm->d.s[t][e] = (double)sm->sc[t][e];
-    if (want_next) { sm->d.ns[t][e] = (double)sm->nsc[t][e]; sm->d.np[t][e] = 0.0; }
-    if (a.scores_log && sm->seq <= a.rec_cap) a.scores_log[((sm->seq - 1) * B + t) * E + e] = sm->sc[t][e];
-  }
-  if (threadIdx.x == 0) sm->d.next_has_pred = 0;
-  __syncthreads();
-
-  StepCtx cx;
-  cx.cfg = &cfg;
-  cx.st = a.st;
-  cx.layers = a.layers;
-  cx.hist = a.hist;
-  cx.logs = nullptr;
-  cx.it = it;
-  cx.layer = layer;
-  cx.has_target = want_next ? 1u : 0u;
-  cx.target_layer = tl;
-  cx.target_it = tit;
-  StepRec* rec = nullptr;
-  TokRec* toks = nullptr;
-  if (a.recs && sm->seq <= a.rec_cap) {
-    rec = a.recs + (sm->seq - 1);
-    toks = a.toks + (sm->seq - 1) * B;
-  }
-  decide_step(cx, &sm->d, &sm->n, &sm->s, rec, toks);
-  __syncthreads();
-
-  // ---------------------------------------------------------------- plan
+  const uint32_t B = cfg.B, E = cfg.E, layer = a.layer;
   DecideSmem* d = &sm->d;
   const StepOut& out = d->out;
-  if (threadIdx.x < 32 * 2 && threadIdx.x < B) {
-    // combine-weight denominators (Mixtral renormalisation)
-    const uint32_t t = threadIdx.x;
-    float s = 0.f;
-    for (uint32_t i = 0; i < d->nsel[t]; ++i) s += sm->sc[t][d->sel[t][i]];
-    sm->denom[t] = s;
-  }
-  for (uint32_t i = threadIdx.x; i < kMaxItems + 2; i += blockDim.x) a.ffn_ctr[i] = 0;
-  __syncthreads();
-  if (threadIdx.x != 0) return;
-
-  Plan* p = a.plan;
-  MailEntry* me = &a.ring[sm->seq % kRing];
-  // the ring slot must have been consumed by the copy thread
-  {
-    const uint64_t t0 = globaltimer_ns();
-    while (sm->seq > kRing && *a.host_ack < sm->seq - kRing) {
-      __nanosleep(1000);
-      if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 4u); break; }
-    }
-  }
+  Plan* p = &sm->plan;
+  EngineState* st = &sm->st;
+  LayerState* ls = &sm->ls;
   uint32_t n_items = 0, n_cmds = 0;
-  EngineState* st = a.st;
-  LayerState* ls = &a.layers[layer];
   auto add_item = [&](const uint16_t* w, uint32_t F, uint32_t wait, uint32_t kind, uint32_t e) {
     Item& itm = p->items[n_items++];
     itm.w = w;
@@ -190,12 +175,9 @@ __global__ void __launch_bounds__(kThreads, 1) decide_kernel(DecideArgs a) {
     itm.expert = e;
     uint32_t n = 0;
     for (uint32_t t = 0; t < B; ++t) {
-      bool sel = false;
-      if (kind == 0) {
-        sel = true;
-      } else {
+      bool sel = kind == 0;
+      if (!sel)
         for (uint32_t i = 0; i < d->nsel[t]; ++i) sel |= d->sel[t][i] == e;
-      }
       if (!sel) continue;
       float wt;
       if (kind == 0) {
@@ -213,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) decide_kernel(DecideArgs a) {
   };
   auto add_cmd = [&](uint32_t src_layer, uint32_t e, uint16_t* dst, uint32_t wait_ffn) -> uint32_t {
     const uint32_t id = ++st->next_copy;
-    MailCmd& c = me->cmd[n_cmds++];
+    MailCmd& c = sm->cmd[n_cmds++];
     c.src_off = ((uint64_t)src_layer * E + e) * a.expert_elems * 2;
     c.dst = (uint64_t)dst;
     c.bytes = a.expert_elems * 2;
@@ -222,7 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1) decide_kernel(DecideArgs a) {
     return id;
   };
   if (a.shared_w) add_item(a.shared_w, a.S, 0, 0, 0);
-  // residents: ready ones first, then those whose (prefetch) upload is in flight
+  // residents: ready ones first, then those whose (prefetch) upload is in
+  // flight, ordered by upload id (the copy stream is FIFO)
   for (int pass = 0; pass < 2; ++pass) {
     for (uint32_t i = 0; i < out.n_res; ++i) {
       const uint32_t e = out.res[i];
@@ -232,7 +215,6 @@ __global__ void __launch_bounds__(kThreads, 1) decide_kernel(DecideArgs a) {
       add_item(slot_ptr(a, layer, slot), a.F, wait, 1, e);
     }
   }
-  // the resident items that wait keep upload order (ids ascending)
   uint32_t n_ready = 0;
   while (n_ready < n_items && p->items[n_ready].wait == 0) ++n_ready;
   for (uint32_t i = n_ready + 1; i < n_items; ++i) {
@@ -280,19 +262,184 @@ __global__ void __launch_bounds__(kThreads, 1) decide_kernel(DecideArgs a) {
     const uint32_t tlayer = out.pref_layer;
     uint16_t* dst = slot >= 0 ? slot_ptr(a, tlayer, slot) : a.staging;
     const uint32_t id = add_cmd(tlayer, e, dst, (uint32_t)sm->seq);
-    if (slot >= 0) a.layers[tlayer].slot_copy[slot] = id;
+    LayerState* tls = (tlayer == layer) ? ls : &sm->tls;
+    if (slot >= 0) tls->slot_copy[slot] = id;
   }
+  // algorithmic bytes of the FFN launch: every item's weights once, plus
+  // u / x in, x out (bf16) and the fp32 layer output
+  uint64_t bytes = 4ull * B * a.d * 2 + (uint64_t)B * a.d * 4;
+  for (uint32_t i = 0; i < n_items; ++i) bytes += 3ull * p->items[i].F * a.d * 2;
+  st->ffn_bytes += bytes;
+  st->ffn_launches += 1;
   p->n_items = n_items;
   p->n_ready = n_ready;
   p->n_d2d = n_d2d;
   p->d2d_elems = a.expert_elems;
   p->seq = (uint32_t)sm->seq;
-  me->n = n_cmds;
-  __threadfence_system();
-  me->seq = sm->seq;
-  __threadfence_system();
-  st->seq = sm->seq;
-  if (layer == L - 1) st->it = it + 1;
+  sm->n_cmds = n_cmds;
+}
+
+// Router gate (all CTAs) then, in the last CTA to finish, the decision step,
+// the FFN plan and the upload mailbox. One launch per layer.
+__global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideArgs ga) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint64_t t_entry = gtimer();
+  // gate phase: us [B][d] bf16 aliases the decision workspace
+  gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw));
+  const uint64_t t_gate = gtimer();
+  DecideKSmem* sm = reinterpret_cast<DecideKSmem*>(smem_raw);
+  __shared__ int s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(ga.ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+    if (s_last) {
+      *ga.ticket = 0;
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+
+  const DecideArgs& a = ga.d;
+  const uint64_t t_elect = gtimer();
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t nw = blockDim.x >> 5;
+  // stage the step's state: one parallel load phase (it / seq come from the
+  // host, so every address is known at launch)
+  const uint32_t L = a.cfg.L, B = a.cfg.B, E = a.cfg.E, layer = a.layer;
+  const uint64_t it = a.it;
+  uint32_t tl = layer + 1;
+  uint64_t tit = it;
+  if (tl == L) { tl = 0; ++tit; }
+  const bool has_target = tit < a.total_iters;
+  const bool want_next = a.cfg.pre && has_target && a.trace;
+  const bool smem_hist = a.cfg.window * E <= kMaxHistSmem;
+  const size_t hwords = (size_t)a.cfg.window * E;
+  cta_copy(&sm->st, a.st);
+  cta_copy(&sm->cfg, &a.cfg);
+  cta_copy(&sm->ls, &a.layers[layer]);
+  if (smem_hist)
+    for (uint32_t i = threadIdx.x; i < hwords; i += blockDim.x) sm->hist[i] = a.hist[layer * hwords + i];
+  if (want_next && tl != layer) {
+    cta_copy(&sm->tls, &a.layers[tl]);
+    if (smem_hist)
+      for (uint32_t i = threadIdx.x; i < hwords; i += blockDim.x) sm->thist[i] = a.hist[tl * hwords + i];
+  }
+  const uint32_t jobs = want_next ? 2 * B : B;
+  for (uint32_t j = warp; j < jobs; j += nw) {
+    if (j < B) {
+      const uint32_t t = j;
+      const float* lg = a.trace ? a.trace + (((it % a.trace_steps) * L + layer) * B + t) * E
+                                : a.logits + (size_t)t * (E + 1);
+      softmax_warp(lg, E, sm->sc[t]);
+      if (lane == 0 && a.shared_gate) {
+        const float z = a.logits[(size_t)t * (E + 1) + E];
+        sm->sg[t] = __fdiv_rn(1.0f, 1.0f + expf(-z));
+      }
+    } else {
+      const uint32_t t = j - B;
+      softmax_warp(a.trace + (((tit % a.trace_steps) * L + tl) * B + t) * E, E, sm->nsc[t]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    sm->it = it;
+    sm->seq = a.seq;
+    sm->d.next_has_pred = 0;
+  }
+  __syncthreads();
+  const DevCfg& cfg = sm->cfg;
+  for (uint32_t i = threadIdx.x; i < B * E; i += blockDim.x) {
+    const uint32_t t = i / E, e = i % E;
+    sm->d.s[t][e] = (double)sm->sc[t][e];
+    if (want_next) sm->d.ns[t][e] = (double)sm->nsc[t][e];
+    if (a.scores_log && a.seq <= a.rec_cap) a.scores_log[((a.seq - 1) * B + t) * E + e] = sm->sc[t][e];
+  }
+  __syncthreads();
+  const uint64_t t_staged = gtimer();
+
+  StepCtx cx;
+  cx.cfg = &cfg;
+  cx.st = &sm->st;
+  cx.ls = &sm->ls;
+  cx.hist_l = smem_hist ? sm->hist : a.hist + layer * hwords;
+  cx.tls = (tl == layer) ? &sm->ls : &sm->tls;
+  cx.thist = (tl == layer) ? cx.hist_l : (smem_hist ? sm->thist : a.hist + tl * hwords);
+  cx.logs = nullptr;
+  cx.it = it;
+  cx.layer = layer;
+  cx.has_target = want_next ? 1u : 0u;
+  cx.target_layer = tl;
+  cx.target_it = tit;
+  cx.prof = sm->st.prof;
+  StepRec* rec = nullptr;
+  TokRec* toks = nullptr;
+  if (a.recs && sm->seq <= a.rec_cap) {
+    rec = a.recs + (sm->seq - 1);
+    toks = a.toks + (sm->seq - 1) * B;
+  }
+  decide_step(cx, &sm->d, &sm->n, &sm->s, rec, toks);
+  __syncthreads();
+  const uint64_t t_decided = gtimer();
+
+  // combine-weight denominators (Mixtral renormalisation), FFN counters
+  if (threadIdx.x < B) {
+    const uint32_t t = threadIdx.x;
+    float s = 0.f;
+    for (uint32_t i = 0; i < sm->d.nsel[t]; ++i) s += sm->sc[t][sm->d.sel[t][i]];
+    sm->denom[t] = s;
+  }
+  for (uint32_t i = threadIdx.x; i < kMaxItems + 2; i += blockDim.x) a.ffn_ctr[i] = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    build_plan(a, sm);
+    // the ring slot must have been consumed by the copy thread
+    const uint64_t t0 = globaltimer_ns();
+    while (sm->seq > kRing && ld_acquire_sys_u64(a.host_ack) < sm->seq - kRing) {
+      __nanosleep(500);
+      if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 4u); break; }
+    }
+    sm->st.prof[11] += globaltimer_ns() - t0;
+    sm->st.seq = sm->seq;
+    if (layer == L - 1) sm->st.it = it + 1;
+    const uint64_t t_plan = gtimer();
+    sm->st.prof[0] += t_gate - t_entry;
+    sm->st.prof[1] += t_elect - t_gate;
+    sm->st.prof[2] += t_staged - t_elect;
+    sm->st.prof[3] += t_decided - t_staged;
+    sm->st.prof[9] += t_plan - t_decided;
+  }
+  __syncthreads();
+  // publish: plan -> global, commands -> mapped host ring, state write-back
+  {
+    Plan* gp = a.plan;
+    const uint32_t n_items = sm->plan.n_items;
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&sm->plan);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(gp);
+    const size_t words = (offsetof(Plan, items) + n_items * sizeof(Item)) / 8;
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + sm->plan.n_d2d * sizeof(D2D) / 8;
+    for (uint32_t i = d0 + threadIdx.x; i < d1; i += blockDim.x) dst[i] = src[i];
+    MailEntry* me = &a.ring[sm->seq % kRing];
+    const uint32_t nc = sm->n_cmds;
+    const uint64_t* cs = reinterpret_cast<const uint64_t*>(sm->cmd);
+    uint64_t* cd = reinterpret_cast<uint64_t*>(me->cmd);
+    for (uint32_t i = threadIdx.x; i < nc * sizeof(MailCmd) / 8; i += blockDim.x) cd[i] = cs[i];
+    if (threadIdx.x == 0) me->n = nc;
+    cta_copy(a.st, &sm->st);
+    cta_copy(&a.layers[layer], &sm->ls);
+    if (want_next && tl != layer) cta_copy(&a.layers[tl], &sm->tls);
+    if (smem_hist)
+      for (uint32_t i = threadIdx.x; i < hwords; i += blockDim.x) a.hist[layer * hwords + i] = sm->hist[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = gtimer();
+    __threadfence_system();
+    a.ring[sm->seq % kRing].seq = sm->seq;
+    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->prof[10]), (unsigned long long)(gtimer() - t0));
+  }
 }
 
 // =================================================================== host
@@ -335,13 +482,50 @@ struct moeb_stack {
   std::string copier_msg;
   int ffn_grid = 0;
   void (*ffn_fn)(FfnArgs) = nullptr;
-  size_t ffn_smem = 0, gate_smem = 0, decide_smem = 0;
+  size_t ffn_smem = 0, gd_smem = 0;
+  DevBuf<uint32_t> ticket;
+  MailEntry* ring_dev = nullptr;
+  uint64_t* ack_dev = nullptr;
+  uint64_t host_it = 0, host_seq = 0;  // mirrors of EngineState::it / seq
   std::mutex io_mu;
   IoAcc io;
   static constexpr int kEv = 512;
   cudaEvent_t ev_a[kEv] = {}, ev_b[kEv] = {};
   bool ev_live[kEv] = {};
   int ev_next = 0;
+
+  // Kernel timing (MOEB_MODEL_TIME_KERNELS): 3 events per layer on the
+  // compute stream: before gate+decide, before FFN, after FFN.
+  bool timing = false;
+  static constexpr int kTk = 3 * 1024;
+  cudaEvent_t tk_ev[kTk] = {};
+  int tk_n = 0;       // recorded, not yet harvested
+  int tk_head = 0;    // oldest unharvested
+  int tk_phase = 0;
+  double kern_ms[2] = {0, 0};  // gate+decide, ffn
+  uint64_t kern_n[2] = {0, 0};
+  void tk_harvest_one() {
+    const int i0 = tk_head;
+    cudaEventSynchronize(tk_ev[(i0 + 2) % kTk]);
+    for (int k = 0; k < 2; ++k) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, tk_ev[(i0 + k) % kTk], tk_ev[(i0 + k + 1) % kTk]) == cudaSuccess) {
+        kern_ms[k] += ms;
+        kern_n[k] += 1;
+      }
+    }
+    tk_head = (tk_head + 3) % kTk;
+    tk_n -= 3;
+  }
+  void tick(cudaStream_t s) {
+    if (tk_phase == 0 && tk_n + 3 > kTk) tk_harvest_one();
+    cudaEventRecord(tk_ev[(tk_head + tk_n) % kTk], s);
+    ++tk_n;
+    tk_phase = (tk_phase + 1) % 3;
+  }
+  void tk_harvest_all() {
+    while (tk_n >= 3) tk_harvest_one();
+  }
 
   void harvest(int i) {  // requires io_mu
     if (!ev_live[i]) return;
@@ -369,7 +553,7 @@ struct moeb_stack {
       for (uint32_t i = 0; i < n; ++i) {
         const MailCmd c = me->cmd[i];
         if (c.wait_ffn &&
-            cuStreamWaitValue32(copy_stream, ffn_ptr, c.wait_ffn, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+            p_wait32(copy_stream, ffn_ptr, c.wait_ffn, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
           copier_msg = "cuStreamWaitValue32 failed";
           copier_error = 5;
         }
@@ -387,7 +571,7 @@ struct moeb_stack {
           copier_msg = std::string("upload failed: ") + cudaGetErrorString(ce);
           copier_error = 5;
         }
-        if (cuStreamWriteValue32(copy_stream, done_ptr, c.id, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+        if (p_write32(copy_stream, done_ptr, c.id, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
           copier_msg = "cuStreamWriteValue32 failed";
           copier_error = 5;
         }
@@ -405,6 +589,8 @@ struct moeb_stack {
     if (copier.joinable()) copier.join();
     if (stream) cudaStreamSynchronize(stream);
     if (copy_stream) cudaStreamSynchronize(copy_stream);
+    for (int i = 0; i < kTk; ++i)
+      if (tk_ev[i]) cudaEventDestroy(tk_ev[i]);
     for (int i = 0; i < kEv; ++i) {
       if (ev_a[i]) cudaEventDestroy(ev_a[i]);
       if (ev_b[i]) cudaEventDestroy(ev_b[i]);
@@ -440,6 +626,33 @@ static FfnFn ffn_kernel_for(uint32_t B) {
 
 static float fan_scale(uint32_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
 
+// (Re)initialise the decision state and upload the initial residents. The
+// layer-step sequence and upload ids stay monotonic across resets: the
+// device flags compared against them (copies_done, ffn_done) only grow.
+static void reset_state(moeb_stack* S, cudaStream_t s) {
+  const uint32_t L = S->L, E = S->E;
+  const uint64_t eb = S->expert_elems * 2;
+  std::vector<LayerState> ls;
+  init_layers(S->dcfg, S->cfg.init_fill, S->cfg.seed, ls);
+  EngineState prev{};
+  MOEB_CUDA(cudaMemcpyAsync(&prev, S->st.p, sizeof prev, cudaMemcpyDeviceToHost, s));
+  MOEB_CUDA(cudaStreamSynchronize(s));
+  EngineState st{};
+  rng_seed(st.rng, derive_seed(S->cfg.seed, 0x94ed1c70ULL));  // pipeline.cpp:62
+  st.seq = prev.seq;
+  st.next_copy = prev.next_copy;
+  S->hist.zero(s);
+  MOEB_CUDA(cudaMemcpyAsync(S->st.p, &st, sizeof st, cudaMemcpyHostToDevice, s));
+  MOEB_CUDA(cudaMemcpyAsync(S->layers.p, ls.data(), L * sizeof(LayerState), cudaMemcpyHostToDevice, s));
+  for (uint32_t l = 0; l < L; ++l)
+    for (uint32_t e = 0; e < E; ++e)
+      if (ls[l].slot_of[e] >= 0)
+        MOEB_CUDA(cudaMemcpyAsync(S->slots.p + ((size_t)l * S->slots_alloc + ls[l].slot_of[e]) * S->expert_elems,
+                                  reinterpret_cast<char*>(S->pool) + ((uint64_t)l * E + e) * eb, eb,
+                                  cudaMemcpyHostToDevice, s));
+  MOEB_CUDA(cudaStreamSynchronize(s));
+}
+
 static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model& m, const void* weights_host,
                         int device) {
   validate(cfg);
@@ -468,13 +681,11 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
     MOEB_CUDA(cudaEventCreate(&S->ev_a[i]));
     MOEB_CUDA(cudaEventCreate(&S->ev_b[i]));
   }
-  int attr = 0;
-  CUdevice cud;
-  if (cuDeviceGet(&cud, device) == CUDA_SUCCESS &&
-      cuDeviceGetAttribute(&attr, CU_DEVICE_ATTRIBUTE_CAN_USE_STREAM_WAIT_VALUE_NOR, cud) == CUDA_SUCCESS) {
-    // stream memory operations are available on every sm_100 driver; the
-    // attribute probe only initialises the driver API here
+  if (m.flags & MOEB_MODEL_TIME_KERNELS) {
+    S->timing = true;
+    for (int i = 0; i < moeb_stack::kTk; ++i) MOEB_CUDA(cudaEventCreate(&S->tk_ev[i]));
   }
+  load_stream_memops();
   const cudaStream_t s = S->stream;
   const uint32_t L = S->L, E = S->E, B = S->B, d = S->d, F = S->F, Sh = S->S;
   const uint64_t seed = m.weight_seed;
@@ -530,24 +741,13 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   S->h.alloc((size_t)kMaxItems * kMaxB * Fmax);
   S->y_layers.alloc((size_t)L * B * d);
   S->y_layers.zero(s);
-  // decision engine state
-  std::vector<LayerState> ls;
-  init_layers(S->dcfg, cfg.init_fill, cfg.seed, ls);
-  EngineState st{};
-  rng_seed(st.rng, derive_seed(cfg.seed, 0x94ed1c70ULL));
+  // decision engine state + initial residency
   S->st.alloc(1);
   S->layers.alloc(L);
   S->hist.alloc((size_t)L * cfg.window * E);
-  S->hist.zero(s);
-  MOEB_CUDA(cudaMemcpyAsync(S->st.p, &st, sizeof st, cudaMemcpyHostToDevice, s));
-  MOEB_CUDA(cudaMemcpyAsync(S->layers.p, ls.data(), L * sizeof(LayerState), cudaMemcpyHostToDevice, s));
-  // initial residency: upload the resident experts into their slots
-  for (uint32_t l = 0; l < L; ++l)
-    for (uint32_t e = 0; e < E; ++e)
-      if (ls[l].slot_of[e] >= 0)
-        MOEB_CUDA(cudaMemcpyAsync(S->slots.p + ((size_t)l * S->slots_alloc + ls[l].slot_of[e]) * S->expert_elems,
-                                  reinterpret_cast<char*>(S->pool) + ((uint64_t)l * E + e) * eb, eb,
-                                  cudaMemcpyHostToDevice, s));
+  EngineState st0{};
+  MOEB_CUDA(cudaMemcpyAsync(S->st.p, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
+  reset_state(S, s);
   S->plan.alloc(1);
   S->ffn_ctr.alloc(kMaxItems + 2);
   S->ffn_ctr.zero(s);
@@ -566,13 +766,19 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   MOEB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->ack), 64, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(S->ack, 0, 64);
   // kernel resources
-  S->gate_smem = (size_t)B * d * 2;
   S->ffn_smem = (size_t)B * d * 2;
-  S->decide_smem = sizeof(DecideKSmem);
-  MOEB_CUDA(cudaFuncSetAttribute(gate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->gate_smem));
+  S->ticket.alloc(1);
+  S->ticket.zero(s);
+  MOEB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->ring_dev), S->ring, 0));
+  MOEB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->ack_dev), S->ack, 0));
+  S->gd_smem = std::max<size_t>((size_t)B * d * 2, sizeof(DecideKSmem));
+  MOEB_CUDA(cudaFuncSetAttribute(gate_decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->gd_smem));
+  // one shared-memory carveout for both per-layer kernels: no L1/smem
+  // reconfiguration drain between them
+  MOEB_CUDA(cudaFuncSetAttribute(gate_decide_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   S->ffn_fn = ffn_kernel_for(B);
   MOEB_CUDA(cudaFuncSetAttribute(S->ffn_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->ffn_smem));
-  MOEB_CUDA(cudaFuncSetAttribute(decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->decide_smem));
+  MOEB_CUDA(cudaFuncSetAttribute(S->ffn_fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int sms = 0, occ = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   MOEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->ffn_fn, kFfnThreads, S->ffn_smem));
@@ -593,7 +799,8 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
   MOEB_CUDA(cudaMemcpyAsync(S->hidden.p, x, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
   int cur = 0;
   for (uint32_t l = 0; l < L; ++l) {
-    GateArgs g{};
+    GateDecideArgs ga{};
+    GateArgs& g = ga.g;
     g.x = S->hidden.p + (size_t)cur * B * d;
     g.wg = S->gate_w.p + (size_t)l * E * d;
     g.wsg = S->model.shared_gate ? S->sgate_w.p + (size_t)l * d : nullptr;
@@ -603,10 +810,7 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     g.d = d;
     g.E = E;
     const uint32_t rows = E + (g.wsg ? 1 : 0);
-    gate_kernel<<<(rows + 1) / 2, kGateThreads, S->gate_smem, s>>>(g);
-    MOEB_CUDA(cudaGetLastError());
-
-    DecideArgs a{};
+    DecideArgs& a = ga.d;
     a.cfg = S->dcfg;
     a.st = S->st.p;
     a.layers = S->layers.p;
@@ -630,18 +834,19 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.expert_elems = S->expert_elems;
     a.plan = S->plan.p;
     a.ffn_ctr = S->ffn_ctr.p;
-    uint64_t* ack_dev = nullptr;
-    MailEntry* ring_dev = nullptr;
-    MOEB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ring_dev), S->ring, 0));
-    MOEB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ack_dev), S->ack, 0));
-    a.ring = ring_dev;
-    a.host_ack = ack_dev;
+    a.ring = S->ring_dev;
+    a.host_ack = S->ack_dev;
     a.scores_log = S->scores_log.p;
     a.recs = S->recs.p;
     a.toks = S->toks.p;
     a.rec_cap = S->rec_cap;
-    decide_kernel<<<1, kThreads, S->decide_smem, s>>>(a);
+    a.it = S->host_it;
+    a.seq = ++S->host_seq;
+    ga.ticket = S->ticket.p;
+    if (S->timing) S->tick(s);
+    gate_decide_kernel<<<(rows + 1) / 2, kGdThreads, S->gd_smem, s>>>(ga);
     MOEB_CUDA(cudaGetLastError());
+    if (S->timing) S->tick(s);
 
     FfnArgs f{};
     f.plan = S->plan.p;
@@ -661,9 +866,11 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     void* fargs[] = {&f};
     MOEB_CUDA(cudaLaunchKernel(S->ffn_fn, dim3(S->ffn_grid), dim3(kFfnThreads), fargs, S->ffn_smem, s));
     MOEB_CUDA(cudaGetLastError());
+    if (S->timing) S->tick(s);
     cur ^= 1;
   }
   MOEB_CUDA(cudaMemcpyAsync(y, S->hidden.p + (size_t)cur * B * d, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
+  S->host_it += 1;
   std::lock_guard<std::mutex> g(S->io_mu);
   S->io.steps += 1;
 }
@@ -790,6 +997,56 @@ int moeb_get_layer_outputs(moeb_stack* s, float* out, size_t cap) {
     MOEB_CUDA(cudaMemcpy(out, s->y_layers.p, n * sizeof(float), cudaMemcpyDeviceToHost));
   });
 }
+
+int moeb_reset(moeb_stack* s) {
+  return guarded([&] {
+    MOEB_CUDA(cudaSetDevice(s->device));
+    MOEB_CUDA(cudaStreamSynchronize(s->stream));
+    MOEB_CUDA(cudaStreamSynchronize(s->copy_stream));
+    reset_state(s, s->stream);
+    s->host_it = 0;
+  });
+}
+
+int moeb_get_kernel_stats(moeb_stack* s, moeb_kernel_stats* out) {
+  return guarded([&] {
+    MOEB_CUDA(cudaSetDevice(s->device));
+    MOEB_CUDA(cudaStreamSynchronize(s->stream));
+    if (s->timing) s->tk_harvest_all();
+    EngineState st;
+    MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
+    *out = moeb_kernel_stats{};
+    out->route_ms = s->kern_ms[0];
+    out->ffn_ms = s->kern_ms[1];
+    out->route_launches = s->kern_n[0];
+    out->ffn_launches = s->kern_n[1];
+    out->ffn_bytes = st.ffn_bytes;
+    out->ffn_planned = st.ffn_launches;
+    for (int i = 0; i < 16; ++i) out->prof_ns[i] = st.prof[i];
+    const uint64_t gb = (uint64_t)s->E * s->d * 2 + 2ull * s->B * s->d * 2 + (uint64_t)s->B * (s->E + 1) * 4 +
+                        (s->model.shared_gate ? (uint64_t)s->d * 2 : 0);
+    out->route_bytes = gb * s->kern_n[0];
+  });
+}
+
+int moeb_reset_kernel_stats(moeb_stack* s) {
+  return guarded([&] {
+    MOEB_CUDA(cudaStreamSynchronize(s->stream));
+    if (s->timing) s->tk_harvest_all();
+    for (int k = 0; k < 2; ++k) { s->kern_ms[k] = 0; s->kern_n[k] = 0; }
+    EngineState st;
+    MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
+    st.ffn_bytes = 0;
+    st.ffn_launches = 0;
+    MOEB_CUDA(cudaMemcpy(s->st.p, &st, sizeof st, cudaMemcpyHostToDevice));
+    std::lock_guard<std::mutex> g(s->io_mu);
+    MOEB_CUDA(cudaStreamSynchronize(s->copy_stream));
+    for (int i = 0; i < moeb_stack::kEv; ++i) s->harvest(i);
+    s->io = IoAcc{};
+  });
+}
+
+void* moeb_stream(moeb_stack* s) { return s->stream; }
 
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes) {
   *pool = s->pool;

@@ -1,0 +1,60 @@
+#!/usr/bin/env python3
+"""Profiling driver: runs the bench workload (DeepSeek-V2-Lite 26-layer stack,
+batch-1, cache 16/64, CE+ER+Pre+BA) for a few tokens so ncu can capture the
+kernels. --allhit makes every expert resident (no uploads, so the FFN never
+waits on the copy stream — required under ncu's serialised replay).
+
+  ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+      --log-file gpurun_out/launches.csv python tools/profile_stack.py --tokens 8
+  ncu --set full --clock-control none --import-source on -k regex:ffn_kernel -s 20 -c 2 \
+      -o gpurun_out/ffn python tools/profile_stack.py --tokens 4 --allhit
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tokens", type=int, default=8)
+    ap.add_argument("--allhit", action="store_true")
+    ap.add_argument("--layers", type=int, default=26)
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--time", action="store_true", help="print per-kernel CUDA-event times")
+    args = ap.parse_args()
+    import torch
+    from paper_2508_18983_b200 import capi
+
+    L, E, B, d = args.layers, 64, args.batch, 2048
+    cfg = capi.Config.make(num_layers=L, experts=E, top_k=6, batch=B, alpha=0.25, seed=7,
+                           slots=E if args.allhit else 16)
+    st = capi.Stack(cfg, 2048, 1408, 2816, weight_seed=7, time_kernels=args.time)
+    T = args.tokens
+    st.set_logits_trace(capi.trace_logits(capi.generate_trace(L, E, B, T, 7)), T)
+    x = torch.randn(T, B, d).to(torch.bfloat16).cuda()
+    y = torch.empty(B, d, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i in range(T):
+        st.step(x[i].data_ptr(), y.data_ptr(), B)
+    st.sync()
+    dt = time.time() - t0
+    if args.time:
+        k = st.kernel_stats()
+        print({kk: (round(v / T, 4) if kk.endswith("_ms") else v) for kk, v in k.items() if kk != "prof_ns"},
+              "ms/token wall", round(dt * 1e3 / T, 3))
+        n = k["route_launches"] or 1
+        names = ["gate", "elect", "stage", "decide", "d:classify", "d:route", "d:hits+record", "d:loads",
+                 "d:prefetch", "plan", "publish", "ring_wait"]
+        print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names)})
+    st.close()
+
+
+if __name__ == "__main__":
+    main()
