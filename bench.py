@@ -187,8 +187,10 @@ def run_ours(args):
     stack = capi.Stack(cfg, weight_seed=7, time_kernels=True, device=local, **MODEL)
     create_s = time.time() - t0
     stack.set_logits_trace(logits, T)
-    s_ptr = stack.stream()
-    s = torch.cuda.ExternalStream(s_ptr)
+    # a torch-owned stream for the stack's work: pinned-buffer copies recorded
+    # on it stay valid after the stack (and its internal streams) is destroyed
+    s = torch.cuda.Stream()
+    s_ptr = s.cuda_stream
 
     def run_steps(lo, hi, e2e=False):
         for i in range(lo, hi):
@@ -245,8 +247,8 @@ def run_ours(args):
         pool_ptr, _ = stack.host_pool()
         st2 = capi.Stack(cfg2, weight_seed=7, device=local, weights_host=(pool_ptr, stack), **MODEL)
         st2.set_logits_trace(logits, T)
-        s2p = st2.stream()
-        s2 = torch.cuda.ExternalStream(s2p)
+        s2 = torch.cuda.Stream()
+        s2p = s2.cuda_stream
         with torch.cuda.stream(s2):
             for i in range(W):
                 st2.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s2p)
@@ -273,7 +275,8 @@ def run_ours(args):
     pool_ptr, _ = stack.host_pool()
     st3 = capi.Stack(cfg3, weight_seed=7, device=local, weights_host=(pool_ptr, stack), time_kernels=True, **MODEL)
     st3.set_logits_trace(logits, T)
-    s3p = st3.stream()
+    s3 = torch.cuda.Stream()
+    s3p = s3.cuda_stream
     n3 = min(64, T)
     for i in range(8):
         st3.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
@@ -361,6 +364,8 @@ def run_ours(args):
         result["ablation"] = abl
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(scores, x_host, args.cpu_sample_tokens)
+    torch.cuda.synchronize()
+    del x_pin, y_pin
     stack.close()
     if rank == 0:
         print(json.dumps(result), flush=True)

@@ -2,10 +2,10 @@
  * moesched_b200.h — C-ABI of the B200-native MoE decode hot path.
  *
  * This is the drop-in boundary for the decision path of the reference
- * scheduler (/root/reference/proj/include/moesched/*.hpp). The reference is a
+ * scheduler (/root/reference/proj/include/moesched/ headers). The reference is a
  * C++20 library with no FFI of its own; the entry points below are what a
  * foreign binding (ctypes / cgo / JNI) of that path binds, and what our C++
- * re-declaration of the reference headers (include/moesched/*.hpp,
+ * re-declaration of the reference headers (include/moesched/,
  * libmoesched.so) calls. Plain pointers and sizes only; no CUDA or torch
  * types cross this boundary (streams are opaque `void*` cudaStream_t).
  *

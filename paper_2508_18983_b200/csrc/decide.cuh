@@ -381,8 +381,120 @@ __device__ inline int admit_or_defer(const StepCtx& cx, DecideSmem* sm, LayerSta
 
 // The step. Caller fills sm->s (and sm->ns / sm->np / sm->next_has_pred when
 // cx.has_target && cfg.pre) and __syncthreads() before the call.
+// The stochastic next-layer predictor (prefetch.cpp:34-83) for every token,
+// the per-expert max merge (pipeline.cpp:412-425) and the build_queue
+// ranking (prefetch.cpp:96-105). Independent of the executing layer's
+// decisions, so the stack runs it on warp 1 while warp 0 routes.
+__device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, NextSmem* nx) {
+  const DevCfg& cfg = *cx.cfg;
+  EngineState* st = cx.st;
+  const int lane = lane_id();
+  const uint32_t E = cfg.E, B = cfg.B, k = cfg.k;
+  for (uint32_t e = lane; e < E; e += 32) sm->merged[e] = 0.0;
+  __syncwarp();
+  uint64_t rs[4] = {st->rng[0], st->rng[1], st->rng[2], st->rng[3]};
+  for (uint32_t t = 0; t < B; ++t) {
+    const double* tn = sm->ns[t];
+    const bool supplied = (sm->next_has_pred >> t) & 1ULL;
+    // kind_of / argmax of the true vector
+    const uint64_t ntop = nx->top[t], nact = nx->act[t];
+    uint32_t head;
+    int kind;
+    // argmax_first (prefetch.cpp:12-20): max value, lowest index
+    auto argmax_first = [&](const double* v) -> uint32_t {
+      double bv = 0.0;
+      uint32_t bi = 0xffffffffu;
+      for (uint32_t e = lane; e < E; e += 32)
+        if (bi == 0xffffffffu || v[e] > bv) { bv = v[e]; bi = e; }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+        const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (i2 != 0xffffffffu && (bi == 0xffffffffu || v2 > bv || (v2 == bv && i2 < bi))) { bv = v2; bi = i2; }
+      }
+      return bi;
+    };
+    uint32_t tt = 0;
+    if (supplied) {
+      head = argmax_first(sm->np[t]);
+      kind = has(ntop, head) ? 0 : (has(nact, head) ? 1 : 2);
+      for (uint32_t e = lane; e < E; e += 32) {
+        const double v = sm->np[t][e];
+        if (sm->merged[e] < v) sm->merged[e] = v;
+      }
+    } else {
+      const uint32_t n_top = __popcll(ntop);
+      if (rng_double(rs) < cfg.p_top && n_top > 0) {
+        const uint32_t pick = rng_below_small(rs, n_top);
+        uint32_t c = 0;
+        head = 0;
+        for (uint32_t r = 0; r < k; ++r) {
+          const uint32_t e = nx->order[t][r];
+          if (has(ntop, e)) { if (c == pick) { head = e; break; } ++c; }
+        }
+        kind = 0;
+      } else {
+        const uint64_t lows = nact & ~ntop;
+        const uint32_t n_low = __popcll(lows);
+        if (rng_double(rs) < cfg.p_active && n_low > 0) {
+          const uint32_t pick = rng_below_small(rs, n_low);
+          uint32_t c = 0;
+          head = 0;
+          for (uint32_t r = 0; r < k; ++r) {
+            const uint32_t e = nx->order[t][r];
+            if (has(lows, e)) { if (c == pick) { head = e; break; } ++c; }
+          }
+          kind = 1;
+        } else {
+          const uint64_t allm = E >= 64 ? ~0ULL : ((1ULL << E) - 1ULL);
+          const uint64_t inact = allm & ~nact;
+          uint32_t pick = rng_below_small(rs, __popcll(inact));
+          uint64_t m = inact;
+          for (uint32_t i = 0; i < pick; ++i) m &= m - 1;
+          head = __ffsll((long long)m) - 1;
+          kind = 2;
+        }
+      }
+      tt = argmax_first(tn);
+      for (uint32_t e = lane; e < E; e += 32) {
+        const double v = (e == head) ? tn[tt] : ((e == tt) ? tn[head] : tn[e]);
+        if (sm->merged[e] < v) sm->merged[e] = v;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      Counters& c = st->c;
+      if (supplied) c.trace_supplied++; else c.draws++;
+      if (kind == 0) c.head_top++; else if (kind == 1) c.head_active++; else c.head_inactive++;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) { st->rng[0] = rs[0]; st->rng[1] = rs[1]; st->rng[2] = rs[2]; st->rng[3] = rs[3]; }
+  // build_queue (prefetch.cpp:85-115): rank merged, first `depth` non-resident
+  uint8_t* qorder = sm->qorder;
+  for (uint32_t e = lane; e < E; e += 32) {
+    const double v = sm->merged[e];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < E; ++j) {
+      const double vj = sm->merged[j];
+      r += (vj > v) || (vj == v && j < e);
+    }
+    qorder[r] = (uint8_t)e;
+  }
+  __syncwarp();
+  __syncwarp();
+}
+
+// Called by warp 0 as soon as the demand-load / BA-stream lists are final
+// (before the GPU task clock, deferrals and prefetch), so the caller can hand
+// the uploads to the copy engine early.
+struct NoHook {
+  __device__ void operator()(DecideSmem*, uint32_t, uint32_t) const {}
+};
+
+template <class Hook = NoHook>
 __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* nx,
-                                   StepScratch* sc, StepRec* rec_out, TokRec* tok_out) {
+                                   StepScratch* sc, StepRec* rec_out, TokRec* tok_out,
+                                   const Hook& on_loads = Hook()) {
   const DevCfg& cfg = *cx.cfg;
   EngineState* st = cx.st;
   const int tid = threadIdx.x, lane = lane_id(), warp = warp_id();
@@ -390,10 +502,14 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   const uint64_t it = cx.it;
 
   const uint32_t nw = blockDim.x >> 5;
+#ifdef MOEB_PROFILE_PHASES
   uint64_t tp = (cx.prof && tid == 0) ? gtimer() : 0;
   auto mark = [&](int i) {
     if (cx.prof && tid == 0) { const uint64_t n = gtimer(); cx.prof[i] += n - tp; tp = n; }
   };
+#else
+  auto mark = [](int) {};  // phase timers compiled out (build with -DMOEB_PROFILE_PHASES)
+#endif
   if (tid == 0) {
     const uint64_t start = st->now;
     // attention + gate (pipeline.cpp:133-145)
@@ -469,6 +585,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
 
   mark(5);
+  if (warp == 1 && want_next) {
+    predict_queue_warp(cx, sm, nx);
+    asm volatile("bar.arrive 2, 64;" ::: "memory");
+    return;
+  }
   if (warp != 0) return;  // the rest is order-dependent: warp 0 in lock-step
 
   // ---- hit accounting + batch_of (pipeline.cpp:176-189)
@@ -582,6 +703,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   if (lane == 0) { st->pcie_free = pcie_t; st->c.demand += n_load; }
   __syncwarp();
+  on_loads(sm, n_load, n_cpu);
 
   // GPU expert compute (pipeline.cpp:242-266)
   uint64_t gpu_t = st->gpu_free > route_end ? st->gpu_free : route_end;
@@ -649,97 +771,9 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     const uint64_t gate = completion + cfg.t_attn;
     LayerState* tls = cx.tls;
     const double* tavg = nullptr;  // computed on the first prefetch admission
-    for (uint32_t e = lane; e < E; e += 32) sm->merged[e] = 0.0;
-    __syncwarp();
-    uint64_t rs[4] = {st->rng[0], st->rng[1], st->rng[2], st->rng[3]};
-    for (uint32_t t = 0; t < B; ++t) {
-      const double* tn = sm->ns[t];
-      const bool supplied = (sm->next_has_pred >> t) & 1ULL;
-      // kind_of / argmax of the true vector
-      const uint64_t ntop = nx->top[t], nact = nx->act[t];
-      uint32_t head;
-      int kind;
-      // argmax_first (prefetch.cpp:12-20): max value, lowest index
-      auto argmax_first = [&](const double* v) -> uint32_t {
-        double bv = 0.0;
-        uint32_t bi = 0xffffffffu;
-        for (uint32_t e = lane; e < E; e += 32)
-          if (bi == 0xffffffffu || v[e] > bv) { bv = v[e]; bi = e; }
-        for (int o = 16; o > 0; o >>= 1) {
-          const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-          const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (i2 != 0xffffffffu && (bi == 0xffffffffu || v2 > bv || (v2 == bv && i2 < bi))) { bv = v2; bi = i2; }
-        }
-        return bi;
-      };
-      uint32_t tt = 0;
-      if (supplied) {
-        head = argmax_first(sm->np[t]);
-        kind = has(ntop, head) ? 0 : (has(nact, head) ? 1 : 2);
-        for (uint32_t e = lane; e < E; e += 32) {
-          const double v = sm->np[t][e];
-          if (sm->merged[e] < v) sm->merged[e] = v;
-        }
-      } else {
-        const uint32_t n_top = __popcll(ntop);
-        if (rng_double(rs) < cfg.p_top && n_top > 0) {
-          const uint32_t pick = rng_below_small(rs, n_top);
-          uint32_t c = 0;
-          head = 0;
-          for (uint32_t r = 0; r < k; ++r) {
-            const uint32_t e = nx->order[t][r];
-            if (has(ntop, e)) { if (c == pick) { head = e; break; } ++c; }
-          }
-          kind = 0;
-        } else {
-          const uint64_t lows = nact & ~ntop;
-          const uint32_t n_low = __popcll(lows);
-          if (rng_double(rs) < cfg.p_active && n_low > 0) {
-            const uint32_t pick = rng_below_small(rs, n_low);
-            uint32_t c = 0;
-            head = 0;
-            for (uint32_t r = 0; r < k; ++r) {
-              const uint32_t e = nx->order[t][r];
-              if (has(lows, e)) { if (c == pick) { head = e; break; } ++c; }
-            }
-            kind = 1;
-          } else {
-            const uint64_t allm = E >= 64 ? ~0ULL : ((1ULL << E) - 1ULL);
-            const uint64_t inact = allm & ~nact;
-            uint32_t pick = rng_below_small(rs, __popcll(inact));
-            uint64_t m = inact;
-            for (uint32_t i = 0; i < pick; ++i) m &= m - 1;
-            head = __ffsll((long long)m) - 1;
-            kind = 2;
-          }
-        }
-        tt = argmax_first(tn);
-        for (uint32_t e = lane; e < E; e += 32) {
-          const double v = (e == head) ? tn[tt] : ((e == tt) ? tn[head] : tn[e]);
-          if (sm->merged[e] < v) sm->merged[e] = v;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        Counters& c = st->c;
-        if (supplied) c.trace_supplied++; else c.draws++;
-        if (kind == 0) c.head_top++; else if (kind == 1) c.head_active++; else c.head_inactive++;
-      }
-      __syncwarp();
-    }
-    if (lane == 0) { st->rng[0] = rs[0]; st->rng[1] = rs[1]; st->rng[2] = rs[2]; st->rng[3] = rs[3]; }
-    // build_queue (prefetch.cpp:85-115): rank merged, first `depth` non-resident
-    __shared__ uint8_t qorder[kMaxE];
-    for (uint32_t e = lane; e < E; e += 32) {
-      const double v = sm->merged[e];
-      uint32_t r = 0;
-      for (uint32_t j = 0; j < E; ++j) {
-        const double vj = sm->merged[j];
-        r += (vj > v) || (vj == v && j < e);
-      }
-      qorder[r] = (uint8_t)e;
-    }
-    __syncwarp();
+    if (nw < 2) predict_queue_warp(cx, sm, nx);  // else warp 1 ran it concurrently
+    else asm volatile("bar.sync 2, 64;" ::: "memory");
+    const uint8_t* qorder = sm->qorder;
     const uint64_t tmask = tls->mask;
     uint32_t qn = 0;
     uint8_t qe[kMaxE];

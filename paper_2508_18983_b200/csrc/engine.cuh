@@ -75,6 +75,7 @@ struct EngineState {
   uint64_t ffn_bytes;              // algorithmic FFN bytes planned (stack mode)
   uint64_t ffn_launches;
   uint64_t prof[16];               // phase timers of the decision launch (ns, summed)
+  uint64_t ack_cache;              // last mailbox acknowledgement seen (stack mode)
 };
 
 // Log records (layouts == moeb_task / moeb_window / moeb_eviction).
@@ -146,6 +147,7 @@ struct DecideSmem {
   double np[kMaxB][kMaxE];   // supplied predictions (optional)
   double merged[kMaxE];
   double mean[kMaxE];
+  uint8_t qorder[kMaxE];     // merged-prediction ranking of the prefetch target
   double avg[kMaxE];         // window averages of the executing layer (this step)
   double tavg[kMaxE];        // ... of the prefetch target layer
   uint8_t order[kMaxB][kMaxE];

@@ -30,6 +30,7 @@
 #include "engine_host.h"
 #include "host_common.h"
 #include "layer.cuh"
+#include "ffn_tma.cuh"
 #include "weights.cuh"
 
 namespace moeb {
@@ -136,6 +137,11 @@ struct DecideKSmem {
   uint32_t n_cmds;
   uint64_t it, seq;
   int last;
+  // uploads published early by EarlyPublish (ids + destinations)
+  uint32_t load_id[kMaxE], cpu_id[kMaxE];
+  uint16_t* load_dst[kMaxE];
+  uint16_t* cpu_dst[kMaxE];
+  int8_t stage_of[kMaxE];
 };
 
 __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const volatile uint64_t* p) {
@@ -148,6 +154,40 @@ __device__ __forceinline__ uint16_t* slot_ptr(const DecideArgs& a, uint32_t laye
   return a.slots + ((size_t)layer * a.slots_alloc + (uint32_t)slot) * a.expert_elems;
 }
 
+// Copy several global segments into shared memory with every load issued
+// before any store (one memory latency for the whole staging phase).
+struct StageSeg {
+  uint64_t* dst;
+  const uint64_t* src;
+  uint32_t words;
+};
+__device__ inline void stage_gather(const StageSeg* segs, int nseg) {
+  constexpr int kPer = 20;
+  uint32_t total = 0;
+  for (int i = 0; i < nseg; ++i) total += segs[i].words;
+  for (uint32_t base = 0; base < total; base += kPer * blockDim.x) {
+    uint64_t v[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      uint32_t i = base + threadIdx.x + k * blockDim.x;
+      if (i < total) {
+        int sgi = 0;
+        while (i >= segs[sgi].words) { i -= segs[sgi].words; ++sgi; }
+        v[k] = segs[sgi].src[i];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      uint32_t i = base + threadIdx.x + k * blockDim.x;
+      if (i < total) {
+        int sgi = 0;
+        while (i >= segs[sgi].words) { i -= segs[sgi].words; ++sgi; }
+        segs[sgi].dst[i] = v[k];
+      }
+    }
+  }
+}
+
 template <class T>
 __device__ __forceinline__ void cta_copy(T* dst, const T* src) {
   static_assert(sizeof(T) % 8 == 0, "8-byte granular");
@@ -155,6 +195,81 @@ __device__ __forceinline__ void cta_copy(T* dst, const T* src) {
   uint64_t* d = reinterpret_cast<uint64_t*>(dst);
   for (uint32_t i = threadIdx.x; i < sizeof(T) / 8; i += blockDim.x) d[i] = s[i];
 }
+
+// The copy thread acknowledges mailbox entries in order; the device only
+// re-reads the (PCIe-mapped) acknowledgement when its cached copy is too old.
+__device__ __forceinline__ void wait_ring_slot(const DecideArgs& a, uint64_t mseq, uint64_t* ack_cache) {
+  if (mseq <= kRing || *ack_cache >= mseq - kRing) return;
+  const uint64_t t0 = globaltimer_ns();
+  for (;;) {
+    *ack_cache = ld_acquire_sys_u64(a.host_ack);
+    if (*ack_cache >= mseq - kRing) break;
+    __nanosleep(500);
+    if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 4u); break; }
+  }
+}
+
+// Mailbox entry A of a layer-step (sequence 2*seq-1): the demand loads and
+// BA-streamed experts, published from inside the decision step the moment
+// the lists are final. Entry B (2*seq) carries the prefetches later.
+struct EarlyPublish {
+  const DecideArgs* a;
+  DecideKSmem* sm;
+  __device__ void operator()(DecideSmem* d, uint32_t n_load, uint32_t n_cpu) const {
+    if (lane_id() == 0) {
+      const DecideArgs& A = *a;
+      const uint64_t mseq = 2 * sm->seq - 1;
+      MailEntry* me = &A.ring[mseq % kRing];
+      wait_ring_slot(A, mseq, &sm->st.ack_cache);
+      EngineState* st = &sm->st;
+      LayerState* ls = &sm->ls;
+      const uint32_t layer = A.layer, E = sm->cfg.E;
+      uint32_t si = 0, n = 0;
+      for (uint32_t e = 0; e < E; ++e) sm->stage_of[e] = -1;
+      auto cmd = [&](uint32_t e, uint16_t* dst) {
+        const uint32_t id = ++st->next_copy;
+        MailCmd c;
+        c.src_off = ((uint64_t)layer * E + e) * A.expert_elems * 2;
+        c.dst = (uint64_t)dst;
+        c.bytes = A.expert_elems * 2;
+        c.id = id;
+        c.wait_ffn = 0;
+        me->cmd[n++] = c;
+        return id;
+      };
+      for (uint32_t i = 0; i < n_load; ++i) {
+        const uint32_t e = d->out.load[i];
+        const int slot = d->out.load_slot[i];
+        uint16_t* dst;
+        if (slot >= 0) {
+          dst = slot_ptr(A, layer, slot);
+        } else {
+          sm->stage_of[e] = (int8_t)si;
+          dst = A.staging + (size_t)(si++ % A.n_stage) * A.expert_elems;
+        }
+        const uint32_t id = cmd(e, dst);
+        if (slot >= 0) ls->slot_copy[slot] = id;
+        sm->load_id[i] = id;
+        sm->load_dst[i] = dst;
+      }
+      for (uint32_t i = 0; i < n_cpu; ++i) {
+        uint16_t* dst = A.staging + (size_t)(si++ % A.n_stage) * A.expert_elems;
+        sm->cpu_id[i] = cmd(d->out.cpu[i], dst);
+        sm->cpu_dst[i] = dst;
+      }
+      me->n = n;
+#ifdef MOEB_PROFILE_PHASES
+      const uint64_t tf0 = gtimer();
+#endif
+      __threadfence_system();
+      me->seq = mseq;
+#ifdef MOEB_PROFILE_PHASES
+      st->prof[13] += gtimer() - tf0;
+#endif
+    }
+    __syncwarp();
+  }
+};
 
 // Thread 0 builds the FFN plan and the upload commands in shared memory.
 __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
@@ -173,25 +288,7 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
     itm.wait = wait;
     itm.kind = kind;
     itm.expert = e;
-    uint32_t n = 0;
-    for (uint32_t t = 0; t < B; ++t) {
-      bool sel = kind == 0;
-      if (!sel)
-        for (uint32_t i = 0; i < d->nsel[t]; ++i) sel |= d->sel[t][i] == e;
-      if (!sel) continue;
-      float wt;
-      if (kind == 0) {
-        wt = a.shared_gate ? sm->sg[t] : 1.0f;
-      } else {
-        wt = sm->sc[t][e];
-        if (a.renormalize) wt = __fdiv_rn(wt, sm->denom[t]);
-        wt = __fmul_rn(wt, a.routed_scale);
-      }
-      itm.tok[n] = (uint8_t)t;
-      itm.wt[n] = wt;
-      ++n;
-    }
-    itm.n_tok = n;
+    itm.n_tok = 0;  // token lists are filled in parallel afterwards (fill_items)
   };
   auto add_cmd = [&](uint32_t src_layer, uint32_t e, uint16_t* dst, uint32_t wait_ffn) -> uint32_t {
     const uint32_t id = ++st->next_copy;
@@ -223,29 +320,9 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
     while (j > n_ready && p->items[j - 1].wait > x.wait) { p->items[j] = p->items[j - 1]; --j; }
     p->items[j] = x;
   }
-  uint32_t si = 0;
-  int8_t stage_of[kMaxE];
-  for (uint32_t e = 0; e < E; ++e) stage_of[e] = -1;
-  for (uint32_t i = 0; i < out.n_load; ++i) {
-    const uint32_t e = out.load[i];
-    const int slot = out.load_slot[i];
-    uint16_t* dst;
-    if (slot >= 0) {
-      dst = slot_ptr(a, layer, slot);
-    } else {
-      stage_of[e] = (int8_t)si;
-      dst = a.staging + (size_t)(si++ % a.n_stage) * a.expert_elems;
-    }
-    const uint32_t id = add_cmd(layer, e, dst, 0);
-    if (slot >= 0) ls->slot_copy[slot] = id;
-    add_item(dst, a.F, id, 2, e);
-  }
-  for (uint32_t i = 0; i < out.n_cpu; ++i) {
-    const uint32_t e = out.cpu[i];
-    uint16_t* dst = a.staging + (size_t)(si++ % a.n_stage) * a.expert_elems;
-    const uint32_t id = add_cmd(layer, e, dst, 0);
-    add_item(dst, a.F, id, 3, e);
-  }
+  for (uint32_t i = 0; i < out.n_load; ++i) add_item(sm->load_dst[i], a.F, sm->load_id[i], 2, out.load[i]);
+  for (uint32_t i = 0; i < out.n_cpu; ++i) add_item(sm->cpu_dst[i], a.F, sm->cpu_id[i], 3, out.cpu[i]);
+  const int8_t* stage_of = sm->stage_of;
   uint32_t n_d2d = 0;
   for (uint32_t i = 0; i < out.n_def; ++i) {
     const uint32_t e = out.def_e[i];
@@ -279,17 +356,61 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
   sm->n_cmds = n_cmds;
 }
 
+// Token lists and combine weights of every plan item, one thread per item.
+__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm) {
+  const uint32_t B = sm->cfg.B;
+  const DecideSmem* d = &sm->d;
+  Plan* p = &sm->plan;
+  for (uint32_t ii = threadIdx.x; ii < p->n_items; ii += blockDim.x) {
+    Item& itm = p->items[ii];
+    const uint32_t kind = itm.kind, e = itm.expert;
+    uint32_t n = 0;
+    for (uint32_t t = 0; t < B; ++t) {
+      bool sel = kind == 0;
+      if (!sel)
+        for (uint32_t i = 0; i < d->nsel[t]; ++i) sel |= d->sel[t][i] == e;
+      if (!sel) continue;
+      float wt;
+      if (kind == 0) {
+        wt = a.shared_gate ? sm->sg[t] : 1.0f;
+      } else {
+        wt = sm->sc[t][e];
+        if (a.renormalize) wt = __fdiv_rn(wt, sm->denom[t]);
+        wt = __fmul_rn(wt, a.routed_scale);
+      }
+      itm.tok[n] = (uint8_t)t;
+      itm.wt[n] = wt;
+      ++n;
+    }
+    itm.n_tok = n;
+  }
+}
+
 // Router gate (all CTAs) then, in the last CTA to finish, the decision step,
 // the FFN plan and the upload mailbox. One launch per layer.
 __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideArgs ga) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const uint64_t t_entry = gtimer();
+#ifdef MOEB_PROFILE_PHASES
+#define MOEB_T(x) const uint64_t x = gtimer()
+#else
+#define MOEB_T(x) const uint64_t x = 0
+#endif
+  // PDL: wait for the previous layer's FFN (x, plan buffers), then let the
+  // next kernel's CTAs start launching as ours retire
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+  MOEB_T(t_entry);
+  __shared__ uint64_t t_plan_g_s;
+  uint64_t& t_plan_g = t_plan_g_s;
   // gate phase: us [B][d] bf16 aliases the decision workspace
   gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw));
-  const uint64_t t_gate = gtimer();
+  MOEB_T(t_gate);
   DecideKSmem* sm = reinterpret_cast<DecideKSmem*>(smem_raw);
   __shared__ int s_last;
   __syncthreads();
+#ifdef MOEB_PROFILE_PHASES
+  if (threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(&ga.d.st->prof[14]), (unsigned long long)t_entry);
+#endif
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t t = atomicAdd(ga.ticket, 1u);
@@ -303,7 +424,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   if (!s_last) return;
 
   const DecideArgs& a = ga.d;
-  const uint64_t t_elect = gtimer();
+  MOEB_T(t_elect);
   const int warp = warp_id(), lane = lane_id();
   const uint32_t nw = blockDim.x >> 5;
   // stage the step's state: one parallel load phase (it / seq come from the
@@ -317,15 +438,46 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   const bool want_next = a.cfg.pre && has_target && a.trace;
   const bool smem_hist = a.cfg.window * E <= kMaxHistSmem;
   const size_t hwords = (size_t)a.cfg.window * E;
-  cta_copy(&sm->st, a.st);
-  cta_copy(&sm->cfg, &a.cfg);
-  cta_copy(&sm->ls, &a.layers[layer]);
-  if (smem_hist)
-    for (uint32_t i = threadIdx.x; i < hwords; i += blockDim.x) sm->hist[i] = a.hist[layer * hwords + i];
-  if (want_next && tl != layer) {
-    cta_copy(&sm->tls, &a.layers[tl]);
-    if (smem_hist)
-      for (uint32_t i = threadIdx.x; i < hwords; i += blockDim.x) sm->thist[i] = a.hist[tl * hwords + i];
+  {
+    // every staging load is issued before any store: one memory latency
+    static_assert(sizeof(EngineState) / 8 <= kGdThreads && sizeof(LayerState) / 8 <= kGdThreads, "staging");
+    constexpr uint32_t kStW = sizeof(EngineState) / 8, kLsW = sizeof(LayerState) / 8;
+    constexpr int kHw = kMaxHistSmem / kGdThreads;  // ring words per thread
+    const uint32_t tid = threadIdx.x;
+    const bool two = want_next && tl != layer;
+    const uint64_t* g_st = reinterpret_cast<const uint64_t*>(a.st);
+    const uint64_t* g_ls = reinterpret_cast<const uint64_t*>(&a.layers[layer]);
+    const uint64_t* g_tls = reinterpret_cast<const uint64_t*>(&a.layers[tl]);
+    const uint64_t* g_h = reinterpret_cast<const uint64_t*>(a.hist + layer * hwords);
+    const uint64_t* g_th = reinterpret_cast<const uint64_t*>(a.hist + tl * hwords);
+    uint64_t r_st = 0, r_ls = 0, r_tls = 0, r_h[kHw], r_th[kHw];
+    if (tid < kStW) r_st = g_st[tid];
+    if (tid < kLsW) r_ls = g_ls[tid];
+    if (two && tid < kLsW) r_tls = g_tls[tid];
+    if (smem_hist) {
+#pragma unroll
+      for (int k = 0; k < kHw; ++k) {
+        const uint32_t i = tid + k * kGdThreads;
+        if (i < hwords) {
+          r_h[k] = g_h[i];
+          if (two) r_th[k] = g_th[i];
+        }
+      }
+    }
+    if (tid < kStW) reinterpret_cast<uint64_t*>(&sm->st)[tid] = r_st;
+    if (tid < kLsW) reinterpret_cast<uint64_t*>(&sm->ls)[tid] = r_ls;
+    if (two && tid < kLsW) reinterpret_cast<uint64_t*>(&sm->tls)[tid] = r_tls;
+    if (smem_hist) {
+#pragma unroll
+      for (int k = 0; k < kHw; ++k) {
+        const uint32_t i = tid + k * kGdThreads;
+        if (i < hwords) {
+          reinterpret_cast<uint64_t*>(sm->hist)[i] = r_h[k];
+          if (two) reinterpret_cast<uint64_t*>(sm->thist)[i] = r_th[k];
+        }
+      }
+    }
+    if (threadIdx.x == 0) sm->cfg = a.cfg;
   }
   const uint32_t jobs = want_next ? 2 * B : B;
   for (uint32_t j = warp; j < jobs; j += nw) {
@@ -357,7 +509,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     if (a.scores_log && a.seq <= a.rec_cap) a.scores_log[((a.seq - 1) * B + t) * E + e] = sm->sc[t][e];
   }
   __syncthreads();
-  const uint64_t t_staged = gtimer();
+  MOEB_T(t_staged);
 
   StepCtx cx;
   cx.cfg = &cfg;
@@ -379,9 +531,9 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     rec = a.recs + (sm->seq - 1);
     toks = a.toks + (sm->seq - 1) * B;
   }
-  decide_step(cx, &sm->d, &sm->n, &sm->s, rec, toks);
+  decide_step(cx, &sm->d, &sm->n, &sm->s, rec, toks, EarlyPublish{&a, sm});
   __syncthreads();
-  const uint64_t t_decided = gtimer();
+  MOEB_T(t_decided);
 
   // combine-weight denominators (Mixtral renormalisation), FFN counters
   if (threadIdx.x < B) {
@@ -394,21 +546,24 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   __syncthreads();
   if (threadIdx.x == 0) {
     build_plan(a, sm);
-    // the ring slot must have been consumed by the copy thread
-    const uint64_t t0 = globaltimer_ns();
-    while (sm->seq > kRing && ld_acquire_sys_u64(a.host_ack) < sm->seq - kRing) {
-      __nanosleep(500);
-      if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 4u); break; }
-    }
-    sm->st.prof[11] += globaltimer_ns() - t0;
+    // entry B's ring slot must have been consumed by the copy thread
+    wait_ring_slot(a, 2 * sm->seq, &sm->st.ack_cache);
     sm->st.seq = sm->seq;
     if (layer == L - 1) sm->st.it = it + 1;
-    const uint64_t t_plan = gtimer();
+  }
+  __syncthreads();
+  fill_items(a, sm);
+  if (threadIdx.x == 0) {
+    MOEB_T(t_plan);
+    t_plan_g = t_plan;
+#ifdef MOEB_PROFILE_PHASES
     sm->st.prof[0] += t_gate - t_entry;
     sm->st.prof[1] += t_elect - t_gate;
     sm->st.prof[2] += t_staged - t_elect;
     sm->st.prof[3] += t_decided - t_staged;
     sm->st.prof[9] += t_plan - t_decided;
+#endif
+    (void)t_entry; (void)t_gate; (void)t_elect; (void)t_staged; (void)t_decided; (void)t_plan;
   }
   __syncthreads();
   // publish: plan -> global, commands -> mapped host ring, state write-back
@@ -421,7 +576,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + sm->plan.n_d2d * sizeof(D2D) / 8;
     for (uint32_t i = d0 + threadIdx.x; i < d1; i += blockDim.x) dst[i] = src[i];
-    MailEntry* me = &a.ring[sm->seq % kRing];
+    MailEntry* me = &a.ring[(2 * sm->seq) % kRing];
     const uint32_t nc = sm->n_cmds;
     const uint64_t* cs = reinterpret_cast<const uint64_t*>(sm->cmd);
     uint64_t* cd = reinterpret_cast<uint64_t*>(me->cmd);
@@ -435,10 +590,43 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint64_t t0 = gtimer();
+    MOEB_T(t_pub0);
     __threadfence_system();
-    a.ring[sm->seq % kRing].seq = sm->seq;
-    atomicAdd(reinterpret_cast<unsigned long long*>(&a.st->prof[10]), (unsigned long long)(gtimer() - t0));
+    a.ring[(2 * sm->seq) % kRing].seq = 2 * sm->seq;
+#ifdef MOEB_PROFILE_PHASES
+    const uint64_t t_pub1 = gtimer();
+    a.st->prof[10] += t_pub1 - t_pub0;
+    a.st->prof[12] += t_pub0 - t_plan_g;
+    const uint64_t first = a.st->prof[14];
+    a.st->prof[15] += t_entry - first;       // start skew of the deciding CTA
+    a.st->prof[11] += t_pub1 - first;        // first CTA start -> publish done
+    a.st->prof[14] = ~0ull;
+#endif
+    (void)t_pub0;
+  }
+  // warm L2 with the next layer's state (the FFN streams ~140 MB of weights
+  // through L2 with evict-first in between): layer state, score ring, and
+  // the next routing logits row
+  {
+    const uint32_t nl = tl, nl2 = (tl + 1 == L) ? 0 : tl + 1;
+    const char* regions[3] = {reinterpret_cast<const char*>(&a.layers[nl]),
+                              reinterpret_cast<const char*>(a.hist + nl * hwords),
+                              reinterpret_cast<const char*>(&a.layers[nl2])};
+    const uint32_t sizes[3] = {(uint32_t)sizeof(LayerState), (uint32_t)(hwords * 8), (uint32_t)sizeof(LayerState)};
+    uint32_t line = threadIdx.x;
+    for (int r = 0; r < 3; ++r) {
+      const uint32_t nlines = (sizes[r] + 127) / 128;
+      if (line < nlines) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(regions[r] + line * 128));
+        break;
+      }
+      line -= nlines;
+    }
+    if (a.trace && threadIdx.x < 2) {
+      const uint64_t nit = (tl == 0) ? it + 1 : it;
+      const float* row = a.trace + (((nit % a.trace_steps) * L + tl) * B) * E;
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(row) + threadIdx.x * 128));
+    }
   }
 }
 
@@ -481,12 +669,14 @@ struct moeb_stack {
   std::atomic<int> copier_error{0};
   std::string copier_msg;
   int ffn_grid = 0;
-  void (*ffn_fn)(FfnArgs) = nullptr;
+  void (*ffn_fn)(FfnTArgs) = nullptr;
+  uint32_t ffn_stages = 0, ffn_stage_bytes = 0, ffn_hbuf = 0;
   size_t ffn_smem = 0, gd_smem = 0;
   DevBuf<uint32_t> ticket;
   MailEntry* ring_dev = nullptr;
   uint64_t* ack_dev = nullptr;
   uint64_t host_it = 0, host_seq = 0;  // mirrors of EngineState::it / seq
+  uint64_t n_launch_layers = 0;        // (gate+decide, FFN) launch pairs
   std::mutex io_mu;
   IoAcc io;
   static constexpr int kEv = 512;
@@ -614,14 +804,13 @@ static void synth(uint16_t* dst, uint64_t n, uint64_t seed, uint64_t tensor, uin
   MOEB_CUDA(cudaGetLastError());
 }
 
-using FfnFn = void (*)(FfnArgs);
+using FfnFn = void (*)(FfnTArgs);
 static FfnFn ffn_kernel_for(uint32_t B) {
-  if (B <= 1) return ffn_kernel<1>;
-  if (B <= 2) return ffn_kernel<2>;
-  if (B <= 4) return ffn_kernel<4>;
-  if (B <= 8) return ffn_kernel<8>;
-  if (B <= 16) return ffn_kernel<16>;
-  return ffn_kernel<32>;
+  if (B <= 1) return ffn_tma_kernel<1>;
+  if (B <= 4) return ffn_tma_kernel<4>;
+  if (B <= 8) return ffn_tma_kernel<8>;
+  if (B <= 16) return ffn_tma_kernel<16>;
+  return ffn_tma_kernel<32>;
 }
 
 static float fan_scale(uint32_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
@@ -641,6 +830,8 @@ static void reset_state(moeb_stack* S, cudaStream_t s) {
   rng_seed(st.rng, derive_seed(S->cfg.seed, 0x94ed1c70ULL));  // pipeline.cpp:62
   st.seq = prev.seq;
   st.next_copy = prev.next_copy;
+  st.ack_cache = prev.ack_cache;
+  st.prof[14] = ~0ull;  // running minimum of CTA start times (phase profiling)
   S->hist.zero(s);
   MOEB_CUDA(cudaMemcpyAsync(S->st.p, &st, sizeof st, cudaMemcpyHostToDevice, s));
   MOEB_CUDA(cudaMemcpyAsync(S->layers.p, ls.data(), L * sizeof(LayerState), cudaMemcpyHostToDevice, s));
@@ -766,7 +957,27 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   MOEB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->ack), 64, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(S->ack, 0, 64);
   // kernel resources
-  S->ffn_smem = (size_t)B * d * 2;
+  // FFN ring: 64 KB stages (8 row pairs at d=2048), as many as fit beside
+  // u [B][d] and the h staging buffer
+  {
+    const uint32_t Fm = std::max(F, Sh);
+    (void)Fm;
+    S->ffn_stage_bytes = 64 * 1024;  // 8 gate+up row pairs at d = 2048
+    const size_t ubytes = (((size_t)B * d * (B <= 4 ? 4 : 2)) + 15) & ~(size_t)15;
+    // h of the ready items (shared + top-k experts x tokens) staged in smem
+    // when it fits beside two ring stages; otherwise read from L2
+    const size_t hwant = ((size_t)Sh + (size_t)cfg.top_k * F) * B * 4;
+    const size_t room = 220 * 1024 - ubytes - kPlanSmem - 2 * (size_t)S->ffn_stage_bytes;
+    S->ffn_hbuf = (uint32_t)(hwant <= room ? hwant : 0);
+    const size_t budget = 220 * 1024 - ubytes - kPlanSmem - S->ffn_hbuf;
+    S->ffn_stages = (uint32_t)std::min<size_t>(kMaxStages, budget / S->ffn_stage_bytes);
+    if (S->ffn_stages < 2) {
+      S->ffn_stage_bytes /= 2;
+      S->ffn_stages = (uint32_t)std::min<size_t>(kMaxStages, budget / S->ffn_stage_bytes);
+    }
+    if (S->ffn_stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
+    S->ffn_smem = (size_t)S->ffn_stages * S->ffn_stage_bytes + ubytes + kPlanSmem + S->ffn_hbuf;
+  }
   S->ticket.alloc(1);
   S->ticket.zero(s);
   MOEB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->ring_dev), S->ring, 0));
@@ -781,13 +992,37 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   MOEB_CUDA(cudaFuncSetAttribute(S->ffn_fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int sms = 0, occ = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  MOEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->ffn_fn, kFfnThreads, S->ffn_smem));
-  if (occ < 1) throw Error(5, "ffn_kernel does not fit on an SM");
-  S->ffn_grid = sms * occ;
-  const uint32_t nW = (uint32_t)S->ffn_grid * kFfnWarps;
-  if ((d + nW - 1) / nW > (uint32_t)kMaxRowsPerWarp) throw Error(1, "model: d_model too large for the FFN grid");
+  MOEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->ffn_fn, kFfnTThreads, S->ffn_smem));
+  if (occ < 1) throw Error(5, "ffn kernel does not fit on an SM");
+  S->ffn_grid = sms;  // one persistent CTA per SM (the per-item counters need co-residency)
+  if ((d + sms - 1) / sms > (uint32_t)kMaxDnRowsPerCta) throw Error(1, "model: d_model too large for the FFN grid");
   MOEB_CUDA(cudaStreamSynchronize(s));
   S->copier = std::thread([S] { S->copy_loop(); });
+}
+
+// Programmatic dependent launch: the next per-layer kernel is scheduled while
+// the current one drains (each kernel opens with griddepcontrol.wait, so
+// data dependences are unchanged), hiding the grid launch latency between
+// the gate+decide and FFN kernels of every layer.
+// Measured on B200: PDL between these two kernels made each layer slower
+// (the FFN grid needs every SM and the decision CTA holds one), so it is
+// off; the griddepcontrol instructions are no-ops without it.
+constexpr bool kUsePdl = false;
+
+template <class Args>
+static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args* args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = kUsePdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* kargs[] = {args};
+  MOEB_CUDA(cudaLaunchKernelExC(&cfg, fn, kargs));
 }
 
 static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaStream_t user) {
@@ -844,11 +1079,12 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.seq = ++S->host_seq;
     ga.ticket = S->ticket.p;
     if (S->timing) S->tick(s);
-    gate_decide_kernel<<<(rows + 1) / 2, kGdThreads, S->gd_smem, s>>>(ga);
+    launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3((rows + 1) / 2), dim3(kGdThreads),
+               S->gd_smem, s, &ga);
     MOEB_CUDA(cudaGetLastError());
     if (S->timing) S->tick(s);
 
-    FfnArgs f{};
+    FfnTArgs f{};
     f.plan = S->plan.p;
     f.u = S->u.p;
     f.x_in = S->hidden.p + (size_t)cur * B * d;
@@ -861,10 +1097,13 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     f.B = B;
     f.d = d;
     f.Fmax = std::max(S->F, S->S);
-    const uint32_t nW = (uint32_t)S->ffn_grid * kFfnWarps;
-    f.rows_per_warp = (d + nW - 1) / nW;
+    f.stages = S->ffn_stages;
+    f.stage_bytes = S->ffn_stage_bytes;
+    f.hbuf_bytes = S->ffn_hbuf;
     void* fargs[] = {&f};
-    MOEB_CUDA(cudaLaunchKernel(S->ffn_fn, dim3(S->ffn_grid), dim3(kFfnThreads), fargs, S->ffn_smem, s));
+    launch_pdl(reinterpret_cast<const void*>(S->ffn_fn), dim3(S->ffn_grid), dim3(kFfnTThreads), S->ffn_smem, s, &f);
+    (void)fargs;
+    S->n_launch_layers += 1;
     MOEB_CUDA(cudaGetLastError());
     if (S->timing) S->tick(s);
     cur ^= 1;
@@ -1018,14 +1257,14 @@ int moeb_get_kernel_stats(moeb_stack* s, moeb_kernel_stats* out) {
     *out = moeb_kernel_stats{};
     out->route_ms = s->kern_ms[0];
     out->ffn_ms = s->kern_ms[1];
-    out->route_launches = s->kern_n[0];
-    out->ffn_launches = s->kern_n[1];
+    out->route_launches = s->n_launch_layers;
+    out->ffn_launches = s->n_launch_layers;
     out->ffn_bytes = st.ffn_bytes;
     out->ffn_planned = st.ffn_launches;
     for (int i = 0; i < 16; ++i) out->prof_ns[i] = st.prof[i];
     const uint64_t gb = (uint64_t)s->E * s->d * 2 + 2ull * s->B * s->d * 2 + (uint64_t)s->B * (s->E + 1) * 4 +
                         (s->model.shared_gate ? (uint64_t)s->d * 2 : 0);
-    out->route_bytes = gb * s->kern_n[0];
+    out->route_bytes = gb * s->n_launch_layers;
   });
 }
 
@@ -1034,6 +1273,7 @@ int moeb_reset_kernel_stats(moeb_stack* s) {
     MOEB_CUDA(cudaStreamSynchronize(s->stream));
     if (s->timing) s->tk_harvest_all();
     for (int k = 0; k < 2; ++k) { s->kern_ms[k] = 0; s->kern_n[k] = 0; }
+    s->n_launch_layers = 0;
     EngineState st;
     MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
     st.ffn_bytes = 0;

@@ -51,8 +51,8 @@ def main():
               "ms/token wall", round(dt * 1e3 / T, 3))
         n = k["route_launches"] or 1
         names = ["gate", "elect", "stage", "decide", "d:classify", "d:route", "d:hits+record", "d:loads",
-                 "d:prefetch", "plan", "publish", "ring_wait"]
-        print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names)})
+                 "d:prefetch", "plan", "pub:fence", "span", "pub:copy", "early:fence", "-", "start_skew"]
+        print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names) if nm != "-"})
     st.close()
 
 
