@@ -93,9 +93,10 @@ int moeb_route(const double* scores, uint32_t B, uint32_t E, const uint8_t* resi
                uint32_t* top_set, uint32_t* n_top_set, uint32_t* pending, uint32_t* n_pending);
 
 /* coalesce_for_batching over an existing RouteResult (in/out arrays as
- * moeb_route's outputs). */
+ * moeb_route's outputs); thresholds: per token {beta, T, L, R} of the
+ * RouteResult's Classification, used exactly as given. */
 int moeb_coalesce(const double* scores, uint32_t B, uint32_t E, const uint8_t* resident_mask,
-                  uint32_t k, double alpha, uint32_t* sel, uint32_t* n_sel, uint32_t* sub,
+                  uint32_t k, const double* thresholds, uint32_t* sel, uint32_t* n_sel, uint32_t* sub,
                   uint32_t* n_sub, uint32_t* kept, uint32_t* n_kept, const uint32_t* top_set,
                   uint32_t n_top_set, uint32_t* pending, uint32_t* n_pending);
 

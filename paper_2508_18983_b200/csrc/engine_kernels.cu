@@ -117,7 +117,9 @@ struct RouteIO {
   uint8_t nsel[kMaxB], nsub[kMaxB], nkept[kMaxB];
   uint64_t C;
   uint64_t pending;
-  // classify outputs for token 0 (moeb_classify)
+  // mode 2: the caller's per-token thresholds {beta, T, L, R} (the bands a
+  // RouteResult was classified with); classify outputs for token 0 (mode 3/4)
+  double thr_tok[kMaxB][4];
   double thr[4];
   uint8_t order[kMaxE];
   uint64_t act, top, low, alt;
@@ -145,6 +147,22 @@ __global__ void __launch_bounds__(kThreads, 1) route_kernel(const double* scores
     }
   }
   __syncthreads();
+  if (mode == 2) {
+    // re-derive the bands from the given thresholds, exactly as classified
+    for (uint32_t t = warp; t < B; t += kWarps) {
+      const double b = io->thr_tok[t][0], T = io->thr_tok[t][1], Lb = io->thr_tok[t][2], R = io->thr_tok[t][3];
+      bool l0 = false, l1 = false, a0 = false, a1 = false;
+      const uint32_t e0 = lane, e1 = lane + 32;
+      if (e0 < E) { const double s0 = d->s[t][e0]; l0 = has(d->act[t], e0) && b > 0.0 && s0 >= Lb && s0 < T; a0 = !has(d->act[t], e0) && b > 0.0 && s0 >= R && s0 < Lb; }
+      if (e1 < E) { const double s1 = d->s[t][e1]; l1 = has(d->act[t], e1) && b > 0.0 && s1 >= Lb && s1 < T; a1 = !has(d->act[t], e1) && b > 0.0 && s1 >= R && s1 < Lb; }
+      const uint64_t low = ballot64(l0, l1), alt = ballot64(a0, a1);
+      if (lane == 0) {
+        d->low[t] = low; d->alt[t] = alt; d->top[t] = d->act[t] & ~low;
+        d->beta[t] = b; d->thT[t] = T; d->thL[t] = Lb; d->thR[t] = R;
+      }
+    }
+    __syncthreads();
+  }
   if (mode == 3 || mode == 4) {
     if (threadIdx.x == 0) {
       io->thr[0] = d->beta[0]; io->thr[1] = d->thT[0]; io->thr[2] = d->thL[0]; io->thr[3] = d->thR[0];
@@ -805,7 +823,7 @@ int moeb_route(const double* scores, uint32_t B, uint32_t E, const uint8_t* resi
 }
 
 int moeb_coalesce(const double* scores, uint32_t B, uint32_t E, const uint8_t* resident_mask,
-                  uint32_t k, double alpha, uint32_t* sel, uint32_t* n_sel, uint32_t* sub,
+                  uint32_t k, const double* thresholds, uint32_t* sel, uint32_t* n_sel, uint32_t* sub,
                   uint32_t* n_sub, uint32_t* kept, uint32_t* n_kept, const uint32_t* top_set,
                   uint32_t n_top_set, uint32_t* pending, uint32_t* n_pending) {
   return guarded([&] {
@@ -823,8 +841,10 @@ int moeb_coalesce(const double* scores, uint32_t B, uint32_t E, const uint8_t* r
       }
     }
     for (uint32_t i = 0; i < n_top_set; ++i) io.C |= 1ULL << top_set[i];
+    for (uint32_t t = 0; t < B; ++t)
+      for (int j = 0; j < 4; ++j) io.thr_tok[t][j] = thresholds[t * 4 + j];
     if (B == 0) { *n_pending = 0; return; }
-    run_route(scores, B, E, resident_mask, k, alpha, 2, io);
+    run_route(scores, B, E, resident_mask, k, 0.0, 2, io);
     export_route(io, B, k, sel, n_sel, sub, n_sub, kept, n_kept, nullptr, nullptr, pending, n_pending);
   });
 }
