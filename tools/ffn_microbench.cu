@@ -38,6 +38,7 @@ int main(int argc, char** argv) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const uint32_t dbg = argc > 2 ? atoi(argv[2]) : 0;
   for (int n_routed : {6, 24}) {
+    if (argc > 4 && n_routed != atoi(argv[4])) continue;
     for (int shared : {1}) {
       std::vector<Plan> hp(n_sets);
       uint64_t bytes = 0;
