@@ -68,6 +68,7 @@ typedef struct moeb_model {
 
 #define MOEB_MODEL_LOG_STEPS 1u     /* record per-step decision records */
 #define MOEB_MODEL_TIME_KERNELS 2u  /* CUDA-event timing of every gate/decide/FFN launch */
+#define MOEB_MODEL_TRACE_TIMELINE 4u /* device-clock timeline of every layer-step (moeb_get_timeline) */
 
 typedef struct moeb_engine moeb_engine; /* decision engine only (simulate path) */
 typedef struct moeb_stack moeb_stack;   /* full MoE decode stack */
@@ -243,6 +244,10 @@ int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction,
                         double* out);
 
 /* Pinned host pool pointer and per-expert bytes (for the CPU oracle). */
+/* Device-clock (ns) timeline of the last <= 16384 layer-steps, 8 words each:
+ * 0 FFN start, 1 FFN saw its last upload land (0: none), 2 FFN end,
+ * 3 decide entry, 4 uploads published, 5 decide end. Diagnostics only. */
+int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n);
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes);
 
 #ifdef __cplusplus

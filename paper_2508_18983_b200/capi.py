@@ -286,8 +286,8 @@ class Stack:
 
     def __init__(self, cfg: Config, d_model, ffn, shared_ffn=0, shared_gate=0, renormalize=0,
                  routed_scale=1.0, weight_seed=7, log_steps=False, device=0, weights_host=None,
-                 time_kernels=False):
-        flags = (MODEL_LOG_STEPS if log_steps else 0) | (2 if time_kernels else 0)
+                 time_kernels=False, trace_timeline=False):
+        flags = (MODEL_LOG_STEPS if log_steps else 0) | (2 if time_kernels else 0) | (4 if trace_timeline else 0)
         m = Model(d_model=d_model, ffn=ffn, shared_ffn=shared_ffn, shared_gate=shared_gate,
                   renormalize=renormalize, routed_scale=routed_scale, weight_seed=weight_seed,
                   max_batch=cfg.batch, flags=flags)
@@ -398,6 +398,14 @@ class _StackExt:
         d = {f: getattr(s, f) for f, _ in KernelStats._fields_}
         d["prof_ns"] = list(s.prof_ns)
         return d
+
+    def timeline(self):
+        """Device-clock (ns) timeline, one row of 8 words per layer-step (see moeb_get_timeline)."""
+        n = C.c_size_t(0)
+        check(lib().moeb_get_timeline(self.h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint64)
+        check(lib().moeb_get_timeline(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
+        return out.reshape(-1, 8)
 
     def reset_kernel_stats(self):
         check(lib().moeb_reset_kernel_stats(self.h))

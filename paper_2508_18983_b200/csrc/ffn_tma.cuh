@@ -16,6 +16,7 @@
 // The decode FFN is a GEMV (B <= 32 tokens): memory-bound, no tensor cores.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -23,11 +24,14 @@
 
 namespace moeb {
 
-constexpr int kConsumers = 8;
-constexpr int kFfnTThreads = 32 * (1 + kConsumers);
-constexpr int kMaxStages = 8;
-constexpr uint32_t kHbufBytes = 48 * 1024;   // h staged in smem when it fits
-constexpr int kMaxDnRowsPerCta = 64;
+constexpr int kMaxStages = 12;
+// FFN grid counters (zeroed by the decide kernel before every launch):
+// [0, kMaxItems) per-item gate_up completion (CTAs), then the deferred-copy
+// barrier, the exit counter and the dynamic gate_up chunk counter
+constexpr int kFfnD2dCtr = kMaxItems;
+constexpr int kFfnExitCtr = kMaxItems + 1;
+constexpr int kFfnGuCtr = kMaxItems + 2;
+constexpr int kFfnCtrWords = kMaxItems + 4;
 constexpr size_t kPlanSmem = (sizeof(Plan) + 15) & ~(size_t)15;  // plan copy in smem, 16 B aligned
 
 // ------------------------------------------------------------- PTX helpers
@@ -89,7 +93,13 @@ struct FfnTArgs {
   uint32_t B, d, Fmax, stages;
   uint32_t stage_bytes;    // bytes per ring stage (multiple of 1 KB)
   uint32_t hbuf_bytes;     // smem reserved for staging h of the ready items
+  uint32_t acc_rows;       // ceil(d / grid): down rows per CTA
+  uint32_t plan_smem;      // bytes of the plan header + items kept in smem
+  uint32_t x_smem;         // bytes of the activation copy in smem (0: B == 1, d <= 2048, registers)
   uint32_t dbg;            // microbenchmark knobs: 1 no consumer math, 2 skip down pass
+  uint64_t* tstamp;        // microbenchmark: per-CTA phase timestamps [grid][8] (nullable)
+  uint64_t* tl;            // timeline trace: this launch's [8] record (nullable): 0 start (CTA 0),
+                           // 1 CTA 0's producer saw its last upload, 2 end (last CTA)
 };
 
 // Row range of CTA c out of G over n rows.
@@ -213,7 +223,7 @@ __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_
 #pragma unroll
   for (int t = 0; t < NT; ++t) a[t] = 0.f;
   // h comes from L2/L1: issue a batch of independent loads before the math
-  constexpr int U = NT <= 1 ? 6 : 2;
+  constexpr int U = NT <= 1 ? 4 : 2;
   if constexpr (NT >= 8) {
     for (uint32_t c = lane; c < nvec; c += 32) {
       const uint4 wv = reinterpret_cast<const uint4*>(ws)[c];
@@ -272,12 +282,172 @@ __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_
   }
 }
 
-template <int NTMAX>
-__global__ void __launch_bounds__(kFfnTThreads, 1) ffn_tma_kernel(FfnTArgs a) {
+// gate_up row pair for one token with the fp32 activations held in
+// registers (xr: chunk c = lane + 32 j, j < 8, packed f32x2 pairs), which
+// covers d <= 2048; wider rows take the remaining chunks from shared memory.
+__device__ __forceinline__ unsigned long long bf2x2_asm(uint32_t w) {
+  unsigned long long r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tshl.b32 lo, %1, 16;\n\tand.b32 hi, %1, 0xffff0000;\n\tmov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r) : "r"(w));
+  return r;
+}
+__device__ inline void gu_pair_x1(const uint16_t* gs, const uint16_t* us_rows, const unsigned long long (&xr)[8][4],
+                                  const float* u32, uint32_t d, float* h_out) {
+  const int lane = lane_id();
+  const uint32_t nvec = d / 8;
+  unsigned long long ag0 = 0ull, ag1 = 0ull, au0 = 0ull, au1 = 0ull;
+  const uint4* g4 = reinterpret_cast<const uint4*>(gs);
+  const uint4* u4 = reinterpret_cast<const uint4*>(us_rows);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t c = lane + 32 * j;
+    if (c < nvec) {
+      const uint4 g = g4[c], u = u4[c];
+      ffma2(ag0, bf2x2_asm(g.x), xr[j][0]);
+      ffma2(au0, bf2x2_asm(u.x), xr[j][0]);
+      ffma2(ag1, bf2x2_asm(g.y), xr[j][1]);
+      ffma2(au1, bf2x2_asm(u.y), xr[j][1]);
+      ffma2(ag0, bf2x2_asm(g.z), xr[j][2]);
+      ffma2(au0, bf2x2_asm(u.z), xr[j][2]);
+      ffma2(ag1, bf2x2_asm(g.w), xr[j][3]);
+      ffma2(au1, bf2x2_asm(u.w), xr[j][3]);
+    }
+  }
+  for (uint32_t c = lane + 256; c < nvec; c += 32) {
+    const uint4 g = g4[c], u = u4[c];
+    const float4* xp = reinterpret_cast<const float4*>(u32 + c * 8);
+    const float4 x0 = xp[0], x1 = xp[1];
+    dot8_f2(ag0, g, x0, x1);
+    dot8_f2(au0, u, x0, x1);
+  }
+  const float gsum = warp_sum(f2sum(ag0) + f2sum(ag1));
+  const float usum = warp_sum(f2sum(au0) + f2sum(au1));
+  if (lane == 0) {
+    const float silu = __fdiv_rn(gsum, 1.0f + expf(-gsum));
+    *h_out = silu * usum;
+  }
+}
+
+// ---- tensor-core GEMV at batch 1 (mma.sync m16n8k16, bf16 -> fp32).
+// A weight row is dotted with the activation through a "diagonal" mapping:
+// A rows 0-7 are eight 8-column groups of weight row r0 (columns i*8..i*8+7
+// and 64+i*8..64+i*8+7 of a 128-column block), A rows 8-15 the same groups
+// of row r1, and B column n holds the activation of group n, so D[i][i] and
+// D[8+i][i] are the partial dots of r0 / r1 over group i. ldmatrix reads 128
+// contiguous bytes per 8x8 matrix (conflict-free on a row-major stage) and
+// one ldmatrix.x4 + one mma cover 512 bytes of weights: the CUDA cores do no
+// bf16 unpacking. Products are exact in fp32, accumulation is fp32.
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+               : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// this lane's ldmatrix row address inside a 128-column block of rows r0 / r1
+__device__ __forceinline__ uint32_t diag_addr(uint32_t r0, uint32_t r1) {
+  const int lane = lane_id();
+  return ((lane & 8) ? r1 : r0) + ((lane >> 4) & 1) * 128 + (lane & 7) * 16;
+}
+// sum the diagonal partials: returns (dot r0, dot r1) on every lane
+__device__ __forceinline__ float2 diag_reduce(const float (&d)[4]) {
+  const int lane = lane_id();
+  const int i = lane >> 2;
+  const bool mine = (lane & 3) == (i >> 1);
+  float v0 = mine ? ((i & 1) ? d[1] : d[0]) : 0.f;
+  float v1 = mine ? ((i & 1) ? d[3] : d[2]) : 0.f;
+  return make_float2(warp_sum(v0), warp_sum(v1));
+}
+// B fragments of one token's bf16 activation (d <= 4096) in registers:
+// block b -> {x32[b*64 + lane], x32[b*64 + 32 + lane]}
+constexpr int kXrBlocks = 32;
+__device__ inline void gu_pair_mma(const uint16_t* gs, const uint16_t* us_rows, const uint32_t (&xb)[kXrBlocks][2],
+                                   uint32_t d, float* h_out) {
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc2[4] = {0.f, 0.f, 0.f, 0.f};
+  const uint32_t base = diag_addr(smem_u32(gs), smem_u32(us_rows));
+  const uint32_t nb = d / 128;
+#pragma unroll
+  for (int b = 0; b < kXrBlocks; b += 2) {
+    if ((uint32_t)b < nb) {
+      uint32_t a[4];
+      ldsm_x4(base + b * 256, a);
+      mma16816(acc, a, xb[b][0], xb[b][1]);
+    }
+    if ((uint32_t)b + 1 < nb) {
+      uint32_t a[4];
+      ldsm_x4(base + (b + 1) * 256, a);
+      mma16816(acc2, a, xb[b + 1][0], xb[b + 1][1]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] += acc2[q];
+  const float2 gu = diag_reduce(acc);
+  if (lane_id() == 0) {
+    const float silu = __fdiv_rn(gu.x, 1.0f + expf(-gu.x));
+    *h_out = silu * gu.y;
+  }
+}
+// down rows r0 / r1 (smem) against h split as bf16 hi + lo (smem words:
+// hi32[F/2] then lo32[F/2]); returns the two dots on every lane
+__device__ inline float2 dn_pair_mma(const uint16_t* w0, const uint16_t* w1, const uint32_t* hw, uint32_t F) {
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc2[4] = {0.f, 0.f, 0.f, 0.f};
+  const int lane = lane_id();
+  const uint32_t base = diag_addr(smem_u32(w0), smem_u32(w1));
+  const uint32_t nb = F / 128, half = F / 2;
+#pragma unroll 2
+  for (uint32_t b = 0; b < nb; ++b) {
+    uint32_t a[4];
+    ldsm_x4(base + b * 256, a);
+    const uint32_t* hb = hw + b * 64 + lane;
+    mma16816(acc, a, hb[0], hb[32]);
+    mma16816(acc2, a, hb[half], hb[half + 32]);
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] += acc2[q];
+  return diag_reduce(acc);
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(uint16_t lo, uint16_t hi) { return (uint32_t)lo | ((uint32_t)hi << 16); }
+// fp32 h -> (hi, lo) bf16 words for the down MMA (h = hi + lo to 2^-16)
+__device__ __forceinline__ void split_h4(float4 v, uint32_t& hi01, uint32_t& hi23, uint32_t& lo01, uint32_t& lo23) {
+  const uint16_t h0 = f32_to_bf16_rne(v.x), h1 = f32_to_bf16_rne(v.y), h2 = f32_to_bf16_rne(v.z), h3 = f32_to_bf16_rne(v.w);
+  hi01 = pack_bf16x2(h0, h1);
+  hi23 = pack_bf16x2(h2, h3);
+  lo01 = pack_bf16x2(f32_to_bf16_rne(v.x - bf2f(h0)), f32_to_bf16_rne(v.y - bf2f(h1)));
+  lo23 = pack_bf16x2(f32_to_bf16_rne(v.z - bf2f(h2)), f32_to_bf16_rne(v.w - bf2f(h3)));
+}
+
+// Launch shape of the FFN kernel for a model / batch (host side).
+struct FfnLaunch {
+  void (*fn)(FfnTArgs);
+  int threads;
+  uint32_t stages, stage_bytes, hbuf_bytes, acc_rows, plan_smem, x_smem;
+  size_t smem;
+};
+
+// Persistent grouped SwiGLU FFN. NC consumer warps in NC/kGroupWarps groups;
+// ring stage k is consumed by group k % groups (several stages in flight on
+// the consumer side), warp w of a group takes gate_up row pair w of a stage
+// and the down rows with (row - dlo) % kGroupWarps == w. Each group keeps its
+// own down accumulators, summed in group order at the end (deterministic).
+constexpr int kGroupWarps = 4;
+constexpr size_t kFfnSmemMax = 225 * 1024;
+
+template <int NTMAX, int NC>
+__global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
+  constexpr int NG = NC / kGroupWarps;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
-  __shared__ float acc_s[kMaxDnRowsPerCta * kMaxB];
-  __shared__ uint32_t s_hdr[4];
+  // dynamic gate_up stages: {item << 16 | rows, first row}; rows == 0 marks
+  // the end of the dynamic phase (second word = next ring step)
+  __shared__ uint32_t s_stage_hdr[kMaxStages][2];
+  __shared__ uint32_t h_off[kMaxItems + 1];
+  __shared__ uint32_t s_cpre[kMaxItems + 1];
+  __shared__ uint32_t s_arrive[kMaxItems];
+  __shared__ uint32_t s_hstage;
   // PDL: the plan and u come from the gate+decide kernel launched just before
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
@@ -285,37 +455,35 @@ __global__ void __launch_bounds__(kFfnTThreads, 1) ffn_tma_kernel(FfnTArgs a) {
   const uint32_t G = gridDim.x, c = blockIdx.x;
   const uint32_t d = a.d, B = a.B, S = a.stages, SB = a.stage_bytes;
   const int warp = warp_id(), lane = lane_id();
-  unsigned char* ring = smem_raw;                                   // S * 32 KB
+  uint64_t* ts = a.tstamp ? a.tstamp + (size_t)c * 8 : nullptr;
+  if (ts && threadIdx.x == 0) ts[0] = globaltimer_ns();
+  if (a.tl && c == 0 && threadIdx.x == 0) a.tl[0] = globaltimer_ns();
+  unsigned char* ring = smem_raw;                                   // S * SB
   uint16_t* us = reinterpret_cast<uint16_t*>(smem_raw + S * SB);  // [B][d] bf16, or [B][d] fp32 when B <= 4
   float* u32 = reinterpret_cast<float*>(us);
   constexpr bool kF32U = NTMAX <= 4;
   // the plan header + items live in shared memory for the whole launch
-  Plan* p = reinterpret_cast<Plan*>(smem_raw + S * SB + (((size_t)B * d * (kF32U ? 4 : 2) + 15) & ~(size_t)15));
-  if (threadIdx.x < 4) s_hdr[threadIdx.x] = reinterpret_cast<const uint32_t*>(gp)[threadIdx.x];
-  __syncthreads();
+  // (one load phase: the smem copy is sized for the largest possible plan)
+  Plan* p = reinterpret_cast<Plan*>(smem_raw + S * SB + a.x_smem);
+  float* acc_s = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(p) + a.plan_smem);  // [NG][acc_rows][B]
+  const uint32_t acc_n = a.acc_rows * B;
+  float* hs = acc_s + ((NG * acc_n + 3) & ~3u);  // h of the ready items
   {
-    const size_t words = (offsetof(Plan, items) + s_hdr[0] * sizeof(Item)) / 8;
     const uint64_t* src = reinterpret_cast<const uint64_t*>(gp);
     uint64_t* dst = reinterpret_cast<uint64_t*>(p);
-    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
-    const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + s_hdr[2] * sizeof(D2D) / 8;
-    for (uint32_t i = d0 + threadIdx.x; i < d1; i += blockDim.x) dst[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < a.plan_smem / 8; i += blockDim.x) dst[i] = src[i];
   }
-  const uint32_t n_items = s_hdr[0], n_ready = s_hdr[1];
-  // h of every ready item, staged once after the ready gate_up barrier
-  float* hs = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(p) + kPlanSmem);
-  __shared__ uint32_t h_off[kMaxItems + 1];
-  __shared__ uint32_t s_hstage;
-  const uint32_t gu_rows = min((uint32_t)kConsumers, max(1u, SB / (4u * d)));  // row pairs per stage
-
+  for (uint32_t i = threadIdx.x; i < kMaxItems; i += blockDim.x) s_arrive[i] = 0;
+  const uint32_t gu_rows = min((uint32_t)kGroupWarps, max(1u, SB / (4u * d)));  // row pairs per stage
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], kConsumers);
+      mbar_init(&empty_bar[s], kGroupWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (kF32U) {
+  if (!a.x_smem) {
+  } else if (kF32U) {
     for (uint32_t i = threadIdx.x; i < B * d / 2; i += blockDim.x) {
       const uint32_t w = reinterpret_cast<const uint32_t*>(a.u)[i];
       u32[2 * i] = __uint_as_float(w << 16);
@@ -327,44 +495,96 @@ __global__ void __launch_bounds__(kFfnTThreads, 1) ffn_tma_kernel(FfnTArgs a) {
   }
   uint32_t dlo, dhi;
   share(d, c, G, dlo, dhi);
-  for (uint32_t i = threadIdx.x; i < (dhi - dlo) * B; i += blockDim.x) acc_s[i] = 0.f;
+  for (uint32_t i = threadIdx.x; i < NG * acc_n; i += blockDim.x) acc_s[i] = 0.f;
+  // this thread's residual inputs for the epilogue, loaded now (off the tail)
+  constexpr uint32_t kXinPre = 2;
+  float xin_pre[kXinPre];
+#pragma unroll
+  for (uint32_t j = 0; j < kXinPre; ++j) {
+    const uint32_t i = threadIdx.x + j * blockDim.x;
+    xin_pre[j] = i < (dhi - dlo) * B ? bf2f(a.x_in[(size_t)(i % B) * d + dlo + i / B]) : 0.f;
+  }
+  __syncthreads();
+  const uint32_t n_items = p->n_items, n_ready = p->n_ready;
   if (threadIdx.x == 0) {
-    uint32_t off = 0;
+    uint32_t off = 0, ch = 0;
     for (uint32_t i = 0; i < n_ready; ++i) {
       h_off[i] = off;
+      s_cpre[i] = ch;
       off += p->items[i].F * p->items[i].n_tok;
+      ch += (p->items[i].F + gu_rows - 1) / gu_rows;
     }
     h_off[n_ready] = off;
+    s_cpre[n_ready] = ch;
     s_hstage = (size_t)off * 4 <= a.hbuf_bytes;
   }
   __syncthreads();
+  if (ts && threadIdx.x == 0) ts[1] = globaltimer_ns();
 
-  // enumerate (item, kind) segments in schedule order
+  // static schedule after the dynamic phase: down rows of the ready items,
+  // then per waiting item its gate_up rows followed by its down rows
   auto seg_item = [&](uint32_t s, uint32_t& item, uint32_t& kind) {
-    if (s < n_ready) { item = s; kind = 0; return; }
-    s -= n_ready;
     if (s < n_ready) { item = s; kind = 1; return; }
     s -= n_ready;
     item = n_ready + s / 2;
     kind = s & 1;
   };
-  const uint32_t n_segs = 2 * n_items;
+  const uint32_t n_segs = n_ready + 2 * (n_items - n_ready);
   auto skip_seg = [&](uint32_t sg) {
     uint32_t ii, kind;
     seg_item(sg, ii, kind);
     return (a.dbg & 2) && kind == 1;
   };
+  auto dn_step = [&](uint32_t F) { return min(4u * kGroupWarps, max(1u, SB / (F * 2))); };
 
   if (warp == 0) {
     // ------------------------------------------------------- producer
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy();
-      uint32_t stage = 0, phase = 0;
+      uint32_t k = 0;  // ring step
+      auto acquire = [&]() -> uint32_t {
+        const uint32_t st = k % S;
+        mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
+        return st;
+      };
+      // (1) gate_up rows of the ready items, chunk by chunk from a grid-wide
+      // counter: SMs that stream faster take more chunks (no static skew)
+      const uint32_t n_chunks = s_cpre[n_ready];
+      uint32_t* gctr = a.ctr + kFfnGuCtr;
+      uint32_t c0 = atomicAdd(gctr, 1u), c1 = atomicAdd(gctr, 1u);
+      uint32_t ii = 0;
+      while (c0 < n_chunks) {
+        const uint32_t cur = c0;
+        c0 = c1;
+        c1 = atomicAdd(gctr, 1u);
+        while (s_cpre[ii + 1] <= cur) ++ii;
+        const Item& it = p->items[ii];
+        const uint32_t F = it.F;
+        const uint32_t r = (cur - s_cpre[ii]) * gu_rows;
+        const uint32_t n = min(gu_rows, F - r);
+        const uint32_t st = acquire();
+        s_stage_hdr[st][0] = (ii << 16) | n;
+        s_stage_hdr[st][1] = r;
+        unsigned char* dst = ring + st * SB;
+        mbar_expect_tx(&full_bar[st], 2 * n * d * 2);
+        bulk_g2s(dst, it.w + (size_t)r * d, n * d * 2, &full_bar[st], pol);
+        bulk_g2s(dst + n * d * 2, it.w + ((size_t)F + r) * d, n * d * 2, &full_bar[st], pol);
+        ++k;
+      }
+      const uint32_t k_next = k + NG;
+      for (int g = 0; g < NG; ++g) {  // one end marker per consumer group
+        const uint32_t st = acquire();
+        s_stage_hdr[st][0] = 0;
+        s_stage_hdr[st][1] = k_next;
+        mbar_arrive(&full_bar[st]);
+        ++k;
+      }
+      // (2) the static segments
       for (uint32_t sg = 0; sg < n_segs; ++sg) {
         if (skip_seg(sg)) continue;
-        uint32_t ii, kind;
-        seg_item(sg, ii, kind);
-        const Item& it = p->items[ii];
+        uint32_t ii2, kind;
+        seg_item(sg, ii2, kind);
+        const Item& it = p->items[ii2];
         const uint32_t F = it.F;
         if (kind == 0 && it.wait) {
           const uint64_t t0 = globaltimer_ns();
@@ -372,6 +592,7 @@ __global__ void __launch_bounds__(kFfnTThreads, 1) ffn_tma_kernel(FfnTArgs a) {
             __nanosleep(128);
             if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 1u); break; }
           }
+          if (a.tl && c == 0) a.tl[1] = globaltimer_ns();
           // the uploaded bytes are read by the async (bulk-copy) proxy next
           asm volatile("fence.proxy.async;" ::: "memory");
         }
@@ -383,36 +604,95 @@ __global__ void __launch_bounds__(kFfnTThreads, 1) ffn_tma_kernel(FfnTArgs a) {
         } else {
           lo = dlo;
           hi = dhi;
-          step = min((uint32_t)kConsumers, max(1u, SB / (F * 2)));
+          step = dn_step(F);
           row_bytes = F * 2;
         }
         for (uint32_t r = lo; r < hi; r += step) {
           const uint32_t n = min(step, hi - r);
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          unsigned char* dst = ring + stage * SB;
+          const uint32_t st = acquire();
+          unsigned char* dst = ring + st * SB;
           if (kind == 0) {
-            const uint16_t* g = it.w + (size_t)r * d;
-            const uint16_t* u = it.w + ((size_t)F + r) * d;
-            mbar_expect_tx(&full_bar[stage], 2 * n * row_bytes);
-            bulk_g2s(dst, g, n * row_bytes, &full_bar[stage], pol);
-            bulk_g2s(dst + n * row_bytes, u, n * row_bytes, &full_bar[stage], pol);
+            mbar_expect_tx(&full_bar[st], 2 * n * row_bytes);
+            bulk_g2s(dst, it.w + (size_t)r * d, n * row_bytes, &full_bar[st], pol);
+            bulk_g2s(dst + n * row_bytes, it.w + ((size_t)F + r) * d, n * row_bytes, &full_bar[st], pol);
           } else {
-            const uint16_t* w = it.w + 2 * (size_t)F * d + (size_t)r * F;
-            mbar_expect_tx(&full_bar[stage], n * row_bytes);
-            bulk_g2s(dst, w, n * row_bytes, &full_bar[stage], pol);
+            mbar_expect_tx(&full_bar[st], n * row_bytes);
+            bulk_g2s(dst, it.w + 2 * (size_t)F * d + (size_t)r * F, n * row_bytes, &full_bar[st], pol);
           }
-          if (++stage == S) { stage = 0; phase ^= 1; }
+          ++k;
         }
       }
     }
   } else {
     // ------------------------------------------------------ consumers
-    // Each consumer warp signals its own completion of an item's gate_up rows
-    // (ctr[i] counts warps, G * kConsumers when complete) and waits on its
-    // own for the down pass: no CTA-wide barriers between items. h is read
-    // straight from global after the acquire (it is tiny and L1-resident).
-    const uint32_t cw = warp - 1;
-    uint32_t stage = 0, phase = 0;
+    // Ring step k (stage k % S) belongs to consumer group k % NG (S is a
+    // multiple of NG, so a stage always has the same group and its phases
+    // are consumed in order). Gate_up completion is aggregated per CTA
+    // (ctr[i] counts CTAs, G when complete); the down pass of an item waits
+    // on it through one poller and a consumer-wide named barrier.
+    const uint32_t cw = warp - 1, grp = cw / kGroupWarps, wg = cw % kGroupWarps;
+    float* acc_g = acc_s + grp * acc_n;
+    // B == 1: the token's bf16 activation as MMA B fragments in registers
+    uint32_t xb[kXrBlocks][2];
+    auto load_xb = [&]() {
+      const uint32_t* u32w = reinterpret_cast<const uint32_t*>(a.u);
+#pragma unroll
+      for (int b = 0; b < kXrBlocks; ++b) {
+        if ((uint32_t)b < d / 128) {
+          xb[b][0] = __ldg(u32w + b * 64 + lane);
+          xb[b][1] = __ldg(u32w + b * 64 + 32 + lane);
+        } else {
+          xb[b][0] = xb[b][1] = 0u;
+        }
+      }
+    };
+    auto gu_rows_of = [&](const unsigned char* src, const Item& it, uint32_t r, uint32_t n, float* h_item) {
+      if (wg >= n || (a.dbg & 1)) return;
+      const uint32_t nt = it.n_tok;
+      const uint16_t* gs = reinterpret_cast<const uint16_t*>(src) + (size_t)wg * d;
+      const uint16_t* ur = reinterpret_cast<const uint16_t*>(src + n * d * 2) + (size_t)wg * d;
+      if (NTMAX == 1) gu_pair_mma(gs, ur, xb, d, h_item + r + wg);
+      else if (kF32U) {
+        if (nt <= 1) gu_compute_f32<1>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
+        else gu_compute_f32<(NTMAX < 4 ? NTMAX : 4)>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
+      }
+      else if (NTMAX <= 8 || nt <= 8) gu_compute<(NTMAX < 8 ? NTMAX : 8)>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
+      else gu_compute<NTMAX>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
+    };
+    auto signal_gu = [&](uint32_t ci) {  // this warp finished its share of item ci's gate_up
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        if (atomicAdd(&s_arrive[ci], 1u) == NC - 1) {
+          __threadfence();
+          atomicAdd(&a.ctr[ci], 1u);
+        }
+      }
+    };
+    if (NTMAX == 1) load_xb();
+    // (1) dynamic gate_up of the ready items
+    uint32_t k = grp;
+    for (;;) {
+      const uint32_t st = k % S;
+      mbar_wait(&full_bar[st], (k / S) & 1);
+      if (ts && k == grp && grp == 0 && lane == 0 && wg == 0) ts[2] = globaltimer_ns();
+      const uint32_t h0 = s_stage_hdr[st][0], r = s_stage_hdr[st][1];
+      const uint32_t n = h0 & 0xffffu;
+      if (n == 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+        k = r;
+        break;
+      }
+      const uint32_t ii = h0 >> 16;
+      gu_rows_of(ring + st * SB, p->items[ii], r, n, a.h + (size_t)ii * kMaxB * a.Fmax);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[st]);
+      k += NG;
+    }
+    if (n_ready) signal_gu(0);
+    if (ts && cw == 0 && lane == 0) ts[3] = globaltimer_ns();
+    // (2) the static segments
     for (uint32_t sg = 0; sg < n_segs; ++sg) {
       if (skip_seg(sg)) continue;
       uint32_t ii, kind;
@@ -429,119 +709,212 @@ __global__ void __launch_bounds__(kFfnTThreads, 1) ffn_tma_kernel(FfnTArgs a) {
       } else {
         lo = dlo;
         hi = dhi;
-        step = min((uint32_t)kConsumers, max(1u, SB / (F * 2)));
-        // ready items signal once, on ctr[0] after the last ready gate_up
-        // segment; each waiting item has its own counter
+        step = dn_step(F);
         const bool ready = ii < n_ready;
-        const bool first_dn = ready && sg == n_ready;  // first down segment of the ready group
+        const bool first_dn = ready && sg == 0;  // first down segment of the ready group
         if (!ready || first_dn) {
+          // one poller per CTA, then a consumer-wide barrier releases every warp
           const uint32_t wc = ready ? 0 : ii;
-          if (lane == 0) {
+          if (cw == 0 && lane == 0) {
             const uint64_t t0 = globaltimer_ns();
-            while (ld_acquire_u32(&a.ctr[wc]) < G * kConsumers) {
-              __nanosleep(32);
+            while (ld_acquire_u32(&a.ctr[wc]) < G) {
+              __nanosleep(20);
               if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 2u); break; }
             }
           }
-          __syncwarp();
+          asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
         }
         if (first_dn && s_hstage) {
-          // stage h of all ready items into shared memory in one batch
-          asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
-          const uint32_t tid = cw * 32 + lane;
-          for (uint32_t i = 0; i < n_ready; ++i) {
-            const Item& ri = p->items[i];
-            const uint32_t q = ri.F / 4;
-            const float* hb = a.h + (size_t)i * kMaxB * a.Fmax;
-            for (uint32_t v = tid; v < ri.n_tok * q; v += kConsumers * 32) {
-              const uint32_t t = v / q, j = v % q;
-              reinterpret_cast<float4*>(hs + h_off[i])[v] =
-                  __ldcg(reinterpret_cast<const float4*>(hb + (size_t)t * a.Fmax) + j);
+          // stage h of all ready items into shared memory in one batch;
+          // every load issued before any store
+          const uint32_t tid = cw * 32 + lane, tot4 = h_off[n_ready] / 4;
+          constexpr uint32_t kU = 8;
+          uint32_t i = 0;  // item of v: v only grows for this thread
+          for (uint32_t v0 = tid; v0 < tot4; v0 += kU * NC * 32) {
+            float4 rv[kU];
+            uint32_t ri[kU];
+#pragma unroll
+            for (uint32_t q = 0; q < kU; ++q) {
+              const uint32_t v = v0 + q * NC * 32;
+              if (v < tot4) {
+                while (h_off[i + 1] / 4 <= v) ++i;
+                const uint32_t loc = v - h_off[i] / 4, qq = p->items[i].F / 4;
+                const uint32_t t = loc / qq, j = loc % qq;
+                rv[q] = __ldcg(reinterpret_cast<const float4*>(a.h + ((size_t)i * kMaxB + t) * a.Fmax) + j);
+                ri[q] = i;
+              }
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < kU; ++q) {
+              const uint32_t v = v0 + q * NC * 32;
+              if (v < tot4) {
+                const uint32_t ii2 = ri[q], Fi = p->items[ii2].F;
+                if (NTMAX == 1 && Fi % 128 == 0) {
+                  // bf16 hi / lo words for the tensor-core down pass
+                  const uint32_t loc = v - h_off[ii2] / 4;
+                  uint32_t* hw = reinterpret_cast<uint32_t*>(hs + h_off[ii2]);
+                  uint2 hv, lv;
+                  split_h4(rv[q], hv.x, hv.y, lv.x, lv.y);
+                  reinterpret_cast<uint2*>(hw)[loc] = hv;
+                  reinterpret_cast<uint2*>(hw + Fi / 2)[loc] = lv;
+                } else {
+                  reinterpret_cast<float4*>(hs)[v] = rv[q];
+                }
+              }
             }
           }
-          asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+          asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
         }
+        if (ts && first_dn && cw == 0 && lane == 0) ts[4] = globaltimer_ns();
         if (ready && s_hstage) {
           hsrc = hs + h_off[ii];
           hstride = F;
         }
       }
-      for (uint32_t r = lo; r < hi; r += step) {
+      if (kind == 0) {
+        // a waiting item's gate_up rows (static share)
+        if (NTMAX == 1) load_xb();
+        for (uint32_t r = lo; r < hi; r += step, ++k) {
+          const uint32_t st = k % S;
+          if (st % NG != grp) continue;
+          mbar_wait(&full_bar[st], (k / S) & 1);
+          gu_rows_of(ring + st * SB, it, r, min(step, hi - r), h_item);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[st]);
+        }
+        signal_gu(ii);
+        continue;
+      }
+      for (uint32_t r = lo; r < hi; r += step, ++k) {
+        const uint32_t st = k % S;
+        if (st % NG != grp) continue;
         const uint32_t n = min(step, hi - r);
-        mbar_wait(&full_bar[stage], phase);
-        const unsigned char* src = ring + stage * SB;
-        if (cw < n && !(a.dbg & 1)) {
-          if (kind == 0) {
-            const uint16_t* gs = reinterpret_cast<const uint16_t*>(src) + (size_t)cw * d;
-            const uint16_t* ur = reinterpret_cast<const uint16_t*>(src + n * d * 2) + (size_t)cw * d;
-            if (kF32U) {
-              if (NTMAX == 1 || nt <= 1) gu_compute_f32<1>(gs, ur, u32, d, it, r + cw, h_item, a.Fmax);
-              else gu_compute_f32<(NTMAX < 4 ? NTMAX : 4)>(gs, ur, u32, d, it, r + cw, h_item, a.Fmax);
+        mbar_wait(&full_bar[st], (k / S) & 1);
+        const unsigned char* src = ring + st * SB;
+        if (!(a.dbg & 1)) {
+          // rows of this step owned by this warp: (row - dlo) % kGroupWarps == wg
+          const uint32_t first = (wg + kGroupWarps - (r - dlo) % kGroupWarps) % kGroupWarps;
+          const bool mma_dn = NTMAX == 1 && F % 128 == 0 && ii < n_ready && s_hstage;
+          if (mma_dn) {
+            const uint32_t* hw = reinterpret_cast<const uint32_t*>(hsrc);
+            const float wt = it.wt[0];
+            const uint32_t tok = it.tok[0];
+            for (uint32_t q = first; q < n; q += 2 * kGroupWarps) {
+              const uint32_t q1 = q + kGroupWarps < n ? q + kGroupWarps : q;
+              const uint16_t* w0 = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
+              const uint16_t* w1 = reinterpret_cast<const uint16_t*>(src) + (size_t)q1 * F;
+              const float2 dd = dn_pair_mma(w0, w1, hw, F);
+              if (lane == 0) {
+                float* a0 = acc_g + (size_t)(r + q - dlo) * B + tok;
+                *a0 = fmaf(wt, dd.x, *a0);
+                if (q1 != q) {
+                  float* a1 = acc_g + (size_t)(r + q1 - dlo) * B + tok;
+                  *a1 = fmaf(wt, dd.y, *a1);
+                }
+              }
             }
-            else if (NTMAX <= 4 || nt <= 4) gu_compute<(NTMAX < 4 ? NTMAX : 4)>(gs, ur, us, d, it, r + cw, h_item, a.Fmax);
-            else if (NTMAX <= 8 || nt <= 8) gu_compute<(NTMAX < 8 ? NTMAX : 8)>(gs, ur, us, d, it, r + cw, h_item, a.Fmax);
-            else gu_compute<NTMAX>(gs, ur, us, d, it, r + cw, h_item, a.Fmax);
           } else {
-            const uint16_t* ws = reinterpret_cast<const uint16_t*>(src) + (size_t)cw * F;
-            float* acc_row = acc_s + (size_t)(r + cw - dlo) * B;
-            if (NTMAX == 1 || nt <= 1) dn_compute<1>(ws, hsrc, hstride, F, it, acc_row);
-            else if (NTMAX <= 4 || nt <= 4) dn_compute<(NTMAX < 4 ? NTMAX : 4)>(ws, hsrc, hstride, F, it, acc_row);
-            else if (NTMAX <= 8 || nt <= 8) dn_compute<(NTMAX < 8 ? NTMAX : 8)>(ws, hsrc, hstride, F, it, acc_row);
-            else dn_compute<NTMAX>(ws, hsrc, hstride, F, it, acc_row);
+            for (uint32_t q = first; q < n; q += kGroupWarps) {
+              const uint16_t* ws = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
+              float* acc_row = acc_g + (size_t)(r + q - dlo) * B;
+              if (NTMAX == 1 || nt <= 1) dn_compute<1>(ws, hsrc, hstride, F, it, acc_row);
+              else if (NTMAX <= 4 || nt <= 4) dn_compute<(NTMAX < 4 ? NTMAX : 4)>(ws, hsrc, hstride, F, it, acc_row);
+              else if (NTMAX <= 8 || nt <= 8) dn_compute<(NTMAX < 8 ? NTMAX : 8)>(ws, hsrc, hstride, F, it, acc_row);
+              else dn_compute<NTMAX>(ws, hsrc, hstride, F, it, acc_row);
+            }
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[stage]);
-        if (++stage == S) { stage = 0; phase ^= 1; }
-      }
-      if (kind == 0 && (ii >= n_ready || ii + 1 == n_ready)) {
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(&a.ctr[ii < n_ready ? 0 : ii], 1u);
-        }
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
       }
     }
   }
   __syncthreads();
-  // epilogue: residual add, bf16 hidden for the next layer, fp32 MoE output
-  for (uint32_t i = threadIdx.x; i < (dhi - dlo) * B; i += blockDim.x) {
+  if (ts && threadIdx.x == 0) ts[5] = globaltimer_ns();
+  // epilogue: group partial sums (fixed order), residual add (x_in was read
+  // at the start), bf16 hidden for the next layer, fp32 MoE output
+  for (uint32_t i = threadIdx.x, j = 0; i < (dhi - dlo) * B; i += blockDim.x, ++j) {
     const uint32_t o = dlo + i / B, t = i % B;
-    const float y = acc_s[i];
-    const float xo = bf2f(a.x_in[(size_t)t * d + o]) + y;
+    float y = acc_s[i];
+#pragma unroll
+    for (int g = 1; g < NG; ++g) y += acc_s[g * acc_n + i];
+    const float xo = (j < kXinPre ? xin_pre[j] : bf2f(a.x_in[(size_t)t * d + o])) + y;
     a.x_out[(size_t)t * d + o] = f32_to_bf16_rne(xo);
     a.y_out[(size_t)t * d + o] = y;
   }
   // deferred admissions: staging -> slot once every CTA finished reading
-  if (p->n_d2d) {
+  const uint32_t n_d2d = p->n_d2d;
+  if (n_d2d) {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      atomicAdd(&a.ctr[kMaxItems], 1u);
+      atomicAdd(&a.ctr[kFfnD2dCtr], 1u);
       const uint64_t t0 = globaltimer_ns();
-      while (ld_acquire_u32(&a.ctr[kMaxItems]) < G) {
+      while (ld_acquire_u32(&a.ctr[kFfnD2dCtr]) < G) {
         __nanosleep(128);
         if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 3u); break; }
       }
     }
     __syncthreads();
-    const uint64_t nv = p->d2d_elems / 8;
-    for (uint32_t j = 0; j < p->n_d2d; ++j) {
-      const uint4* src = reinterpret_cast<const uint4*>(p->d2d[j].src);
-      uint4* dst = reinterpret_cast<uint4*>(p->d2d[j].dst);
+    const uint64_t nv = gp->d2d_elems / 8;
+    for (uint32_t j = 0; j < n_d2d; ++j) {
+      const uint4* src = reinterpret_cast<const uint4*>(gp->d2d[j].src);
+      uint4* dst = reinterpret_cast<uint4*>(gp->d2d[j].dst);
       for (uint64_t v = c * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)G * blockDim.x)
         dst[v] = ldg_cg(src + v);
     }
   }
   __syncthreads();
+  if (ts && threadIdx.x == 0) ts[7] = globaltimer_ns();
   if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t prev = atomicAdd(&a.ctr[kMaxItems + 1], 1u);
+    // slot reads are complete (they landed in smem); only the deferred
+    // staging->slot copies must be visible before ffn_done releases the
+    // copy stream's prefetches into those slots
+    if (n_d2d) __threadfence();
+    const uint32_t prev = atomicAdd(&a.ctr[kFfnExitCtr], 1u);
     if (prev == G - 1) {
-      __threadfence_system();
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ffn_done), "r"(p->seq) : "memory");
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ffn_done), "r"(p->seq) : "memory");
+      if (a.tl) a.tl[2] = globaltimer_ns();
     }
+    if (ts) ts[6] = globaltimer_ns();
   }
+}
+
+// Kernel instance and shared-memory layout for a model / batch. Throws
+// nothing: returns stages == 0 when the shapes do not fit.
+inline FfnLaunch ffn_launch_config(uint32_t B, uint32_t d, uint32_t F, uint32_t S, uint32_t E, uint32_t top_k,
+                                   int sms) {
+  FfnLaunch L{};
+  int nc;
+  if (B <= 1) { L.fn = ffn_tma_kernel<1, 12>; nc = 12; }
+  else if (B <= 4) { L.fn = ffn_tma_kernel<4, 12>; nc = 12; }
+  else if (B <= 8) { L.fn = ffn_tma_kernel<8, 8>; nc = 8; }
+  else if (B <= 16) { L.fn = ffn_tma_kernel<16, 8>; nc = 8; }
+  else { L.fn = ffn_tma_kernel<32, 8>; nc = 8; }
+  L.threads = 32 * (nc + 1);
+  const uint32_t ng = nc / kGroupWarps;
+  const uint32_t max_items = 1 + std::min(E, B * top_k);
+  L.plan_smem = (uint32_t)((offsetof(Plan, items) + (size_t)max_items * sizeof(Item) + 15) & ~(size_t)15);
+  L.x_smem = (B == 1 && d <= 2048) ? 0u : (uint32_t)((((size_t)B * d * (B <= 4 ? 4 : 2)) + 15) & ~(size_t)15);
+  L.acc_rows = (d + sms - 1) / sms;
+  const size_t accb = ((size_t)ng * L.acc_rows * B + 3) / 4 * 16;
+  const size_t fixed = L.x_smem + L.plan_smem + accb;
+  const size_t pair = 4ull * d;  // one gate + one up row
+  // h of the ready items (shared + top-k experts x tokens) staged in smem
+  // when it fits beside one ring stage of one pair per group
+  const size_t hwant = ((size_t)S + (size_t)top_k * F) * B * 4;
+  const size_t min_ring = 2ull * ng * pair;
+  L.hbuf_bytes = (uint32_t)(kFfnSmemMax >= fixed + min_ring + hwant ? hwant : 0);
+  const size_t budget = kFfnSmemMax - fixed - L.hbuf_bytes;
+  // two stages per consumer group; each stage up to kGroupWarps row pairs
+  const uint32_t per = 2;
+  size_t sb = budget / (per * ng) / pair * pair;
+  if (sb > kGroupWarps * pair) sb = kGroupWarps * pair;
+  L.stage_bytes = (uint32_t)sb;
+  L.stages = sb >= pair ? per * ng : 0;
+  L.smem = (size_t)L.stages * L.stage_bytes + fixed + L.hbuf_bytes;
+  return L;
 }
 
 }  // namespace moeb

@@ -98,12 +98,15 @@ struct DecideArgs {
   uint64_t expert_elems;
   Plan* plan;
   uint32_t* ffn_ctr;
+  const uint32_t* copies_done; // upload ids landed so far (written by the copy stream)
   MailEntry* ring;
   const volatile uint64_t* host_ack;
   float* scores_log;          // [rec_cap][B][E] or null
   StepRec* recs;
   TokRec* toks;
   uint64_t rec_cap;
+  uint64_t* tl;               // timeline trace record of this layer-step (nullable):
+                              // 3 decider entry, 4 uploads published (entry A), 5 end of decide
   uint64_t it;                // decode iteration of this launch (host-tracked)
   uint64_t seq;               // 1-based layer-step sequence number (host-tracked)
 };
@@ -263,6 +266,7 @@ struct EarlyPublish {
 #endif
       __threadfence_system();
       me->seq = mseq;
+      if (A.tl) A.tl[4] = globaltimer_ns();
 #ifdef MOEB_PROFILE_PHASES
       st->prof[13] += gtimer() - tf0;
 #endif
@@ -301,6 +305,14 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
     return id;
   };
   if (a.shared_w) add_item(a.shared_w, a.S, 0, 0, 0);
+  // uploads already landed (the copy stream is FIFO and copies_done only
+  // grows): their slots are plain residents again
+  const uint32_t landed = ld_acquire_u32(a.copies_done);
+  for (uint32_t i = 0; i < out.n_res; ++i) {
+    const int slot = out.res_slot[i];
+    const uint32_t w = ls->slot_copy[slot];
+    if (w && (int32_t)(landed - w) >= 0) ls->slot_copy[slot] = 0;
+  }
   // residents: ready ones first, then those whose (prefetch) upload is in
   // flight, ordered by upload id (the copy stream is FIFO)
   for (int pass = 0; pass < 2; ++pass) {
@@ -424,6 +436,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   if (!s_last) return;
 
   const DecideArgs& a = ga.d;
+  if (a.tl && threadIdx.x == 0) a.tl[3] = globaltimer_ns();
   MOEB_T(t_elect);
   const int warp = warp_id(), lane = lane_id();
   const uint32_t nw = blockDim.x >> 5;
@@ -542,7 +555,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     for (uint32_t i = 0; i < sm->d.nsel[t]; ++i) s += sm->sc[t][sm->d.sel[t][i]];
     sm->denom[t] = s;
   }
-  for (uint32_t i = threadIdx.x; i < kMaxItems + 2; i += blockDim.x) a.ffn_ctr[i] = 0;
+  for (uint32_t i = threadIdx.x; i < kFfnCtrWords; i += blockDim.x) a.ffn_ctr[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     build_plan(a, sm);
@@ -593,6 +606,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     MOEB_T(t_pub0);
     __threadfence_system();
     a.ring[(2 * sm->seq) % kRing].seq = 2 * sm->seq;
+    if (a.tl) a.tl[5] = globaltimer_ns();
 #ifdef MOEB_PROFILE_PHASES
     const uint64_t t_pub1 = gtimer();
     a.st->prof[10] += t_pub1 - t_pub0;
@@ -656,6 +670,7 @@ struct moeb_stack {
   DevBuf<Plan> plan;
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
   DevBuf<StepRec> recs;
+  DevBuf<uint64_t> timeline;  // [rec_cap][8] (MOEB_MODEL_TRACE_TIMELINE)
   DevBuf<TokRec> toks;
   uint64_t rec_cap = 0;
   uint64_t trace_steps = 0, total_iters = ~0ull;
@@ -669,9 +684,8 @@ struct moeb_stack {
   std::atomic<int> copier_error{0};
   std::string copier_msg;
   int ffn_grid = 0;
-  void (*ffn_fn)(FfnTArgs) = nullptr;
-  uint32_t ffn_stages = 0, ffn_stage_bytes = 0, ffn_hbuf = 0;
-  size_t ffn_smem = 0, gd_smem = 0;
+  FfnLaunch ffn{};
+  size_t gd_smem = 0;
   DevBuf<uint32_t> ticket;
   MailEntry* ring_dev = nullptr;
   uint64_t* ack_dev = nullptr;
@@ -804,15 +818,6 @@ static void synth(uint16_t* dst, uint64_t n, uint64_t seed, uint64_t tensor, uin
   MOEB_CUDA(cudaGetLastError());
 }
 
-using FfnFn = void (*)(FfnTArgs);
-static FfnFn ffn_kernel_for(uint32_t B) {
-  if (B <= 1) return ffn_tma_kernel<1>;
-  if (B <= 4) return ffn_tma_kernel<4>;
-  if (B <= 8) return ffn_tma_kernel<8>;
-  if (B <= 16) return ffn_tma_kernel<16>;
-  return ffn_tma_kernel<32>;
-}
-
 static float fan_scale(uint32_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
 
 // (Re)initialise the decision state and upload the initial residents. The
@@ -940,12 +945,16 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   MOEB_CUDA(cudaMemcpyAsync(S->st.p, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
   reset_state(S, s);
   S->plan.alloc(1);
-  S->ffn_ctr.alloc(kMaxItems + 2);
+  S->ffn_ctr.alloc(kFfnCtrWords);
   S->ffn_ctr.zero(s);
   S->copies_done.alloc(1);
   S->copies_done.zero(s);
   S->ffn_done.alloc(1);
   S->ffn_done.zero(s);
+  if (m.flags & MOEB_MODEL_TRACE_TIMELINE) {
+    S->timeline.alloc(16384 * 8);
+    S->timeline.zero(s);
+  }
   if (m.flags & MOEB_MODEL_LOG_STEPS) {
     S->rec_cap = 16384;
     S->recs.alloc(S->rec_cap);
@@ -956,28 +965,11 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   std::memset(S->ring, 0, sizeof(MailEntry) * kRing);
   MOEB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->ack), 64, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(S->ack, 0, 64);
-  // kernel resources
-  // FFN ring: 64 KB stages (8 row pairs at d=2048), as many as fit beside
-  // u [B][d] and the h staging buffer
-  {
-    const uint32_t Fm = std::max(F, Sh);
-    (void)Fm;
-    S->ffn_stage_bytes = 64 * 1024;  // 8 gate+up row pairs at d = 2048
-    const size_t ubytes = (((size_t)B * d * (B <= 4 ? 4 : 2)) + 15) & ~(size_t)15;
-    // h of the ready items (shared + top-k experts x tokens) staged in smem
-    // when it fits beside two ring stages; otherwise read from L2
-    const size_t hwant = ((size_t)Sh + (size_t)cfg.top_k * F) * B * 4;
-    const size_t room = 220 * 1024 - ubytes - kPlanSmem - 2 * (size_t)S->ffn_stage_bytes;
-    S->ffn_hbuf = (uint32_t)(hwant <= room ? hwant : 0);
-    const size_t budget = 220 * 1024 - ubytes - kPlanSmem - S->ffn_hbuf;
-    S->ffn_stages = (uint32_t)std::min<size_t>(kMaxStages, budget / S->ffn_stage_bytes);
-    if (S->ffn_stages < 2) {
-      S->ffn_stage_bytes /= 2;
-      S->ffn_stages = (uint32_t)std::min<size_t>(kMaxStages, budget / S->ffn_stage_bytes);
-    }
-    if (S->ffn_stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
-    S->ffn_smem = (size_t)S->ffn_stages * S->ffn_stage_bytes + ubytes + kPlanSmem + S->ffn_hbuf;
-  }
+  // kernel resources: FFN launch shape (ring stages, h staging, accumulators)
+  int sms = 0;
+  MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  S->ffn = ffn_launch_config(B, d, F, Sh, E, cfg.top_k, sms);
+  if (S->ffn.stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
   S->ticket.alloc(1);
   S->ticket.zero(s);
   MOEB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&S->ring_dev), S->ring, 0));
@@ -987,15 +979,12 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // one shared-memory carveout for both per-layer kernels: no L1/smem
   // reconfiguration drain between them
   MOEB_CUDA(cudaFuncSetAttribute(gate_decide_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  S->ffn_fn = ffn_kernel_for(B);
-  MOEB_CUDA(cudaFuncSetAttribute(S->ffn_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->ffn_smem));
-  MOEB_CUDA(cudaFuncSetAttribute(S->ffn_fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  int sms = 0, occ = 0;
-  MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  MOEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->ffn_fn, kFfnTThreads, S->ffn_smem));
+  MOEB_CUDA(cudaFuncSetAttribute(S->ffn.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S->ffn.smem));
+  MOEB_CUDA(cudaFuncSetAttribute(S->ffn.fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int occ = 0;
+  MOEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->ffn.fn, S->ffn.threads, S->ffn.smem));
   if (occ < 1) throw Error(5, "ffn kernel does not fit on an SM");
   S->ffn_grid = sms;  // one persistent CTA per SM (the per-item counters need co-residency)
-  if ((d + sms - 1) / sms > (uint32_t)kMaxDnRowsPerCta) throw Error(1, "model: d_model too large for the FFN grid");
   MOEB_CUDA(cudaStreamSynchronize(s));
   S->copier = std::thread([S] { S->copy_loop(); });
 }
@@ -1003,11 +992,10 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
 // Programmatic dependent launch: the next per-layer kernel is scheduled while
 // the current one drains (each kernel opens with griddepcontrol.wait, so
 // data dependences are unchanged), hiding the grid launch latency between
-// the gate+decide and FFN kernels of every layer.
-// Measured on B200: PDL between these two kernels made each layer slower
-// (the FFN grid needs every SM and the decision CTA holds one), so it is
-// off; the griddepcontrol instructions are no-ops without it.
-constexpr bool kUsePdl = false;
+// the gate+decide and FFN kernels of every layer. Measured on B200 (device
+// timeline, DSV2-Lite B=1): decide end -> FFN start 4.4 -> 2.0 us, FFN end ->
+// next decide 6.5 -> 4.8 us. MOEB_NO_PDL=1 turns it off.
+static const bool kUsePdl = getenv("MOEB_NO_PDL") == nullptr;
 
 template <class Args>
 static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args* args) {
@@ -1069,6 +1057,7 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.expert_elems = S->expert_elems;
     a.plan = S->plan.p;
     a.ffn_ctr = S->ffn_ctr.p;
+    a.copies_done = S->copies_done.p;
     a.ring = S->ring_dev;
     a.host_ack = S->ack_dev;
     a.scores_log = S->scores_log.p;
@@ -1077,6 +1066,7 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.rec_cap = S->rec_cap;
     a.it = S->host_it;
     a.seq = ++S->host_seq;
+    a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * 8 : nullptr;
     ga.ticket = S->ticket.p;
     if (S->timing) S->tick(s);
     launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3((rows + 1) / 2), dim3(kGdThreads),
@@ -1097,12 +1087,14 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     f.B = B;
     f.d = d;
     f.Fmax = std::max(S->F, S->S);
-    f.stages = S->ffn_stages;
-    f.stage_bytes = S->ffn_stage_bytes;
-    f.hbuf_bytes = S->ffn_hbuf;
-    void* fargs[] = {&f};
-    launch_pdl(reinterpret_cast<const void*>(S->ffn_fn), dim3(S->ffn_grid), dim3(kFfnTThreads), S->ffn_smem, s, &f);
-    (void)fargs;
+    f.stages = S->ffn.stages;
+    f.stage_bytes = S->ffn.stage_bytes;
+    f.hbuf_bytes = S->ffn.hbuf_bytes;
+    f.acc_rows = S->ffn.acc_rows;
+    f.plan_smem = S->ffn.plan_smem;
+    f.tl = a.tl;
+    f.x_smem = S->ffn.x_smem;
+    launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s, &f);
     S->n_launch_layers += 1;
     MOEB_CUDA(cudaGetLastError());
     if (S->timing) S->tick(s);
@@ -1287,6 +1279,16 @@ int moeb_reset_kernel_stats(moeb_stack* s) {
 }
 
 void* moeb_stream(moeb_stack* s) { return s->stream; }
+
+int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n) {
+  return guarded([&] {
+    if (!s->timeline.p) throw Error(1, "timeline: create the stack with MOEB_MODEL_TRACE_TIMELINE");
+    MOEB_CUDA(cudaStreamSynchronize(s->stream));
+    const size_t have = (size_t)std::min<uint64_t>(s->host_seq, 16384) * 8;
+    *n = have;
+    if (out) MOEB_CUDA(cudaMemcpy(out, s->timeline.p, std::min(cap, have) * 8, cudaMemcpyDeviceToHost));
+  });
+}
 
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes) {
   *pool = s->pool;

@@ -28,10 +28,13 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&xo, B * d * 2));
   CK(cudaMalloc(&y, B * d * 4));
   CK(cudaMalloc(&h, (size_t)kMaxItems * kMaxB * S * 4));
-  CK(cudaMalloc(&ctr, (kMaxItems + 2) * 4));
+  CK(cudaMalloc(&ctr, kFfnCtrWords * 4));
   CK(cudaMalloc(&cd, 4));
   CK(cudaMalloc(&fd, 4));
   CK(cudaMalloc(&plan, kPlanSmem * n_sets));
+  uint64_t* tsd;
+  CK(cudaMalloc(&tsd, 8 * 8 * 1024));
+  CK(cudaMemset(tsd, 0, 8 * 8 * 1024));
   CK(cudaMemset(u, 0, B * d * 2));
   CK(cudaMemset(x, 0, B * d * 2));
   int sms;
@@ -59,35 +62,43 @@ int main(int argc, char** argv) {
         if (si == 0) for (int i = 0; i < n; ++i) bytes += 3ull * p.items[i].F * d * 2;
       }
       CK(cudaMemcpy(plan, hp.data(), kPlanSmem * n_sets, cudaMemcpyHostToDevice));
-      const uint32_t SB = argc > 3 ? atoi(argv[3]) * 1024 : 64 * 1024;
-      const size_t ubytes = (size_t)B * d * 4;
-      const size_t hb = (size_t)(S + 6 * F) * B * 4;
-      size_t budget = 220 * 1024 - ubytes - kPlanSmem - hb;
-      uint32_t stages = (uint32_t)std::min<size_t>(kMaxStages, budget / SB);
-      if (argc > 1 && atoi(argv[1]) > 0) stages = std::min<uint32_t>(stages, atoi(argv[1]));
-      size_t smem = (size_t)stages * SB + ubytes + kPlanSmem + hb;
-      CK(cudaFuncSetAttribute(ffn_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      FfnLaunch fl = ffn_launch_config(B, d, F, S, 64, n_routed, sms);
+      if (argc > 1 && atoi(argv[1]) > 0) fl.stages = std::min<uint32_t>(fl.stages, atoi(argv[1]));
+      const size_t smem = fl.smem - 0;
+      CK(cudaFuncSetAttribute(fl.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       cudaEvent_t a, b;
       cudaEventCreate(&a); cudaEventCreate(&b);
       const int iters = 48;
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(a);
         for (int i = 0; i < iters; ++i) {
-          cudaMemsetAsync(ctr, 0, (kMaxItems + 2) * 4);
+          cudaMemsetAsync(ctr, 0, kFfnCtrWords * 4);
           FfnTArgs f{};
           f.plan = plan + (i % n_sets); f.u = u; f.x_in = x; f.x_out = xo; f.y_out = y; f.h = h; f.ctr = ctr;
-          f.copies_done = cd; f.ffn_done = fd; f.B = B; f.d = d; f.Fmax = S; f.stages = stages; f.stage_bytes = SB;
-          f.dbg = dbg;
-          f.hbuf_bytes = (uint32_t)hb;
-          ffn_tma_kernel<1><<<sms, kFfnTThreads, smem>>>(f);
+          f.copies_done = cd; f.ffn_done = fd; f.B = B; f.d = d; f.Fmax = S; f.stages = fl.stages;
+          f.stage_bytes = fl.stage_bytes; f.acc_rows = fl.acc_rows; f.plan_smem = fl.plan_smem; f.x_smem = fl.x_smem; f.dbg = dbg; f.hbuf_bytes = fl.hbuf_bytes;
+          f.tstamp = (rep == 1 && i == iters - 1) ? tsd : nullptr;
+          fl.fn<<<sms, fl.threads, smem>>>(f);
         }
         cudaEventRecord(b);
         CK(cudaEventSynchronize(b));
         float ms;
         cudaEventElapsedTime(&ms, a, b);
-        if (rep == 1)
-          printf("dbg=%u routed=%2d shared=%d stages=%u: %.1f us/launch, %.1f MB, %.0f GB/s (incl memset)\n", dbg, n_routed, shared,
-                 stages, ms * 1e3 / iters, bytes / 1e6, bytes / (ms * 1e-3 / iters) / 1e9);
+        if (rep == 1) {
+        std::vector<uint64_t> t(8 * sms);
+        CK(cudaMemcpy(t.data(), tsd, 8 * 8 * sms, cudaMemcpyDeviceToHost));
+        uint64_t t0 = ~0ull;
+        for (int i = 0; i < sms; ++i) t0 = std::min(t0, t[i * 8]);
+        const char* nm[8] = {"start", "prologue", "first_stage", "gu_done", "barrier", "consumers_done", "end", "pre_atomic"};
+        for (int k = 0; k < 8; ++k) {
+          double mn = 1e30, mx = 0, avg = 0;
+          for (int i = 0; i < sms; ++i) { double v = (t[i * 8 + k] - t0) * 1e-3; mn = std::min(mn, v); mx = std::max(mx, v); avg += v / sms; }
+          printf("   %-15s min %7.2f avg %7.2f max %7.2f us\n", nm[k], mn, avg, mx);
+        }
+      }
+      if (rep == 1)
+          printf("dbg=%u routed=%2d shared=%d stages=%u: %.1f us/launch, %.1f MB, %.0f GB/s (incl memset) SB=%u\n", dbg, n_routed, shared,
+                 fl.stages, ms * 1e3 / iters, bytes / 1e6, bytes / (ms * 1e-3 / iters) / 1e9, fl.stage_bytes);
       }
     }
   }

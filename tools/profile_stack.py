@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--layers", type=int, default=26)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--time", action="store_true", help="print per-kernel CUDA-event times")
+    ap.add_argument("--timeline", action="store_true", help="device-clock timeline summary per layer-step")
     args = ap.parse_args()
     import torch
     from paper_2508_18983_b200 import capi
@@ -34,7 +35,7 @@ def main():
     L, E, B, d = args.layers, 64, args.batch, 2048
     cfg = capi.Config.make(num_layers=L, experts=E, top_k=6, batch=B, alpha=0.25, seed=7,
                            slots=E if args.allhit else 16)
-    st = capi.Stack(cfg, 2048, 1408, 2816, weight_seed=7, time_kernels=args.time)
+    st = capi.Stack(cfg, 2048, 1408, 2816, weight_seed=7, time_kernels=args.time, trace_timeline=args.timeline)
     T = args.tokens
     st.set_logits_trace(capi.trace_logits(capi.generate_trace(L, E, B, T, 7)), T)
     x = torch.randn(T, B, d).to(torch.bfloat16).cuda()
@@ -53,6 +54,26 @@ def main():
         names = ["gate", "elect", "stage", "decide", "d:classify", "d:route", "d:hits+record", "d:loads",
                  "d:prefetch", "plan", "pub:fence", "span", "pub:copy", "early:fence", "-", "start_skew"]
         print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names) if nm != "-"})
+    if args.timeline:
+        tl = st.timeline().astype(np.int64)
+        tl = tl[len(tl) // 4:]  # skip the cold start
+        us = lambda v: round(float(np.mean(v)) / 1e3, 2) if len(v) else None
+        miss = tl[:, 1] != 0
+        nxt = tl[1:]
+        cur = tl[:-1]
+        print("layer-steps", len(tl), "with uploads", int(miss.sum()))
+        print("decide entry->publish", us(tl[:, 4] - tl[:, 3]), "entry->end", us(tl[:, 5] - tl[:, 3]))
+        print("decide end->ffn start", us(tl[:, 0] - tl[:, 5]))
+        print("ffn start->end (no uploads)", us((tl[:, 2] - tl[:, 0])[~miss]))
+        print("ffn last upload seen->end (uploads)", us((tl[:, 2] - tl[:, 1])[miss]))
+        print("ffn end->next decide entry", us(nxt[:, 3] - cur[:, 2]))
+        print("layer period", us(nxt[:, 3] - cur[:, 3]))
+        # from one layer's last upload to the next publish (PCIe idle, less host issue latency)
+        idx = np.nonzero(miss)[0]
+        gaps = []
+        for a, b in zip(idx[:-1], idx[1:]):
+            gaps.append(tl[b, 4] - tl[a, 1])
+        print("last upload seen -> next uploads published", us(np.array(gaps)))
     st.close()
 
 
