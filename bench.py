@@ -140,6 +140,20 @@ def divergence(y_sub, y_exact, x_in):
             "identical_tokens": int((diff == 0).sum())}
 
 
+def timeline_summary(tl):
+    """Per layer-step averages (us) from the device-clock timeline rows
+    (moeb_get_timeline): decide entry->publish/end, FFN duration, gaps."""
+    tl = tl.astype(np.int64)
+    up = tl[:, 1] != 0
+    r = lambda v: round(float(np.mean(v)) / 1e3, 2) if len(v) else None
+    return {"decide_to_publish_us": r(tl[:, 4] - tl[:, 3]), "decide_us": r(tl[:, 5] - tl[:, 3]),
+            "ffn_us": r((tl[:, 2] - tl[:, 0])[~up]) if (~up).any() else None,
+            "ffn_tail_after_last_upload_us": r((tl[:, 2] - tl[:, 1])[up]) if up.any() else None,
+            "gap_decide_to_ffn_us": r(tl[:, 0] - tl[:, 5]), "gap_ffn_to_next_decide_us": r(tl[1:, 3] - tl[:-1, 2]),
+            "layer_period_us": r(tl[1:, 3] - tl[:-1, 3]), "layer_steps_with_uploads": int(up.sum()),
+            "layer_steps": int(len(tl))}
+
+
 def measure_pcie_gbs(torch):
     """Pinned H2D copy-engine bandwidth: 256 MB, best of 10 (the PCIe roofline)."""
     n = 256 << 20
@@ -204,7 +218,10 @@ def run_ours(args):
 
     cfg = capi.Config.make(**CFG)
     t0 = time.time()
-    stack = capi.Stack(cfg, weight_seed=7, time_kernels=True, device=local, **MODEL)
+    # no per-kernel CUDA events in the timed stack (they would serialise the
+    # programmatic dependent launches); the per-kernel split comes from the
+    # device-clock timeline (globaltimer stamps written by the kernels)
+    stack = capi.Stack(cfg, weight_seed=7, trace_timeline=True, device=local, **MODEL)
     create_s = time.time() - t0
     stack.set_logits_trace(logits, T)
     # a torch-owned stream for the stack's work: pinned-buffer copies recorded
@@ -243,6 +260,7 @@ def run_ours(args):
     m1 = stack.metrics()
     io = stack.io_stats()
     ks = stack.kernel_stats()
+    tl_main = timeline_summary(stack.timeline()[-K * L:])
     ms_max = max_over_ranks(ms)
 
     # ---- end to end through the C-ABI with host buffers (e2e)
@@ -298,22 +316,37 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
     cfg3 = capi.Config.make(**dict(CFG, slots=E))
     pool_ptr, _ = stack.host_pool()
-    st3 = capi.Stack(cfg3, weight_seed=7, device=local, weights_host=(pool_ptr, stack), time_kernels=True, **MODEL)
-    st3.set_logits_trace(logits, T)
-    s3 = torch.cuda.Stream()
-    s3p = s3.cuda_stream
     n3 = min(64, T)
-    for i in range(8):
-        st3.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
-    st3.sync()
-    st3.reset_kernel_stats()
-    h0 = time.time()
-    for i in range(8, 8 + n3):
-        st3.step(x_dev[i % T].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
-    st3.sync()
-    allhit_wall = time.time() - h0
-    k3 = st3.kernel_stats()
-    st3.close()
+
+    def allhit_pass(**kw):
+        st3 = capi.Stack(cfg3, weight_seed=7, device=local, weights_host=(pool_ptr, stack), **kw, **MODEL)
+        st3.set_logits_trace(logits, T)
+        s3 = torch.cuda.Stream()
+        s3p = s3.cuda_stream
+        with torch.cuda.stream(s3):
+            for i in range(8):
+                st3.step(x_dev[i].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
+            st3.sync()
+            st3.reset_kernel_stats()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(s3)
+            for i in range(8, 8 + n3):
+                st3.step(x_dev[i % T].data_ptr(), y_dev.data_ptr(), B, stream=s3p)
+            a1.record(s3)
+            a1.synchronize()
+            st3.sync()
+        out = (a0.elapsed_time(a1) / n3, st3.kernel_stats(), st3.timeline()[-n3 * L:] if kw.get("trace_timeline") else None)
+        st3.close()
+        return out
+
+    # (1) CUDA events around every FFN launch on its stream: the roofline's
+    # conservative per-launch duration (events also stop the launches from
+    # overlapping, so this includes the launch latency)
+    _, k3, _ = allhit_pass(time_kernels=True)
+    # (2) the same work as it runs in the stack (no events): ms/token and the
+    # device-clock FFN duration
+    allhit_ms_token, _, tl3 = allhit_pass(trace_timeline=True)
+    tl_hit = timeline_summary(tl3)
     ffn_gbs = k3["ffn_bytes"] / (k3["ffn_ms"] * 1e-3) / 1e9
     per_launch_bytes = k3["ffn_bytes"] / max(k3["ffn_launches"], 1)
     traffic = None
@@ -322,7 +355,6 @@ def run_ours(args):
             traffic = json.load(f).get("dram_bytes_per_launch")
     except Exception:
         pass
-    allhit_ms_token = (k3["route_ms"] + k3["ffn_ms"]) / n3
 
     # ---- path roofline: T_roof = max(B_hbm / BW_hbm, B_pcie / BW_pcie) per token
     pcie_peak = measure_pcie_gbs(torch)
@@ -369,6 +401,8 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "kernel": "ffn_kernel (all-resident pass, no uploads)",
                      "achieved": round(ffn_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                      "frac": round(ffn_gbs / hbm_peak, 4), "traffic": traffic,
+                     "device_clock_achieved": round(per_launch_bytes / (tl_hit["ffn_us"] * 1e-6) / 1e9, 1),
+                     "device_clock_frac": round(per_launch_bytes / (tl_hit["ffn_us"] * 1e-6) / 1e9 / hbm_peak, 4),
                      "algorithmic_bytes_per_launch": int(per_launch_bytes), "peak_source": peak_kind,
                      "allhit_ms_per_token": round(allhit_ms_token, 4)},
         "path_roofline": {"t_roof_ms": round(t_roof, 4), "t_measured_ms": round(ms_tok, 4),
@@ -377,10 +411,8 @@ def run_ours(args):
                           "pcie_achieved_gbs_copy_stream": round(io["h2d_bytes"] / max(io["copy_ms"], 1e-9) / 1e6, 2),
                           "pcie_busy_frac": round(io["copy_ms"] / ms, 4),
                           "bound": "pcie" if b_pcie / pcie_peak > b_hbm / hbm_peak else "hbm"},
-        "kernel_ms_per_token": {"gate_decide": round(ks["route_ms"] / K, 4),
-                                "ffn_incl_upload_waits": round(ks["ffn_ms"] / K, 4),
-                                "allhit_gate_decide": round(k3["route_ms"] / n3, 4),
-                                "allhit_ffn": round(k3["ffn_ms"] / n3, 4)},
+        "layer_us_device_clock": {"timed_run": tl_main, "all_resident": tl_hit},
+        "allhit_ffn_event_us": round(k3["ffn_ms"] * 1e3 / max(k3["ffn_launches"], 1), 2),
         "gpu_launches": int(2 * L * K),
         "clocks": clk,
         "create_s": round(create_s, 2),

@@ -628,8 +628,17 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   LayerState* ls = cx.ls;
   double* hist_l = cx.hist_l;
   record_scores_warp(ls, hist_l, cfg.window, E, sm->mean);  // pipeline.cpp:191
-  if (cfg.policy == 0)
-    for (uint32_t e = lane; e < E; e += 32) sm->avg[e] = window_average(ls, hist_l, cfg.window, E, e);
+  // window averages (ScoreWindow) are computed on the first admission that
+  // needs them: the history does not change again in this step
+  bool avg_ready = cfg.policy != 0;
+  auto avg = [&]() -> const double* {
+    if (!avg_ready) {
+      for (uint32_t e = lane; e < E; e += 32) sm->avg[e] = window_average(ls, hist_l, cfg.window, E, e);
+      __syncwarp();
+      avg_ready = true;
+    }
+    return sm->avg;
+  };
 
   // residents: shield + touch; misses -> demand set (pipeline.cpp:196-205)
   const uint64_t route_end = sc->route_end, attn_end = sc->attn_end;
@@ -697,7 +706,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     const uint32_t e = sm->out.load[i];
     if (lane == 0) log_task(cx.logs, R_PCIE, K_DEMAND, (int)layer, e, pcie_t, pcie_t + cfg.t_load, layer, it);
     pcie_t += cfg.t_load;
-    const int slot = admit_or_defer(cx, sm, ls, hist_l, layer, e, pcie_t, true, ev_layer, ev_e, sm->avg);
+    const int slot = admit_or_defer(cx, sm, ls, hist_l, layer, e, pcie_t, true, ev_layer, ev_e, avg());
     if (lane == 0) sm->out.load_slot[i] = (int8_t)(slot >= 0 ? slot : -1);
     ready[i] = pcie_t;
   }
@@ -752,7 +761,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     if (lane == 0) sm->n_def = 0;
     __syncwarp();
     for (uint32_t i = 0; i < nd; ++i) {
-      const int slot = admit_or_defer(cx, sm, ls, hist_l, layer, def_copy[i], completion, false, ev_layer, ev_e, sm->avg);
+      const int slot = admit_or_defer(cx, sm, ls, hist_l, layer, def_copy[i], completion, false, ev_layer, ev_e, avg());
       if (lane == 0 && slot >= 0 && sm->out.n_def < kMaxE) {
         sm->out.def_e[sm->out.n_def] = (uint8_t)def_copy[i];
         sm->out.def_slot[sm->out.n_def] = (int8_t)slot;
@@ -793,7 +802,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       issued |= bit(i);
       if (!tavg && cfg.policy == 0) {
         if (tl == layer) {
-          tavg = sm->avg;
+          tavg = avg();
         } else {
           for (uint32_t x = lane; x < E; x += 32) sm->tavg[x] = window_average(tls, cx.thist, cfg.window, E, x);
           __syncwarp();

@@ -73,11 +73,15 @@ struct MailCmd {
   uint32_t id;        // upload id; copies_done := id after the copy
   uint32_t wait_ffn;  // nonzero: copy waits for ffn_done >= wait_ffn
 };
+// seq word = (sequence << 8) | command count: one 64-bit store publishes
+// both, so an empty entry needs no system fence (only the commands of a
+// non-empty entry must be visible before it)
 struct MailEntry {
   volatile uint64_t seq;
   uint32_t n, pad;
   MailCmd cmd[kMaxCmds];
 };
+static_assert(kMaxCmds < 256, "command count is packed in 8 bits");
 
 struct DecideArgs {
   DevCfg cfg;
@@ -138,6 +142,7 @@ struct DecideKSmem {
   Plan plan;
   MailCmd cmd[kMaxCmds];
   uint32_t n_cmds;
+  uint32_t landed;            // copies_done when the step's state was staged
   uint64_t it, seq;
   int last;
   // uploads published early by EarlyPublish (ids + destinations)
@@ -264,8 +269,8 @@ struct EarlyPublish {
 #ifdef MOEB_PROFILE_PHASES
       const uint64_t tf0 = gtimer();
 #endif
-      __threadfence_system();
-      me->seq = mseq;
+      if (n) __threadfence_system();
+      me->seq = (mseq << 8) | n;
       if (A.tl) A.tl[4] = globaltimer_ns();
 #ifdef MOEB_PROFILE_PHASES
       st->prof[13] += gtimer() - tf0;
@@ -306,8 +311,8 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
   };
   if (a.shared_w) add_item(a.shared_w, a.S, 0, 0, 0);
   // uploads already landed (the copy stream is FIFO and copies_done only
-  // grows): their slots are plain residents again
-  const uint32_t landed = ld_acquire_u32(a.copies_done);
+  // grows; read during staging): their slots are plain residents again
+  const uint32_t landed = sm->landed;
   for (uint32_t i = 0; i < out.n_res; ++i) {
     const int slot = out.res_slot[i];
     const uint32_t w = ls->slot_copy[slot];
@@ -464,6 +469,8 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     const uint64_t* g_h = reinterpret_cast<const uint64_t*>(a.hist + layer * hwords);
     const uint64_t* g_th = reinterpret_cast<const uint64_t*>(a.hist + tl * hwords);
     uint64_t r_st = 0, r_ls = 0, r_tls = 0, r_h[kHw], r_th[kHw];
+    uint32_t r_cd = 0;
+    if (tid == kGdThreads - 1) r_cd = *reinterpret_cast<const volatile uint32_t*>(a.copies_done);
     if (tid < kStW) r_st = g_st[tid];
     if (tid < kLsW) r_ls = g_ls[tid];
     if (two && tid < kLsW) r_tls = g_tls[tid];
@@ -491,6 +498,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
       }
     }
     if (threadIdx.x == 0) sm->cfg = a.cfg;
+    if (tid == kGdThreads - 1) sm->landed = r_cd;
   }
   const uint32_t jobs = want_next ? 2 * B : B;
   for (uint32_t j = warp; j < jobs; j += nw) {
@@ -604,8 +612,9 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   __syncthreads();
   if (threadIdx.x == 0) {
     MOEB_T(t_pub0);
-    __threadfence_system();
-    a.ring[(2 * sm->seq) % kRing].seq = 2 * sm->seq;
+    const uint32_t nc = sm->n_cmds;
+    if (nc) __threadfence_system();
+    a.ring[(2 * sm->seq) % kRing].seq = ((2 * sm->seq) << 8) | nc;
     if (a.tl) a.tl[5] = globaltimer_ns();
 #ifdef MOEB_PROFILE_PHASES
     const uint64_t t_pub1 = gtimer();
@@ -747,13 +756,14 @@ struct moeb_stack {
     unsigned spins = 0;
     while (!stop.load(std::memory_order_relaxed)) {
       MailEntry* me = &ring[expect % kRing];
-      if (me->seq != expect) {
+      const uint64_t sv = me->seq;
+      if ((sv >> 8) != expect) {
         if (++spins > 2000) std::this_thread::yield();
         continue;
       }
       spins = 0;
       std::atomic_thread_fence(std::memory_order_acquire);
-      const uint32_t n = me->n;
+      const uint32_t n = (uint32_t)(sv & 0xff);
       for (uint32_t i = 0; i < n; ++i) {
         const MailCmd c = me->cmd[i];
         if (c.wait_ffn &&
