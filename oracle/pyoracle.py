@@ -112,6 +112,8 @@ def ref():
         lib.ref_route_json.restype = C.c_void_p
         lib.ref_free.argtypes = [C.c_void_p]
         lib.ref_time_simulate.restype = C.c_double
+        if hasattr(lib, "ref_report_from_trace_file"):
+            lib.ref_report_from_trace_file.restype = C.c_void_p
         _ref = lib
     return _ref
 
@@ -175,6 +177,14 @@ def ref_simulate(cfg: SimCfg, scores, pred=None, has_pred=None, timeline=True):
     p = lib.ref_simulate_json(C.byref(c), _dptr(scores), _dptr(pred) if pred is not None else None,
                               _u8ptr(has_pred) if has_pred is not None else None,
                               C.c_uint64(scores.shape[0]), C.c_int(int(timeline)))
+    return _take_json(lib, lib.ref_free, p)
+
+
+def ref_report_from_trace_file(cfg: SimCfg, path: str):
+    """The reference's load_trace() + simulate() + build_report() on a JSONL file."""
+    lib = ref()
+    c = cfg.to_c()
+    p = lib.ref_report_from_trace_file(C.byref(c), path.encode())
     return _take_json(lib, lib.ref_free, p)
 
 

@@ -21,6 +21,7 @@
 #include "moesched/cache.hpp"
 #include "moesched/pipeline.hpp"
 #include "moesched/prefetch.hpp"
+#include "moesched/report.hpp"
 #include "moesched/router.hpp"
 #include "moesched/trace.hpp"
 
@@ -216,6 +217,19 @@ double ref_time_simulate(const orc_config* c, const double* scores, std::uint64_
   const auto t1 = std::chrono::steady_clock::now();
   if (sink == 0xffffffffffffULL) std::puts("");
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// The reference's own JSONL loader (with its validation) + simulate() +
+// build_report() on a trace file: the receiving side of the wire-format
+// bridge (paper_2508_18983_b200/bridge.py).
+char* ref_report_from_trace_file(const orc_config* c, const char* path) {
+  try {
+    const GateTrace tr = load_trace(path);
+    const SimOutput out = simulate(tr, to_cfg(c));
+    return dup(build_report(to_cfg(c), out, fingerprint_file(path)).dump());
+  } catch (const std::exception& e) {
+    return dup(std::string("{\"error\":\"") + e.what() + "\"}");
+  }
 }
 
 void ref_free(void* p) { std::free(p); }
