@@ -244,9 +244,12 @@ int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction,
                         double* out);
 
 /* Pinned host pool pointer and per-expert bytes (for the CPU oracle). */
-/* Device-clock (ns) timeline of the last <= 16384 layer-steps, 8 words each:
+/* Device-clock (ns) timeline of the last <= 16384 layer-steps, 16 words each:
  * 0 FFN start, 1 FFN saw its last upload land (0: none), 2 FFN end,
- * 3 decide entry, 4 uploads published, 5 decide end. Diagnostics only. */
+ * 3 decide entry, 4 uploads published, 5 decide end, 6 FFN has the
+ * speculative plan (batch 1), 7 FFN CTA 0 entry, 8 speculative gate_up done,
+ * 9 final gate_up done, 10 down pass starts, 11 FFN CTA 0 compute done
+ * (8-11: CTA 0). Diagnostics only. */
 int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n);
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes);
 

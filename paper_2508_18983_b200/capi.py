@@ -405,7 +405,7 @@ class _StackExt:
         check(lib().moeb_get_timeline(self.h, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint64)
         check(lib().moeb_get_timeline(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n.value, C.byref(n)))
-        return out.reshape(-1, 8)
+        return out.reshape(-1, 16)
 
     def reset_kernel_stats(self):
         check(lib().moeb_reset_kernel_stats(self.h))

@@ -487,8 +487,12 @@ __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, Nex
 // Called by warp 0 as soon as the demand-load / BA-stream lists are final
 // (before the GPU task clock, deferrals and prefetch), so the caller can hand
 // the uploads to the copy engine early.
+// classified(): called by every thread right after classification (before
+// routing), with the pre-route residency untouched — the stack publishes the
+// experts certain to be selected there (speculative FFN start).
 struct NoHook {
   __device__ void operator()(DecideSmem*, uint32_t, uint32_t) const {}
+  __device__ void classified(DecideSmem*) const {}
 };
 
 template <class Hook = NoHook>
@@ -556,6 +560,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   __syncthreads();
   mark(4);
+  on_loads.classified(sm);
 
   if (cfg.er) {
     if (tid == 0) {

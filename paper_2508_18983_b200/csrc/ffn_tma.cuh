@@ -30,8 +30,12 @@ constexpr int kMaxStages = 12;
 // barrier, the exit counter and the dynamic gate_up chunk counter
 constexpr int kFfnD2dCtr = kMaxItems;
 constexpr int kFfnExitCtr = kMaxItems + 1;
-constexpr int kFfnGuCtr = kMaxItems + 2;
-constexpr int kFfnCtrWords = kMaxItems + 4;
+constexpr int kFfnGuCtr = kMaxItems + 2;        // dynamic gate_up chunks, final plan
+constexpr int kFfnReadyDoneCtr = kMaxItems + 3;  // CTAs done with the final plan's ready gate_up
+constexpr int kFfnSpecGuCtr = kMaxItems + 4;     // dynamic gate_up chunks, speculative plan
+constexpr int kFfnSpecDoneCtr = kMaxItems + 5;   // CTAs done with the speculative gate_up
+constexpr int kFfnCtrWords = kMaxItems + 6;
+constexpr int kTlWords = 16;  // timeline record words per layer-step
 constexpr size_t kPlanSmem = (sizeof(Plan) + 15) & ~(size_t)15;  // plan copy in smem, 16 B aligned
 
 // ------------------------------------------------------------- PTX helpers
@@ -98,8 +102,12 @@ struct FfnTArgs {
   uint32_t x_smem;         // bytes of the activation copy in smem (0: B == 1, d <= 2048, registers)
   uint32_t dbg;            // microbenchmark knobs: 1 no consumer math, 2 skip down pass
   uint64_t* tstamp;        // microbenchmark: per-CTA phase timestamps [grid][8] (nullable)
-  uint64_t* tl;            // timeline trace: this launch's [8] record (nullable): 0 start (CTA 0),
-                           // 1 CTA 0's producer saw its last upload, 2 end (last CTA)
+  uint64_t* tl;            // timeline trace: this launch's [8] record (nullable): 0 final plan in
+                           // hand (CTA 0), 1 CTA 0's producer saw its last upload, 2 end (last
+                           // CTA), 6 speculative plan in hand (CTA 0)
+  const Plan* spec_plan;   // speculative plan (null: none); published when *spec_flag == seq
+  const uint32_t* spec_flag;
+  uint32_t seq;
 };
 
 // Row range of CTA c out of G over n rows.
@@ -442,39 +450,36 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages];
   // dynamic gate_up stages: {item << 16 | rows, first row}; rows == 0 marks
-  // the end of the dynamic phase (second word = next ring step)
+  // the end of a dynamic phase (second word = next ring step)
   __shared__ uint32_t s_stage_hdr[kMaxStages][2];
-  __shared__ uint32_t h_off[kMaxItems + 1];
-  __shared__ uint32_t s_cpre[kMaxItems + 1];
-  __shared__ uint32_t s_arrive[kMaxItems];
-  __shared__ uint32_t s_hstage;
-  // PDL: the plan and u come from the gate+decide kernel launched just before
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ uint32_t h_off[kMaxItems + 1];   // h staging offsets of the current phase's ready items
+  __shared__ uint32_t s_cpre[kMaxItems + 1];  // gate_up chunk prefix of the current phase's ready items
+  __shared__ uint32_t s_arrive[kMaxItems + 2];
+  __shared__ uint32_t s_hstage, s_phase_sync;
+  // PDL: the next layer's gate+decide kernel may be scheduled once every CTA
+  // of this grid is running (it waits for our completion before reading)
   asm volatile("griddepcontrol.launch_dependents;");
-  const Plan* gp = a.plan;
+  if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
   const uint32_t G = gridDim.x, c = blockIdx.x;
   const uint32_t d = a.d, B = a.B, S = a.stages, SB = a.stage_bytes;
   const int warp = warp_id(), lane = lane_id();
   uint64_t* ts = a.tstamp ? a.tstamp + (size_t)c * 8 : nullptr;
-  if (ts && threadIdx.x == 0) ts[0] = globaltimer_ns();
-  if (a.tl && c == 0 && threadIdx.x == 0) a.tl[0] = globaltimer_ns();
   unsigned char* ring = smem_raw;                                   // S * SB
   uint16_t* us = reinterpret_cast<uint16_t*>(smem_raw + S * SB);  // [B][d] bf16, or [B][d] fp32 when B <= 4
   float* u32 = reinterpret_cast<float*>(us);
   constexpr bool kF32U = NTMAX <= 4;
   // the plan header + items live in shared memory for the whole launch
-  // (one load phase: the smem copy is sized for the largest possible plan)
   Plan* p = reinterpret_cast<Plan*>(smem_raw + S * SB + a.x_smem);
   float* acc_s = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(p) + a.plan_smem);  // [NG][acc_rows][B]
   const uint32_t acc_n = a.acc_rows * B;
-  float* hs = acc_s + ((NG * acc_n + 3) & ~3u);  // h of the ready items
-  {
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(gp);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(p);
-    for (uint32_t i = threadIdx.x; i < a.plan_smem / 8; i += blockDim.x) dst[i] = src[i];
-  }
-  for (uint32_t i = threadIdx.x; i < kMaxItems; i += blockDim.x) s_arrive[i] = 0;
+  float* hs = acc_s + ((NG * acc_n + 3) & ~3u);  // h of the current phase's ready items
   const uint32_t gu_rows = min((uint32_t)kGroupWarps, max(1u, SB / (4u * d)));  // row pairs per stage
+  uint32_t dlo, dhi;
+  share(d, c, G, dlo, dhi);
+
+  // ---- set-up that depends on nothing the decide kernel writes
+  for (uint32_t i = threadIdx.x; i < kMaxItems + 2; i += blockDim.x) s_arrive[i] = 0;
+  for (uint32_t i = threadIdx.x; i < NG * acc_n; i += blockDim.x) acc_s[i] = 0.f;
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -482,21 +487,8 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (!a.x_smem) {
-  } else if (kF32U) {
-    for (uint32_t i = threadIdx.x; i < B * d / 2; i += blockDim.x) {
-      const uint32_t w = reinterpret_cast<const uint32_t*>(a.u)[i];
-      u32[2 * i] = __uint_as_float(w << 16);
-      u32[2 * i + 1] = __uint_as_float(w & 0xffff0000u);
-    }
-  } else {
-    for (uint32_t i = threadIdx.x; i < B * d / 8; i += blockDim.x)
-      reinterpret_cast<uint4*>(us)[i] = reinterpret_cast<const uint4*>(a.u)[i];
-  }
-  uint32_t dlo, dhi;
-  share(d, c, G, dlo, dhi);
-  for (uint32_t i = threadIdx.x; i < NG * acc_n; i += blockDim.x) acc_s[i] = 0.f;
-  // this thread's residual inputs for the epilogue, loaded now (off the tail)
+  // this thread's residual inputs for the epilogue (the previous FFN wrote
+  // x_in and has completed: the decide kernel in between waited for it)
   constexpr uint32_t kXinPre = 2;
   float xin_pre[kXinPre];
 #pragma unroll
@@ -504,44 +496,210 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
     const uint32_t i = threadIdx.x + j * blockDim.x;
     xin_pre[j] = i < (dhi - dlo) * B ? bf2f(a.x_in[(size_t)(i % B) * d + dlo + i / B]) : 0.f;
   }
-  __syncthreads();
-  const uint32_t n_items = p->n_items, n_ready = p->n_ready;
-  if (threadIdx.x == 0) {
-    uint32_t off = 0, ch = 0;
-    for (uint32_t i = 0; i < n_ready; ++i) {
-      h_off[i] = off;
-      s_cpre[i] = ch;
-      off += p->items[i].F * p->items[i].n_tok;
-      ch += (p->items[i].F + gu_rows - 1) / gu_rows;
+
+  // ---- speculative phase: wait for the decide kernel's early plan
+  uint32_t n_spec = 0;
+  if (a.spec_plan) {
+    if (threadIdx.x == 0) {
+      if (ts) ts[0] = globaltimer_ns();
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_u32(a.spec_flag) != a.seq) {
+        __nanosleep(64);
+        if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 5u); break; }
+      }
+      if (a.tl && c == 0) a.tl[6] = globaltimer_ns();
     }
-    h_off[n_ready] = off;
-    s_cpre[n_ready] = ch;
-    s_hstage = (size_t)off * 4 <= a.hbuf_bytes;
+    __syncthreads();
+    const uint32_t ns = ld_acquire_u32(&a.spec_plan->n_spec);
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(a.spec_plan);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(p);
+    const uint32_t words = (uint32_t)((offsetof(Plan, items) + ns * sizeof(Item)) / 8);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
+    n_spec = ns;
+  }
+  const bool after_spec = a.spec_plan != nullptr;  // the final plan is read after griddepcontrol.wait
+  if (!after_spec) {
+    // PDL: the plan and u come from the gate+decide kernel launched just before
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (ts && threadIdx.x == 0) ts[0] = globaltimer_ns();
+  }
+  // u: written by the gate phase before the decider was elected (and
+  // released with the spec flag)
+  if (!a.x_smem) {
+  } else if (kF32U) {
+    for (uint32_t i = threadIdx.x; i < B * d / 2; i += blockDim.x) {
+      const uint32_t w = __ldcg(reinterpret_cast<const uint32_t*>(a.u) + i);
+      u32[2 * i] = __uint_as_float(w << 16);
+      u32[2 * i + 1] = __uint_as_float(w & 0xffff0000u);
+    }
+  } else {
+    for (uint32_t i = threadIdx.x; i < B * d / 8; i += blockDim.x)
+      reinterpret_cast<uint4*>(us)[i] = __ldcg(reinterpret_cast<const uint4*>(a.u) + i);
+  }
+  if (!after_spec) {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(a.plan);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(p);
+    for (uint32_t i = threadIdx.x; i < a.plan_smem / 8; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
-  if (ts && threadIdx.x == 0) ts[1] = globaltimer_ns();
+  if (a.tl && c == 0 && threadIdx.x == 0 && !after_spec) a.tl[0] = globaltimer_ns();
 
-  // static schedule after the dynamic phase: down rows of the ready items,
-  // then per waiting item its gate_up rows followed by its down rows
-  auto seg_item = [&](uint32_t s, uint32_t& item, uint32_t& kind) {
-    if (s < n_ready) { item = s; kind = 1; return; }
-    s -= n_ready;
-    item = n_ready + s / 2;
-    kind = s & 1;
-  };
-  const uint32_t n_segs = n_ready + 2 * (n_items - n_ready);
-  auto skip_seg = [&](uint32_t sg) {
-    uint32_t ii, kind;
-    seg_item(sg, ii, kind);
-    return (a.dbg & 2) && kind == 1;
+  // Phase bookkeeping (thread 0): gate_up chunks of the ready items
+  // [g0, nr), h staging offsets of all ready items [0, nr)
+  auto setup_phase = [&](uint32_t g0, uint32_t nr) {
+    if (threadIdx.x == 0) {
+      uint32_t off = 0, ch = 0;
+      for (uint32_t i = 0; i < nr; ++i) {
+        h_off[i] = off;
+        off += p->items[i].F * p->items[i].n_tok;
+      }
+      h_off[nr] = off;
+      for (uint32_t i = g0; i < nr; ++i) {
+        s_cpre[i] = ch;
+        ch += (p->items[i].F + gu_rows - 1) / gu_rows;
+      }
+      s_cpre[nr] = ch;
+      s_hstage = (size_t)off * 4 <= a.hbuf_bytes;
+    }
   };
   auto dn_step = [&](uint32_t F) { return min(4u * kGroupWarps, max(1u, SB / (F * 2))); };
 
-  if (warp == 0) {
-    // ------------------------------------------------------- producer
+  // A phase: gate_up of the ready items [g0, nr) in grid-dynamic chunks
+  // (counter gctr); then, unless gu_only, a grid barrier (kFfnReadyDoneCtr,
+  // counting CTAs), the down rows of every ready item [0, nr) (this CTA's
+  // static share), and the items [nr, ni) that wait for their uploads — per
+  // item: static gate_up share, grid barrier on ctr[item], down share.
+  uint32_t k = 0;  // ring step (producer) / this group's next ring step (consumers)
+  const uint32_t cw = warp - 1, grp = cw / kGroupWarps, wg = cw % kGroupWarps;
+  if (warp > 0) k = grp;
+  // B == 1: the token's bf16 activation as MMA B fragments in registers
+  uint32_t xb[kXrBlocks][2];
+  auto load_xb = [&]() {
+    const uint32_t* u32w = reinterpret_cast<const uint32_t*>(a.u);
+#pragma unroll
+    for (int b = 0; b < kXrBlocks; ++b) {
+      if ((uint32_t)b < d / 128) {
+        xb[b][0] = __ldcg(u32w + b * 64 + lane);
+        xb[b][1] = __ldcg(u32w + b * 64 + 32 + lane);
+      } else {
+        xb[b][0] = xb[b][1] = 0u;
+      }
+    }
+  };
+  auto gu_rows_of = [&](const unsigned char* src, const Item& it, uint32_t r, uint32_t n, float* h_item) {
+    if (wg >= n || (a.dbg & 1)) return;
+    const uint32_t nt = it.n_tok;
+    const uint16_t* gs = reinterpret_cast<const uint16_t*>(src) + (size_t)wg * d;
+    const uint16_t* ur = reinterpret_cast<const uint16_t*>(src + n * d * 2) + (size_t)wg * d;
+    if (NTMAX == 1) gu_pair_mma(gs, ur, xb, d, h_item + r + wg);
+    else if (kF32U) {
+      if (nt <= 1) gu_compute_f32<1>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
+      else gu_compute_f32<(NTMAX < 4 ? NTMAX : 4)>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
+    }
+    else if (NTMAX <= 8 || nt <= 8) gu_compute<(NTMAX < 8 ? NTMAX : 8)>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
+    else gu_compute<NTMAX>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
+  };
+  auto signal = [&](uint32_t si, uint32_t ci) {  // this warp finished its share; last warp of the CTA signals
+    __syncwarp();
     if (lane == 0) {
+      __threadfence();
+      if (atomicAdd(&s_arrive[si], 1u) == NC - 1) {
+        __threadfence();
+        atomicAdd(&a.ctr[ci], 1u);
+      }
+    }
+  };
+  auto grid_wait = [&](uint32_t ci) {  // one poller per CTA, then every consumer warp
+    if (cw == 0 && lane == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_u32(&a.ctr[ci]) < G) {
+        __nanosleep(20);
+        if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 2u); break; }
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
+  };
+  auto stage_h = [&](uint32_t i0, uint32_t nr) {  // h of items [i0, nr) -> smem (consumers)
+    const uint32_t tid = cw * 32 + lane, tot4 = h_off[nr] / 4;
+    constexpr uint32_t kU = 8;
+    uint32_t i = i0;  // item of v: v only grows for this thread
+    for (uint32_t v0 = tid; v0 < tot4; v0 += kU * NC * 32) {
+      float4 rv[kU];
+      uint32_t ri[kU];
+#pragma unroll
+      for (uint32_t q = 0; q < kU; ++q) {
+        const uint32_t v = v0 + q * NC * 32;
+        if (v < tot4) {
+          while (h_off[i + 1] / 4 <= v) ++i;
+          const uint32_t loc = v - h_off[i] / 4, qq = p->items[i].F / 4;
+          const uint32_t t = loc / qq, j = loc % qq;
+          rv[q] = __ldcg(reinterpret_cast<const float4*>(a.h + ((size_t)i * kMaxB + t) * a.Fmax) + j);
+          ri[q] = i;
+        }
+      }
+#pragma unroll
+      for (uint32_t q = 0; q < kU; ++q) {
+        const uint32_t v = v0 + q * NC * 32;
+        if (v < tot4) {
+          const uint32_t ii2 = ri[q], Fi = p->items[ii2].F;
+          if (NTMAX == 1 && Fi % 128 == 0) {
+            // bf16 hi / lo words for the tensor-core down pass
+            const uint32_t loc = v - h_off[ii2] / 4;
+            uint32_t* hw = reinterpret_cast<uint32_t*>(hs + h_off[ii2]);
+            uint2 hv, lv;
+            split_h4(rv[q], hv.x, hv.y, lv.x, lv.y);
+            reinterpret_cast<uint2*>(hw)[loc] = hv;
+            reinterpret_cast<uint2*>(hw + Fi / 2)[loc] = lv;
+          } else {
+            reinterpret_cast<float4*>(hs)[v] = rv[q];
+          }
+        }
+      }
+    }
+  };
+  auto dn_rows = [&](const unsigned char* src, const Item& it, uint32_t ii, uint32_t r, uint32_t n, bool staged,
+                     float* acc_g) {
+    if (a.dbg & 1) return;
+    const uint32_t F = it.F, nt = it.n_tok;
+    const float* hsrc = staged ? hs + h_off[ii] : a.h + (size_t)ii * kMaxB * a.Fmax;
+    const uint32_t hstride = staged ? F : a.Fmax;
+    // rows of this step owned by this warp: (row - dlo) % kGroupWarps == wg
+    const uint32_t first = (wg + kGroupWarps - (r - dlo) % kGroupWarps) % kGroupWarps;
+    if (NTMAX == 1 && F % 128 == 0 && staged) {
+      const uint32_t* hw = reinterpret_cast<const uint32_t*>(hsrc);
+      const float wt = it.wt[0];
+      const uint32_t tok = it.tok[0];
+      for (uint32_t q = first; q < n; q += 2 * kGroupWarps) {
+        const uint32_t q1 = q + kGroupWarps < n ? q + kGroupWarps : q;
+        const uint16_t* w0 = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
+        const uint16_t* w1 = reinterpret_cast<const uint16_t*>(src) + (size_t)q1 * F;
+        const float2 dd = dn_pair_mma(w0, w1, hw, F);
+        if (lane == 0) {
+          float* a0 = acc_g + (size_t)(r + q - dlo) * B + tok;
+          *a0 = fmaf(wt, dd.x, *a0);
+          if (q1 != q) {
+            float* a1 = acc_g + (size_t)(r + q1 - dlo) * B + tok;
+            *a1 = fmaf(wt, dd.y, *a1);
+          }
+        }
+      }
+    } else {
+      for (uint32_t q = first; q < n; q += kGroupWarps) {
+        const uint16_t* ws = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
+        float* acc_row = acc_g + (size_t)(r + q - dlo) * B;
+        if (NTMAX == 1 || nt <= 1) dn_compute<1>(ws, hsrc, hstride, F, it, acc_row);
+        else if (NTMAX <= 4 || nt <= 4) dn_compute<(NTMAX < 4 ? NTMAX : 4)>(ws, hsrc, hstride, F, it, acc_row);
+        else if (NTMAX <= 8 || nt <= 8) dn_compute<(NTMAX < 8 ? NTMAX : 8)>(ws, hsrc, hstride, F, it, acc_row);
+        else dn_compute<NTMAX>(ws, hsrc, hstride, F, it, acc_row);
+      }
+    }
+  };
+
+  auto run_phase = [&](uint32_t g0, uint32_t nr, uint32_t ni, uint32_t gctr_i, bool gu_only) {
+    if (warp == 0) {
+      // --------------------------------------------------------- producer
+      if (lane != 0) return;
       const uint64_t pol = l2_evict_first_policy();
-      uint32_t k = 0;  // ring step
       auto acquire = [&]() -> uint32_t {
         const uint32_t st = k % S;
         mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
@@ -549,44 +707,59 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
       };
       // (1) gate_up rows of the ready items, chunk by chunk from a grid-wide
       // counter: SMs that stream faster take more chunks (no static skew)
-      const uint32_t n_chunks = s_cpre[n_ready];
-      uint32_t* gctr = a.ctr + kFfnGuCtr;
-      uint32_t c0 = atomicAdd(gctr, 1u), c1 = atomicAdd(gctr, 1u);
-      uint32_t ii = 0;
-      while (c0 < n_chunks) {
-        const uint32_t cur = c0;
-        c0 = c1;
-        c1 = atomicAdd(gctr, 1u);
-        while (s_cpre[ii + 1] <= cur) ++ii;
-        const Item& it = p->items[ii];
-        const uint32_t F = it.F;
-        const uint32_t r = (cur - s_cpre[ii]) * gu_rows;
-        const uint32_t n = min(gu_rows, F - r);
-        const uint32_t st = acquire();
-        s_stage_hdr[st][0] = (ii << 16) | n;
-        s_stage_hdr[st][1] = r;
-        unsigned char* dst = ring + st * SB;
-        mbar_expect_tx(&full_bar[st], 2 * n * d * 2);
-        bulk_g2s(dst, it.w + (size_t)r * d, n * d * 2, &full_bar[st], pol);
-        bulk_g2s(dst + n * d * 2, it.w + ((size_t)F + r) * d, n * d * 2, &full_bar[st], pol);
-        ++k;
+      if (nr > g0) {
+        const uint32_t n_chunks = s_cpre[nr];
+        uint32_t* gctr = a.ctr + gctr_i;
+        uint32_t c0 = atomicAdd(gctr, 1u), c1 = atomicAdd(gctr, 1u);
+        uint32_t ii = g0;
+        while (c0 < n_chunks) {
+          const uint32_t cur = c0;
+          c0 = c1;
+          c1 = atomicAdd(gctr, 1u);
+          while (s_cpre[ii + 1] <= cur) ++ii;
+          const Item& it = p->items[ii];
+          const uint32_t F = it.F;
+          const uint32_t r = (cur - s_cpre[ii]) * gu_rows;
+          const uint32_t n = min(gu_rows, F - r);
+          const uint32_t st = acquire();
+          s_stage_hdr[st][0] = (ii << 16) | n;
+          s_stage_hdr[st][1] = r;
+          unsigned char* dst = ring + st * SB;
+          mbar_expect_tx(&full_bar[st], 2 * n * d * 2);
+          bulk_g2s(dst, it.w + (size_t)r * d, n * d * 2, &full_bar[st], pol);
+          bulk_g2s(dst + n * d * 2, it.w + ((size_t)F + r) * d, n * d * 2, &full_bar[st], pol);
+          ++k;
+        }
+        const uint32_t k_next = k + NG;
+        for (int g = 0; g < NG; ++g) {  // one end marker per consumer group
+          const uint32_t st = acquire();
+          s_stage_hdr[st][0] = 0;
+          s_stage_hdr[st][1] = k_next;
+          mbar_arrive(&full_bar[st]);
+          ++k;
+        }
       }
-      const uint32_t k_next = k + NG;
-      for (int g = 0; g < NG; ++g) {  // one end marker per consumer group
-        const uint32_t st = acquire();
-        s_stage_hdr[st][0] = 0;
-        s_stage_hdr[st][1] = k_next;
-        mbar_arrive(&full_bar[st]);
-        ++k;
+      if (gu_only) return;
+      if (nr > 0) {
+        // (2) down rows of the ready items (static share)
+        for (uint32_t ii2 = 0; ii2 < nr; ++ii2) {
+          if (a.dbg & 2) break;
+          const Item& it = p->items[ii2];
+          const uint32_t F = it.F, step = dn_step(F);
+          for (uint32_t r = dlo; r < dhi; r += step) {
+            const uint32_t n = min(step, dhi - r);
+            const uint32_t st = acquire();
+            mbar_expect_tx(&full_bar[st], n * F * 2);
+            bulk_g2s(ring + st * SB, it.w + 2 * (size_t)F * d + (size_t)r * F, n * F * 2, &full_bar[st], pol);
+            ++k;
+          }
+        }
       }
-      // (2) the static segments
-      for (uint32_t sg = 0; sg < n_segs; ++sg) {
-        if (skip_seg(sg)) continue;
-        uint32_t ii2, kind;
-        seg_item(sg, ii2, kind);
+      // (3) the waiting items, one at a time
+      for (uint32_t ii2 = nr; ii2 < ni; ++ii2) {
         const Item& it = p->items[ii2];
         const uint32_t F = it.F;
-        if (kind == 0 && it.wait) {
+        if (it.wait) {
           const uint64_t t0 = globaltimer_ns();
           while ((int32_t)(ld_acquire_u32(a.copies_done) - it.wait) < 0) {
             __nanosleep(128);
@@ -596,241 +769,164 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
           // the uploaded bytes are read by the async (bulk-copy) proxy next
           asm volatile("fence.proxy.async;" ::: "memory");
         }
-        uint32_t lo, hi, step, row_bytes;
-        if (kind == 0) {
-          share(F, c, G, lo, hi);
-          step = gu_rows;
-          row_bytes = d * 2;
-        } else {
-          lo = dlo;
-          hi = dhi;
-          step = dn_step(F);
-          row_bytes = F * 2;
-        }
-        for (uint32_t r = lo; r < hi; r += step) {
-          const uint32_t n = min(step, hi - r);
+        uint32_t lo, hi;
+        share(F, c, G, lo, hi);
+        for (uint32_t r = lo; r < hi; r += gu_rows) {
+          const uint32_t n = min(gu_rows, hi - r);
           const uint32_t st = acquire();
           unsigned char* dst = ring + st * SB;
-          if (kind == 0) {
-            mbar_expect_tx(&full_bar[st], 2 * n * row_bytes);
-            bulk_g2s(dst, it.w + (size_t)r * d, n * row_bytes, &full_bar[st], pol);
-            bulk_g2s(dst + n * row_bytes, it.w + ((size_t)F + r) * d, n * row_bytes, &full_bar[st], pol);
-          } else {
-            mbar_expect_tx(&full_bar[st], n * row_bytes);
-            bulk_g2s(dst, it.w + 2 * (size_t)F * d + (size_t)r * F, n * row_bytes, &full_bar[st], pol);
-          }
+          mbar_expect_tx(&full_bar[st], 2 * n * d * 2);
+          bulk_g2s(dst, it.w + (size_t)r * d, n * d * 2, &full_bar[st], pol);
+          bulk_g2s(dst + n * d * 2, it.w + ((size_t)F + r) * d, n * d * 2, &full_bar[st], pol);
+          ++k;
+        }
+        if (a.dbg & 2) continue;
+        const uint32_t step = dn_step(F);
+        for (uint32_t r = dlo; r < dhi; r += step) {
+          const uint32_t n = min(step, dhi - r);
+          const uint32_t st = acquire();
+          mbar_expect_tx(&full_bar[st], n * F * 2);
+          bulk_g2s(ring + st * SB, it.w + 2 * (size_t)F * d + (size_t)r * F, n * F * 2, &full_bar[st], pol);
           ++k;
         }
       }
+      return;
     }
-  } else {
-    // ------------------------------------------------------ consumers
+    // ----------------------------------------------------------- consumers
     // Ring step k (stage k % S) belongs to consumer group k % NG (S is a
-    // multiple of NG, so a stage always has the same group and its phases
-    // are consumed in order). Gate_up completion is aggregated per CTA
-    // (ctr[i] counts CTAs, G when complete); the down pass of an item waits
-    // on it through one poller and a consumer-wide named barrier.
-    const uint32_t cw = warp - 1, grp = cw / kGroupWarps, wg = cw % kGroupWarps;
+    // multiple of NG, so a stage always has the same group and its phases are
+    // consumed in order).
     float* acc_g = acc_s + grp * acc_n;
-    // B == 1: the token's bf16 activation as MMA B fragments in registers
-    uint32_t xb[kXrBlocks][2];
-    auto load_xb = [&]() {
-      const uint32_t* u32w = reinterpret_cast<const uint32_t*>(a.u);
-#pragma unroll
-      for (int b = 0; b < kXrBlocks; ++b) {
-        if ((uint32_t)b < d / 128) {
-          xb[b][0] = __ldg(u32w + b * 64 + lane);
-          xb[b][1] = __ldg(u32w + b * 64 + 32 + lane);
-        } else {
-          xb[b][0] = xb[b][1] = 0u;
-        }
-      }
-    };
-    auto gu_rows_of = [&](const unsigned char* src, const Item& it, uint32_t r, uint32_t n, float* h_item) {
-      if (wg >= n || (a.dbg & 1)) return;
-      const uint32_t nt = it.n_tok;
-      const uint16_t* gs = reinterpret_cast<const uint16_t*>(src) + (size_t)wg * d;
-      const uint16_t* ur = reinterpret_cast<const uint16_t*>(src + n * d * 2) + (size_t)wg * d;
-      if (NTMAX == 1) gu_pair_mma(gs, ur, xb, d, h_item + r + wg);
-      else if (kF32U) {
-        if (nt <= 1) gu_compute_f32<1>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
-        else gu_compute_f32<(NTMAX < 4 ? NTMAX : 4)>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
-      }
-      else if (NTMAX <= 8 || nt <= 8) gu_compute<(NTMAX < 8 ? NTMAX : 8)>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
-      else gu_compute<NTMAX>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
-    };
-    auto signal_gu = [&](uint32_t ci) {  // this warp finished its share of item ci's gate_up
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();
-        if (atomicAdd(&s_arrive[ci], 1u) == NC - 1) {
-          __threadfence();
-          atomicAdd(&a.ctr[ci], 1u);
-        }
-      }
-    };
-    if (NTMAX == 1) load_xb();
-    // (1) dynamic gate_up of the ready items
-    uint32_t k = grp;
-    for (;;) {
-      const uint32_t st = k % S;
-      mbar_wait(&full_bar[st], (k / S) & 1);
-      if (ts && k == grp && grp == 0 && lane == 0 && wg == 0) ts[2] = globaltimer_ns();
-      const uint32_t h0 = s_stage_hdr[st][0], r = s_stage_hdr[st][1];
-      const uint32_t n = h0 & 0xffffu;
-      if (n == 0) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty_bar[st]);
-        k = r;
-        break;
-      }
-      const uint32_t ii = h0 >> 16;
-      gu_rows_of(ring + st * SB, p->items[ii], r, n, a.h + (size_t)ii * kMaxB * a.Fmax);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[st]);
-      k += NG;
-    }
-    if (n_ready) signal_gu(0);
-    if (ts && cw == 0 && lane == 0) ts[3] = globaltimer_ns();
-    // (2) the static segments
-    for (uint32_t sg = 0; sg < n_segs; ++sg) {
-      if (skip_seg(sg)) continue;
-      uint32_t ii, kind;
-      seg_item(sg, ii, kind);
-      const Item& it = p->items[ii];
-      const uint32_t F = it.F, nt = it.n_tok;
-      float* h_item = a.h + (size_t)ii * kMaxB * a.Fmax;
-      uint32_t lo, hi, step;
-      const float* hsrc = h_item;
-      uint32_t hstride = a.Fmax;
-      if (kind == 0) {
-        share(F, c, G, lo, hi);
-        step = gu_rows;
-      } else {
-        lo = dlo;
-        hi = dhi;
-        step = dn_step(F);
-        const bool ready = ii < n_ready;
-        const bool first_dn = ready && sg == 0;  // first down segment of the ready group
-        if (!ready || first_dn) {
-          // one poller per CTA, then a consumer-wide barrier releases every warp
-          const uint32_t wc = ready ? 0 : ii;
-          if (cw == 0 && lane == 0) {
-            const uint64_t t0 = globaltimer_ns();
-            while (ld_acquire_u32(&a.ctr[wc]) < G) {
-              __nanosleep(20);
-              if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 2u); break; }
-            }
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
-        }
-        if (first_dn && s_hstage) {
-          // stage h of all ready items into shared memory in one batch;
-          // every load issued before any store
-          const uint32_t tid = cw * 32 + lane, tot4 = h_off[n_ready] / 4;
-          constexpr uint32_t kU = 8;
-          uint32_t i = 0;  // item of v: v only grows for this thread
-          for (uint32_t v0 = tid; v0 < tot4; v0 += kU * NC * 32) {
-            float4 rv[kU];
-            uint32_t ri[kU];
-#pragma unroll
-            for (uint32_t q = 0; q < kU; ++q) {
-              const uint32_t v = v0 + q * NC * 32;
-              if (v < tot4) {
-                while (h_off[i + 1] / 4 <= v) ++i;
-                const uint32_t loc = v - h_off[i] / 4, qq = p->items[i].F / 4;
-                const uint32_t t = loc / qq, j = loc % qq;
-                rv[q] = __ldcg(reinterpret_cast<const float4*>(a.h + ((size_t)i * kMaxB + t) * a.Fmax) + j);
-                ri[q] = i;
-              }
-            }
-#pragma unroll
-            for (uint32_t q = 0; q < kU; ++q) {
-              const uint32_t v = v0 + q * NC * 32;
-              if (v < tot4) {
-                const uint32_t ii2 = ri[q], Fi = p->items[ii2].F;
-                if (NTMAX == 1 && Fi % 128 == 0) {
-                  // bf16 hi / lo words for the tensor-core down pass
-                  const uint32_t loc = v - h_off[ii2] / 4;
-                  uint32_t* hw = reinterpret_cast<uint32_t*>(hs + h_off[ii2]);
-                  uint2 hv, lv;
-                  split_h4(rv[q], hv.x, hv.y, lv.x, lv.y);
-                  reinterpret_cast<uint2*>(hw)[loc] = hv;
-                  reinterpret_cast<uint2*>(hw + Fi / 2)[loc] = lv;
-                } else {
-                  reinterpret_cast<float4*>(hs)[v] = rv[q];
-                }
-              }
-            }
-          }
-          asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
-        }
-        if (ts && first_dn && cw == 0 && lane == 0) ts[4] = globaltimer_ns();
-        if (ready && s_hstage) {
-          hsrc = hs + h_off[ii];
-          hstride = F;
-        }
-      }
-      if (kind == 0) {
-        // a waiting item's gate_up rows (static share)
-        if (NTMAX == 1) load_xb();
-        for (uint32_t r = lo; r < hi; r += step, ++k) {
-          const uint32_t st = k % S;
-          if (st % NG != grp) continue;
-          mbar_wait(&full_bar[st], (k / S) & 1);
-          gu_rows_of(ring + st * SB, it, r, min(step, hi - r), h_item);
+    if (nr > g0) {
+      if (NTMAX == 1) load_xb();
+      for (;;) {  // (1) dynamic gate_up
+        const uint32_t st = k % S;
+        mbar_wait(&full_bar[st], (k / S) & 1);
+        const uint32_t h0 = s_stage_hdr[st][0], r = s_stage_hdr[st][1];
+        const uint32_t n = h0 & 0xffffu;
+        if (n == 0) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty_bar[st]);
+          k = r + grp;  // r = first step after the end markers; this group's first step
+          break;
         }
-        signal_gu(ii);
-        continue;
+        const uint32_t ii = h0 >> 16;
+        gu_rows_of(ring + st * SB, p->items[ii], r, n, a.h + (size_t)ii * kMaxB * a.Fmax);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+        k += NG;
       }
-      for (uint32_t r = lo; r < hi; r += step, ++k) {
-        const uint32_t st = k % S;
-        if (st % NG != grp) continue;
-        const uint32_t n = min(step, hi - r);
-        mbar_wait(&full_bar[st], (k / S) & 1);
-        const unsigned char* src = ring + st * SB;
-        if (!(a.dbg & 1)) {
-          // rows of this step owned by this warp: (row - dlo) % kGroupWarps == wg
-          const uint32_t first = (wg + kGroupWarps - (r - dlo) % kGroupWarps) % kGroupWarps;
-          const bool mma_dn = NTMAX == 1 && F % 128 == 0 && ii < n_ready && s_hstage;
-          if (mma_dn) {
-            const uint32_t* hw = reinterpret_cast<const uint32_t*>(hsrc);
-            const float wt = it.wt[0];
-            const uint32_t tok = it.tok[0];
-            for (uint32_t q = first; q < n; q += 2 * kGroupWarps) {
-              const uint32_t q1 = q + kGroupWarps < n ? q + kGroupWarps : q;
-              const uint16_t* w0 = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
-              const uint16_t* w1 = reinterpret_cast<const uint16_t*>(src) + (size_t)q1 * F;
-              const float2 dd = dn_pair_mma(w0, w1, hw, F);
-              if (lane == 0) {
-                float* a0 = acc_g + (size_t)(r + q - dlo) * B + tok;
-                *a0 = fmaf(wt, dd.x, *a0);
-                if (q1 != q) {
-                  float* a1 = acc_g + (size_t)(r + q1 - dlo) * B + tok;
-                  *a1 = fmaf(wt, dd.y, *a1);
-                }
-              }
-            }
-          } else {
-            for (uint32_t q = first; q < n; q += kGroupWarps) {
-              const uint16_t* ws = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
-              float* acc_row = acc_g + (size_t)(r + q - dlo) * B;
-              if (NTMAX == 1 || nt <= 1) dn_compute<1>(ws, hsrc, hstride, F, it, acc_row);
-              else if (NTMAX <= 4 || nt <= 4) dn_compute<(NTMAX < 4 ? NTMAX : 4)>(ws, hsrc, hstride, F, it, acc_row);
-              else if (NTMAX <= 8 || nt <= 8) dn_compute<(NTMAX < 8 ? NTMAX : 8)>(ws, hsrc, hstride, F, it, acc_row);
-              else dn_compute<NTMAX>(ws, hsrc, hstride, F, it, acc_row);
-            }
+    }
+    if (gu_only) {
+      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[8] = globaltimer_ns();
+      return;
+    }
+    if (nr > 0) {
+      signal(kMaxItems, kFfnReadyDoneCtr);
+      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[9] = globaltimer_ns();
+      if (ts && cw == 0 && lane == 0) ts[3] = globaltimer_ns();
+      // (2) down rows of the ready items, after every CTA's gate_up
+      grid_wait(kFfnReadyDoneCtr);
+      if (s_hstage) {
+        stage_h(0, nr);
+        asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
+      }
+      if (ts && cw == 0 && lane == 0) ts[4] = globaltimer_ns();
+      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[10] = globaltimer_ns();
+      if (!(a.dbg & 2)) {
+        // steps are numbered globally: walk them, take this group's
+        uint32_t kk = k - grp;  // global step of the first down stage
+        for (uint32_t ii = 0; ii < nr; ++ii) {
+          const Item& it = p->items[ii];
+          const uint32_t F = it.F, step = dn_step(F);
+          for (uint32_t r = dlo; r < dhi; r += step, ++kk) {
+            const uint32_t st = kk % S;
+            if (st % NG != grp) continue;
+            mbar_wait(&full_bar[st], (kk / S) & 1);
+            dn_rows(ring + st * SB, it, ii, r, min(step, dhi - r), s_hstage != 0, acc_g);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
           }
         }
+        k = kk + grp;
+      }
+    }
+    // (3) the waiting items
+    uint32_t kk = k - grp;
+    for (uint32_t ii = nr; ii < ni; ++ii) {
+      const Item& it = p->items[ii];
+      const uint32_t F = it.F;
+      float* h_item = a.h + (size_t)ii * kMaxB * a.Fmax;
+      uint32_t lo, hi;
+      share(F, c, G, lo, hi);
+      if (NTMAX == 1) load_xb();
+      for (uint32_t r = lo; r < hi; r += gu_rows, ++kk) {
+        const uint32_t st = kk % S;
+        if (st % NG != grp) continue;
+        mbar_wait(&full_bar[st], (kk / S) & 1);
+        gu_rows_of(ring + st * SB, it, r, min(gu_rows, hi - r), h_item);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar[st]);
+      }
+      signal(ii, ii);
+      if (a.dbg & 2) continue;
+      grid_wait(ii);
+      const uint32_t step = dn_step(F);
+      for (uint32_t r = dlo; r < dhi; r += step, ++kk) {
+        const uint32_t st = kk % S;
+        if (st % NG != grp) continue;
+        mbar_wait(&full_bar[st], (kk / S) & 1);
+        dn_rows(ring + st * SB, it, ii, r, min(step, dhi - r), false, acc_g);
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[st]);
       }
     }
+    k = kk + grp;
+  };
+
+  // ---- gate_up of the speculative items, overlapped with the rest of the
+  // decision (their down rows go with the final plan's ready items)
+  if (after_spec && n_spec) {
+    setup_phase(0, n_spec);
+    __syncthreads();
+    run_phase(0, n_spec, n_spec, kFfnSpecGuCtr, true);
+  }
+  if (after_spec) {
+    // ---- the final plan: every item after the speculative ones. Taken from
+    // the decide kernel's release of spec_flag[1], not griddepcontrol.wait
+    // (kernel completion flushes behind this kernel's own weight stream)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_u32(a.spec_flag + 1) != a.seq) {
+        __nanosleep(32);
+        if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 6u); break; }
+      }
+      if (a.tl && c == 0) a.tl[0] = globaltimer_ns();
+    }
+    __syncthreads();
+    const Plan* gp = a.plan;
+    if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(p)[threadIdx.x] = __ldcg(reinterpret_cast<const uint32_t*>(gp) + threadIdx.x);
+    {
+      const uint64_t* src = reinterpret_cast<const uint64_t*>(gp->items + n_spec);
+      uint64_t* dst = reinterpret_cast<uint64_t*>(p->items + n_spec);
+      const uint32_t words = (uint32_t)((a.plan_smem - offsetof(Plan, items)) / 8 - n_spec * (sizeof(Item) / 8));
+      for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
+    }
+    if (threadIdx.x == 0) p->d2d_elems = __ldcg(&gp->d2d_elems);
+  }
+  // every warp has left the speculative phase and sees the final plan; the
+  // down accumulators of the speculative items stay in acc_s
+  __syncthreads();
+  {
+    const uint32_t n_items = p->n_items, n_ready = p->n_ready;
+    setup_phase(n_spec, n_ready);
+    __syncthreads();
+    run_phase(n_spec, n_ready, n_items, kFfnGuCtr, false);
   }
   __syncthreads();
   if (ts && threadIdx.x == 0) ts[5] = globaltimer_ns();
+  if (a.tl && c == 0 && threadIdx.x == 0) a.tl[11] = globaltimer_ns();
   // epilogue: group partial sums (fixed order), residual add (x_in was read
   // at the start), bf16 hidden for the next layer, fp32 MoE output
   for (uint32_t i = threadIdx.x, j = 0; i < (dhi - dlo) * B; i += blockDim.x, ++j) {
@@ -856,10 +952,11 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
       }
     }
     __syncthreads();
-    const uint64_t nv = gp->d2d_elems / 8;
+    const Plan* gp = a.plan;
+    const uint64_t nv = p->d2d_elems / 8;
     for (uint32_t j = 0; j < n_d2d; ++j) {
-      const uint4* src = reinterpret_cast<const uint4*>(gp->d2d[j].src);
-      uint4* dst = reinterpret_cast<uint4*>(gp->d2d[j].dst);
+      const uint4* src = reinterpret_cast<const uint4*>(__ldcg(reinterpret_cast<const unsigned long long*>(&gp->d2d[j].src)));
+      uint4* dst = reinterpret_cast<uint4*>(__ldcg(reinterpret_cast<const unsigned long long*>(&gp->d2d[j].dst)));
       for (uint64_t v = c * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)G * blockDim.x)
         dst[v] = ldg_cg(src + v);
     }
@@ -884,7 +981,8 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
 // Kernel instance and shared-memory layout for a model / batch. Throws
 // nothing: returns stages == 0 when the shapes do not fit.
 inline FfnLaunch ffn_launch_config(uint32_t B, uint32_t d, uint32_t F, uint32_t S, uint32_t E, uint32_t top_k,
-                                   int sms) {
+                                   int grid) {
+  const int sms = grid;  // CTAs of the persistent grid
   FfnLaunch L{};
   int nc;
   if (B <= 1) { L.fn = ffn_tma_kernel<1, 12>; nc = 12; }
@@ -904,15 +1002,20 @@ inline FfnLaunch ffn_launch_config(uint32_t B, uint32_t d, uint32_t F, uint32_t 
   // h of the ready items (shared + top-k experts x tokens) staged in smem
   // when it fits beside one ring stage of one pair per group
   const size_t hwant = ((size_t)S + (size_t)top_k * F) * B * 4;
-  const size_t min_ring = 2ull * ng * pair;
+  const size_t min_ring = 2ull * ng * std::max<size_t>(pair, (2 * std::max(F, S) + 1023) / 1024 * 1024);
   L.hbuf_bytes = (uint32_t)(kFfnSmemMax >= fixed + min_ring + hwant ? hwant : 0);
   const size_t budget = kFfnSmemMax - fixed - L.hbuf_bytes;
-  // two stages per consumer group; each stage up to kGroupWarps row pairs
-  const uint32_t per = 2;
-  size_t sb = budget / (per * ng) / pair * pair;
+  // two stages per consumer group; a stage holds up to kGroupWarps gate+up
+  // row pairs and at least one down row (2 * ffn bytes) and one pair
+  const size_t fmax = std::max(F, S);
+  const size_t min_sb = std::max<size_t>(pair, (2 * fmax + 1023) / 1024 * 1024);
+  size_t sb = budget / (2 * ng) / pair * pair;
   if (sb > kGroupWarps * pair) sb = kGroupWarps * pair;
+  if (sb < min_sb) sb = min_sb;
+  uint32_t st = (uint32_t)std::min<size_t>(kMaxStages, budget / sb);
+  st -= st % ng;  // a stage always belongs to the same consumer group
   L.stage_bytes = (uint32_t)sb;
-  L.stages = sb >= pair ? per * ng : 0;
+  L.stages = st >= ng ? st : 0;
   L.smem = (size_t)L.stages * L.stage_bytes + fixed + L.hbuf_bytes;
   return L;
 }

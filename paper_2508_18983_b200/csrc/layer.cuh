@@ -43,6 +43,8 @@ struct D2D {
 struct Plan {
   uint32_t n_items, n_ready, n_d2d, seq;
   uint64_t d2d_elems;
+  uint32_t n_spec;    // items [0, n_spec) were published early (speculative plan)
+  uint32_t pad;
   Item items[kMaxItems];
   D2D d2d[kMaxE];
 };

@@ -101,6 +101,9 @@ struct DecideArgs {
   uint32_t n_stage;
   uint64_t expert_elems;
   Plan* plan;
+  Plan* spec_plan;            // early plan of the certain, ready items (B == 1) or null
+  uint32_t* spec_flag;        // := seq once spec_plan is published
+  uint32_t spec_late;         // diagnostics: publish after the whole decision
   uint32_t* ffn_ctr;
   const uint32_t* copies_done; // upload ids landed so far (written by the copy stream)
   MailEntry* ring;
@@ -143,6 +146,8 @@ struct DecideKSmem {
   MailCmd cmd[kMaxCmds];
   uint32_t n_cmds;
   uint32_t landed;            // copies_done when the step's state was staged
+  uint32_t spec_n;            // items in the speculative plan (0: none published)
+  uint64_t spec_set;          // routed experts in it
   uint64_t it, seq;
   int last;
   // uploads published early by EarlyPublish (ids + destinations)
@@ -220,9 +225,14 @@ __device__ __forceinline__ void wait_ring_slot(const DecideArgs& a, uint64_t mse
 // Mailbox entry A of a layer-step (sequence 2*seq-1): the demand loads and
 // BA-streamed experts, published from inside the decision step the moment
 // the lists are final. Entry B (2*seq) carries the prefetches later.
+__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d);
+
 struct EarlyPublish {
   const DecideArgs* a;
   DecideKSmem* sm;
+  __device__ void classified(DecideSmem* d) const {
+    if (!a->spec_late) publish_spec(*a, sm, d);
+  }
   __device__ void operator()(DecideSmem* d, uint32_t n_load, uint32_t n_cpu) const {
     if (lane_id() == 0) {
       const DecideArgs& A = *a;
@@ -280,6 +290,54 @@ struct EarlyPublish {
   }
 };
 
+// Speculative plan (batch 1): right after classification the shared expert
+// and every routed expert certain to be selected — the top-score class with
+// substitution on (route pass 1, router.cpp:114-120), the k actives without
+// (plain_top_k) — that is resident in the pre-route snapshot with its upload
+// landed is final: hits are shielded (pipeline.cpp:196-201), so its slot
+// cannot change in this step. Publishing these lets the FFN kernel (already
+// resident via PDL) stream them while the rest of the decision runs.
+__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d) {
+  if (threadIdx.x != 0) return;
+  sm->spec_n = 0;
+  sm->spec_set = 0;
+  if (!a.spec_plan) return;
+  const DevCfg& cfg = sm->cfg;
+  const LayerState* ls = &sm->ls;
+  const uint64_t certain = (cfg.er ? d->top[0] : d->act[0]) & ls->mask;
+  Plan* sp = a.spec_plan;
+  uint32_t n = 0;
+  auto item = [&](const uint16_t* w, uint32_t F, uint32_t kind, uint32_t e, float wt) {
+    Item& it = sp->items[n++];
+    it.w = w;
+    it.F = F;
+    it.wait = 0;
+    it.n_tok = 1;
+    it.kind = kind;
+    it.expert = e;
+    it.tok[0] = 0;
+    it.wt[0] = wt;
+  };
+  if (a.shared_w) item(a.shared_w, a.S, 0, 0, a.shared_gate ? sm->sg[0] : 1.0f);
+  uint64_t set = 0;
+  for (uint64_t m = certain; m; m &= m - 1) {
+    const uint32_t e = __ffsll((long long)m) - 1;
+    const int slot = ls->slot_of[e];
+    const uint32_t w = ls->slot_copy[slot];
+    if (w && (int32_t)(sm->landed - w) < 0) continue;  // upload still in flight
+    item(slot_ptr(a, a.layer, slot), a.F, 1, e, __fmul_rn(sm->sc[0][e], a.routed_scale));
+    set |= 1ull << e;
+  }
+  sp->n_items = n;
+  sp->n_ready = n;
+  sp->n_spec = n;
+  sp->seq = (uint32_t)sm->seq;
+  sm->spec_n = n;
+  sm->spec_set = set;
+  __threadfence();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
+}
+
 // Thread 0 builds the FFN plan and the upload commands in shared memory.
 __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
   const DevCfg& cfg = sm->cfg;
@@ -310,6 +368,11 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
     return id;
   };
   if (a.shared_w) add_item(a.shared_w, a.S, 0, 0, 0);
+  // the speculative plan's routed experts next, in its (ascending) order
+  for (uint64_t m = sm->spec_set; m; m &= m - 1) {
+    const uint32_t e = __ffsll((long long)m) - 1;
+    add_item(slot_ptr(a, layer, ls->slot_of[e]), a.F, 0, 1, e);
+  }
   // uploads already landed (the copy stream is FIFO and copies_done only
   // grows; read during staging): their slots are plain residents again
   const uint32_t landed = sm->landed;
@@ -326,6 +389,7 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
       const int slot = out.res_slot[i];
       const uint32_t wait = ls->slot_copy[slot];
       if ((wait == 0) != (pass == 0)) continue;
+      if ((sm->spec_set >> e) & 1) continue;  // already first
       add_item(slot_ptr(a, layer, slot), a.F, wait, 1, e);
     }
   }
@@ -367,6 +431,7 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
   st->ffn_launches += 1;
   p->n_items = n_items;
   p->n_ready = n_ready;
+  p->n_spec = sm->spec_n;
   p->n_d2d = n_d2d;
   p->d2d_elems = a.expert_elems;
   p->seq = (uint32_t)sm->seq;
@@ -442,6 +507,12 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
 
   const DecideArgs& a = ga.d;
   if (a.tl && threadIdx.x == 0) a.tl[3] = globaltimer_ns();
+  // the FFN grid counters of this step, zeroed before the FFN kernel (which
+  // may already be resident) can see the speculative plan or the final one;
+  // thread 0 alone, so its release of the spec flag / the kernel boundary
+  // publishes them
+  if (threadIdx.x == 0)
+    for (uint32_t i = 0; i < (uint32_t)kFfnCtrWords; ++i) a.ffn_ctr[i] = 0;
   MOEB_T(t_elect);
   const int warp = warp_id(), lane = lane_id();
   const uint32_t nw = blockDim.x >> 5;
@@ -553,6 +624,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     toks = a.toks + (sm->seq - 1) * B;
   }
   decide_step(cx, &sm->d, &sm->n, &sm->s, rec, toks, EarlyPublish{&a, sm});
+  if (a.spec_late) publish_spec(a, sm, &sm->d);  // diagnostics (MOEB_SPEC_LATE)
   __syncthreads();
   MOEB_T(t_decided);
 
@@ -563,7 +635,6 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     for (uint32_t i = 0; i < sm->d.nsel[t]; ++i) s += sm->sc[t][sm->d.sel[t][i]];
     sm->denom[t] = s;
   }
-  for (uint32_t i = threadIdx.x; i < kFfnCtrWords; i += blockDim.x) a.ffn_ctr[i] = 0;
   __syncthreads();
   if (threadIdx.x == 0) {
     build_plan(a, sm);
@@ -597,6 +668,15 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
     const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + sm->plan.n_d2d * sizeof(D2D) / 8;
     for (uint32_t i = d0 + threadIdx.x; i < d1; i += blockDim.x) dst[i] = src[i];
+    if (a.spec_plan) {
+      // the FFN kernel (already running its speculative items) takes the
+      // final plan from this flag instead of waiting for this kernel to
+      // complete: every writer fences, then one release
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 1), "r"((uint32_t)sm->seq) : "memory");
+    }
     MailEntry* me = &a.ring[(2 * sm->seq) % kRing];
     const uint32_t nc = sm->n_cmds;
     const uint64_t* cs = reinterpret_cast<const uint64_t*>(sm->cmd);
@@ -676,10 +756,12 @@ struct moeb_stack {
   DevBuf<EngineState> st;
   DevBuf<LayerState> layers;
   DevBuf<double> hist;
-  DevBuf<Plan> plan;
+  DevBuf<Plan> plan, spec_plan;
+  DevBuf<uint32_t> spec_flag;
+  bool spec = false;
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
   DevBuf<StepRec> recs;
-  DevBuf<uint64_t> timeline;  // [rec_cap][8] (MOEB_MODEL_TRACE_TIMELINE)
+  DevBuf<uint64_t> timeline;  // [rec_cap][kTlWords] (MOEB_MODEL_TRACE_TIMELINE)
   DevBuf<TokRec> toks;
   uint64_t rec_cap = 0;
   uint64_t trace_steps = 0, total_iters = ~0ull;
@@ -955,6 +1037,13 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   MOEB_CUDA(cudaMemcpyAsync(S->st.p, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
   reset_state(S, s);
   S->plan.alloc(1);
+  // speculative FFN start (batch 1, combine weights known at classification)
+  S->spec = B == 1 && !m.renormalize && getenv("MOEB_NO_SPEC") == nullptr;
+  if (S->spec) {
+    S->spec_plan.alloc(1);
+    S->spec_flag.alloc(2);  // [0] speculative plan published, [1] final plan published
+    S->spec_flag.zero(s);
+  }
   S->ffn_ctr.alloc(kFfnCtrWords);
   S->ffn_ctr.zero(s);
   S->copies_done.alloc(1);
@@ -962,7 +1051,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   S->ffn_done.alloc(1);
   S->ffn_done.zero(s);
   if (m.flags & MOEB_MODEL_TRACE_TIMELINE) {
-    S->timeline.alloc(16384 * 8);
+    S->timeline.alloc(16384 * kTlWords);
     S->timeline.zero(s);
   }
   if (m.flags & MOEB_MODEL_LOG_STEPS) {
@@ -978,7 +1067,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // kernel resources: FFN launch shape (ring stages, h staging, accumulators)
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  S->ffn = ffn_launch_config(B, d, F, Sh, E, cfg.top_k, sms);
+  S->ffn = ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
   if (S->ffn.stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
   S->ticket.alloc(1);
   S->ticket.zero(s);
@@ -994,7 +1083,10 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   int occ = 0;
   MOEB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, S->ffn.fn, S->ffn.threads, S->ffn.smem));
   if (occ < 1) throw Error(5, "ffn kernel does not fit on an SM");
-  S->ffn_grid = sms;  // one persistent CTA per SM (the per-item counters need co-residency)
+  // one persistent CTA per SM (the grid counters need co-residency); with
+  // the speculative start the FFN runs beside the deciding CTA, so one SM
+  // is left to it
+  S->ffn_grid = S->spec ? sms - 1 : sms;
   MOEB_CUDA(cudaStreamSynchronize(s));
   S->copier = std::thread([S] { S->copy_loop(); });
 }
@@ -1066,6 +1158,9 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.n_stage = S->n_stage;
     a.expert_elems = S->expert_elems;
     a.plan = S->plan.p;
+    a.spec_plan = S->spec ? S->spec_plan.p : nullptr;
+    a.spec_flag = S->spec_flag.p;
+    a.spec_late = getenv("MOEB_SPEC_LATE") != nullptr;
     a.ffn_ctr = S->ffn_ctr.p;
     a.copies_done = S->copies_done.p;
     a.ring = S->ring_dev;
@@ -1076,7 +1171,7 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.rec_cap = S->rec_cap;
     a.it = S->host_it;
     a.seq = ++S->host_seq;
-    a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * 8 : nullptr;
+    a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * kTlWords : nullptr;
     ga.ticket = S->ticket.p;
     if (S->timing) S->tick(s);
     launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3((rows + 1) / 2), dim3(kGdThreads),
@@ -1103,6 +1198,9 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     f.acc_rows = S->ffn.acc_rows;
     f.plan_smem = S->ffn.plan_smem;
     f.tl = a.tl;
+    f.spec_plan = a.spec_plan;
+    f.spec_flag = S->spec_flag.p;
+    f.seq = (uint32_t)a.seq;
     f.x_smem = S->ffn.x_smem;
     launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s, &f);
     S->n_launch_layers += 1;
@@ -1294,7 +1392,7 @@ int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n) {
   return guarded([&] {
     if (!s->timeline.p) throw Error(1, "timeline: create the stack with MOEB_MODEL_TRACE_TIMELINE");
     MOEB_CUDA(cudaStreamSynchronize(s->stream));
-    const size_t have = (size_t)std::min<uint64_t>(s->host_seq, 16384) * 8;
+    const size_t have = (size_t)std::min<uint64_t>(s->host_seq, 16384) * kTlWords;
     *n = have;
     if (out) MOEB_CUDA(cudaMemcpy(out, s->timeline.p, std::min(cap, have) * 8, cudaMemcpyDeviceToHost));
   });

@@ -128,7 +128,7 @@ def test_c5_independent_streams_concurrent_handles(gpu):
     handles = []
     for seed in (7, 8):
         kw = dict(num_layers=L, experts=s["E"], top_k=s["k"], batch=B, slots=16, alpha=0.25, seed=seed)
-        st = gpu.Stack(gpu.Config.make(**kw), s["d"], s["F"], s["S"], weight_seed=7, log_steps=True)
+        st = gpu.Stack(gpu.Config.make(**kw), s["d"], s["F"], s["S"], weight_seed=seed, log_steps=True)
         st.set_logits_trace(gpu.trace_logits(gpu.generate_trace(L, s["E"], B, T, seed)), T)
         xs = torch.randn(T, B, s["d"], generator=torch.Generator().manual_seed(seed)).to(torch.bfloat16).cuda()
         handles.append((st, kw, xs))
