@@ -490,9 +490,12 @@ __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, Nex
 // classified(): called by every thread right after classification (before
 // routing), with the pre-route residency untouched — the stack publishes the
 // experts certain to be selected there (speculative FFN start).
+// plan_ready(): called by warp 0 once the executing layer's outcome (hits,
+// loads, BA split, deferred admissions) is final, before the prefetch phase.
 struct NoHook {
   __device__ void operator()(DecideSmem*, uint32_t, uint32_t) const {}
   __device__ void classified(DecideSmem*) const {}
+  __device__ void plan_ready(DecideSmem*) const {}
 };
 
 template <class Hook = NoHook>
@@ -775,6 +778,9 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       __syncwarp();
     }
   }
+  if (lane == 0) sm->out.completion = completion;
+  __syncwarp();
+  on_loads.plan_ready(sm);
 
   mark(7);
   // prefetch for the next layer (pipeline.cpp:293-344)

@@ -544,20 +544,18 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
   __syncthreads();
   if (a.tl && c == 0 && threadIdx.x == 0 && !after_spec) a.tl[0] = globaltimer_ns();
 
-  // Phase bookkeeping (thread 0): gate_up chunks of the ready items
-  // [g0, nr), h staging offsets of all ready items [0, nr)
+  // Phase bookkeeping (thread 0): gate_up chunks and h staging offsets of
+  // the phase's ready items [g0, nr)
   auto setup_phase = [&](uint32_t g0, uint32_t nr) {
     if (threadIdx.x == 0) {
       uint32_t off = 0, ch = 0;
-      for (uint32_t i = 0; i < nr; ++i) {
-        h_off[i] = off;
-        off += p->items[i].F * p->items[i].n_tok;
-      }
-      h_off[nr] = off;
       for (uint32_t i = g0; i < nr; ++i) {
+        h_off[i] = off;
         s_cpre[i] = ch;
+        off += p->items[i].F * p->items[i].n_tok;
         ch += (p->items[i].F + gu_rows - 1) / gu_rows;
       }
+      h_off[nr] = off;
       s_cpre[nr] = ch;
       s_hstage = (size_t)off * 4 <= a.hbuf_bytes;
     }
@@ -565,10 +563,10 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
   auto dn_step = [&](uint32_t F) { return min(4u * kGroupWarps, max(1u, SB / (F * 2))); };
 
   // A phase: gate_up of the ready items [g0, nr) in grid-dynamic chunks
-  // (counter gctr); then, unless gu_only, a grid barrier (kFfnReadyDoneCtr,
-  // counting CTAs), the down rows of every ready item [0, nr) (this CTA's
-  // static share), and the items [nr, ni) that wait for their uploads — per
-  // item: static gate_up share, grid barrier on ctr[item], down share.
+  // (counter gctr_i), a grid barrier (counter done_i, counting CTAs), the
+  // down rows of those items (this CTA's static share), then the items
+  // [nr, ni) that wait for their uploads — per item: static gate_up share,
+  // grid barrier on ctr[item], down share.
   uint32_t k = 0;  // ring step (producer) / this group's next ring step (consumers)
   const uint32_t cw = warp - 1, grp = cw / kGroupWarps, wg = cw % kGroupWarps;
   if (warp > 0) k = grp;
@@ -695,7 +693,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
     }
   };
 
-  auto run_phase = [&](uint32_t g0, uint32_t nr, uint32_t ni, uint32_t gctr_i, bool gu_only) {
+  auto run_phase = [&](uint32_t g0, uint32_t nr, uint32_t ni, uint32_t gctr_i, uint32_t done_i) {
     if (warp == 0) {
       // --------------------------------------------------------- producer
       if (lane != 0) return;
@@ -738,11 +736,8 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
           mbar_arrive(&full_bar[st]);
           ++k;
         }
-      }
-      if (gu_only) return;
-      if (nr > 0) {
         // (2) down rows of the ready items (static share)
-        for (uint32_t ii2 = 0; ii2 < nr; ++ii2) {
+        for (uint32_t ii2 = g0; ii2 < nr; ++ii2) {
           if (a.dbg & 2) break;
           const Item& it = p->items[ii2];
           const uint32_t F = it.F, step = dn_step(F);
@@ -817,26 +812,23 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
         k += NG;
       }
     }
-    if (gu_only) {
-      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[8] = globaltimer_ns();
-      return;
-    }
-    if (nr > 0) {
-      signal(kMaxItems, kFfnReadyDoneCtr);
-      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[9] = globaltimer_ns();
+    if (nr > g0) {
+      const bool spec_phase = done_i == kFfnSpecDoneCtr;
+      signal(kMaxItems + (spec_phase ? 1 : 0), done_i);
+      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[spec_phase ? 8 : 9] = globaltimer_ns();
       if (ts && cw == 0 && lane == 0) ts[3] = globaltimer_ns();
       // (2) down rows of the ready items, after every CTA's gate_up
-      grid_wait(kFfnReadyDoneCtr);
+      grid_wait(done_i);
       if (s_hstage) {
-        stage_h(0, nr);
+        stage_h(g0, nr);
         asm volatile("bar.sync 1, %0;" ::"n"(NC * 32) : "memory");
       }
       if (ts && cw == 0 && lane == 0) ts[4] = globaltimer_ns();
-      if (a.tl && c == 0 && cw == 0 && lane == 0) a.tl[10] = globaltimer_ns();
+      if (a.tl && c == 0 && cw == 0 && lane == 0 && !spec_phase) a.tl[10] = globaltimer_ns();
       if (!(a.dbg & 2)) {
         // steps are numbered globally: walk them, take this group's
         uint32_t kk = k - grp;  // global step of the first down stage
-        for (uint32_t ii = 0; ii < nr; ++ii) {
+        for (uint32_t ii = g0; ii < nr; ++ii) {
           const Item& it = p->items[ii];
           const uint32_t F = it.F, step = dn_step(F);
           for (uint32_t r = dlo; r < dhi; r += step, ++kk) {
@@ -884,12 +876,12 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
     k = kk + grp;
   };
 
-  // ---- gate_up of the speculative items, overlapped with the rest of the
-  // decision (their down rows go with the final plan's ready items)
+  // ---- the speculative items (gate_up, grid barrier, down rows),
+  // overlapped with the rest of the decision
   if (after_spec && n_spec) {
     setup_phase(0, n_spec);
     __syncthreads();
-    run_phase(0, n_spec, n_spec, kFfnSpecGuCtr, true);
+    run_phase(0, n_spec, n_spec, kFfnSpecGuCtr, kFfnSpecDoneCtr);
   }
   if (after_spec) {
     // ---- the final plan: every item after the speculative ones. Taken from
@@ -922,7 +914,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
     const uint32_t n_items = p->n_items, n_ready = p->n_ready;
     setup_phase(n_spec, n_ready);
     __syncthreads();
-    run_phase(n_spec, n_ready, n_items, kFfnGuCtr, false);
+    run_phase(n_spec, n_ready, n_items, kFfnGuCtr, kFfnReadyDoneCtr);
   }
   __syncthreads();
   if (ts && threadIdx.x == 0) ts[5] = globaltimer_ns();

@@ -103,7 +103,6 @@ struct DecideArgs {
   Plan* plan;
   Plan* spec_plan;            // early plan of the certain, ready items (B == 1) or null
   uint32_t* spec_flag;        // := seq once spec_plan is published
-  uint32_t spec_late;         // diagnostics: publish after the whole decision
   uint32_t* ffn_ctr;
   const uint32_t* copies_done; // upload ids landed so far (written by the copy stream)
   MailEntry* ring;
@@ -230,9 +229,8 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
 struct EarlyPublish {
   const DecideArgs* a;
   DecideKSmem* sm;
-  __device__ void classified(DecideSmem* d) const {
-    if (!a->spec_late) publish_spec(*a, sm, d);
-  }
+  __device__ void classified(DecideSmem* d) const { publish_spec(*a, sm, d); }
+  __device__ void plan_ready(DecideSmem* d) const;
   __device__ void operator()(DecideSmem* d, uint32_t n_load, uint32_t n_cpu) const {
     if (lane_id() == 0) {
       const DecideArgs& A = *a;
@@ -339,15 +337,18 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
 }
 
 // Thread 0 builds the FFN plan and the upload commands in shared memory.
-__device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
+// The FFN items (and deferred staging->slot copies) of this step; called as
+// soon as the loads and deferred admissions are final, before the prefetch
+// phase (which only touches the prefetch target's state and the copy stream).
+__device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
   const DevCfg& cfg = sm->cfg;
-  const uint32_t B = cfg.B, E = cfg.E, layer = a.layer;
+  const uint32_t B = cfg.B, layer = a.layer;
   DecideSmem* d = &sm->d;
   const StepOut& out = d->out;
   Plan* p = &sm->plan;
   EngineState* st = &sm->st;
   LayerState* ls = &sm->ls;
-  uint32_t n_items = 0, n_cmds = 0;
+  uint32_t n_items = 0;
   auto add_item = [&](const uint16_t* w, uint32_t F, uint32_t wait, uint32_t kind, uint32_t e) {
     Item& itm = p->items[n_items++];
     itm.w = w;
@@ -357,16 +358,7 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
     itm.expert = e;
     itm.n_tok = 0;  // token lists are filled in parallel afterwards (fill_items)
   };
-  auto add_cmd = [&](uint32_t src_layer, uint32_t e, uint16_t* dst, uint32_t wait_ffn) -> uint32_t {
-    const uint32_t id = ++st->next_copy;
-    MailCmd& c = sm->cmd[n_cmds++];
-    c.src_off = ((uint64_t)src_layer * E + e) * a.expert_elems * 2;
-    c.dst = (uint64_t)dst;
-    c.bytes = a.expert_elems * 2;
-    c.id = id;
-    c.wait_ffn = wait_ffn;
-    return id;
-  };
+
   if (a.shared_w) add_item(a.shared_w, a.S, 0, 0, 0);
   // the speculative plan's routed experts next, in its (ascending) order
   for (uint64_t m = sm->spec_set; m; m &= m - 1) {
@@ -414,15 +406,6 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
     ls->slot_copy[slot] = 0;  // filled by this step's FFN epilogue
     ++n_d2d;
   }
-  for (uint32_t i = 0; i < out.n_pref; ++i) {
-    const uint32_t e = out.pref[i];
-    const int slot = out.pref_slot[i];
-    const uint32_t tlayer = out.pref_layer;
-    uint16_t* dst = slot >= 0 ? slot_ptr(a, tlayer, slot) : a.staging;
-    const uint32_t id = add_cmd(tlayer, e, dst, (uint32_t)sm->seq);
-    LayerState* tls = (tlayer == layer) ? ls : &sm->tls;
-    if (slot >= 0) tls->slot_copy[slot] = id;
-  }
   // algorithmic bytes of the FFN launch: every item's weights once, plus
   // u / x in, x out (bf16) and the fp32 layer output
   uint64_t bytes = 4ull * B * a.d * 2 + (uint64_t)B * a.d * 4;
@@ -435,15 +418,80 @@ __device__ void build_plan(const DecideArgs& a, DecideKSmem* sm) {
   p->n_d2d = n_d2d;
   p->d2d_elems = a.expert_elems;
   p->seq = (uint32_t)sm->seq;
+}
+
+// The prefetch upload commands (mailbox entry B), after the prefetch phase.
+__device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm) {
+  const uint32_t E = sm->cfg.E, layer = a.layer;
+  const StepOut& out = sm->d.out;
+  EngineState* st = &sm->st;
+  uint32_t n_cmds = 0;
+  for (uint32_t i = 0; i < out.n_pref; ++i) {
+    const uint32_t e = out.pref[i];
+    const int slot = out.pref_slot[i];
+    const uint32_t tlayer = out.pref_layer;
+    uint16_t* dst = slot >= 0 ? slot_ptr(a, tlayer, slot) : a.staging;
+    const uint32_t id = ++st->next_copy;
+    MailCmd& c = sm->cmd[n_cmds++];
+    c.src_off = ((uint64_t)tlayer * E + e) * a.expert_elems * 2;
+    c.dst = (uint64_t)dst;
+    c.bytes = a.expert_elems * 2;
+    c.id = id;
+    c.wait_ffn = (uint32_t)sm->seq;
+    LayerState* tls = (tlayer == layer) ? &sm->ls : &sm->tls;
+    if (slot >= 0) tls->slot_copy[slot] = id;
+  }
   sm->n_cmds = n_cmds;
 }
 
+// Warp 0, as soon as the step's FFN items are final (before the prefetch
+// phase): build the plan, fill token lists / weights, publish it to global
+// memory and (speculative mode) release it to the running FFN kernel.
+__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm, uint32_t first, uint32_t stride);
+
+__device__ void EarlyPublish::plan_ready(DecideSmem* d) const {
+  const DecideArgs& A = *a;
+  const int lane = lane_id();
+  const uint32_t B = sm->cfg.B;
+  if ((uint32_t)lane < B) {  // combine-weight denominators (Mixtral renormalisation)
+    const uint32_t t = lane;
+    float s = 0.f;
+    for (uint32_t i = 0; i < d->nsel[t]; ++i) s += sm->sc[t][d->sel[t][i]];
+    sm->denom[t] = s;
+  }
+  __syncwarp();
+  if (lane == 0) build_items(A, sm);
+  __syncwarp();
+  fill_items(A, sm, lane, 32);
+  __syncwarp();
+  Plan* gp = A.plan;
+  const uint32_t n_items = sm->plan.n_items;
+  const uint64_t* src = reinterpret_cast<const uint64_t*>(&sm->plan);
+  uint64_t* dst = reinterpret_cast<uint64_t*>(gp);
+  const size_t words = (offsetof(Plan, items) + n_items * sizeof(Item)) / 8;
+  for (uint32_t i = lane; i < words; i += 32) dst[i] = src[i];
+  const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + sm->plan.n_d2d * sizeof(D2D) / 8;
+  for (uint32_t i = d0 + lane; i < d1; i += 32) dst[i] = src[i];
+  if (A.spec_plan) {
+    // the FFN kernel (already running its speculative items) takes the final
+    // plan from this flag instead of waiting for this kernel to complete:
+    // every writer fences, then one release
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(A.spec_flag + 1), "r"((uint32_t)sm->seq) : "memory");
+      if (A.tl) A.tl[12] = globaltimer_ns();
+    }
+  }
+  __syncwarp();
+}
+
 // Token lists and combine weights of every plan item, one thread per item.
-__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm) {
+__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm, uint32_t first, uint32_t stride) {
   const uint32_t B = sm->cfg.B;
   const DecideSmem* d = &sm->d;
   Plan* p = &sm->plan;
-  for (uint32_t ii = threadIdx.x; ii < p->n_items; ii += blockDim.x) {
+  for (uint32_t ii = first; ii < p->n_items; ii += stride) {
     Item& itm = p->items[ii];
     const uint32_t kind = itm.kind, e = itm.expert;
     uint32_t n = 0;
@@ -624,27 +672,16 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     toks = a.toks + (sm->seq - 1) * B;
   }
   decide_step(cx, &sm->d, &sm->n, &sm->s, rec, toks, EarlyPublish{&a, sm});
-  if (a.spec_late) publish_spec(a, sm, &sm->d);  // diagnostics (MOEB_SPEC_LATE)
   __syncthreads();
   MOEB_T(t_decided);
 
-  // combine-weight denominators (Mixtral renormalisation), FFN counters
-  if (threadIdx.x < B) {
-    const uint32_t t = threadIdx.x;
-    float s = 0.f;
-    for (uint32_t i = 0; i < sm->d.nsel[t]; ++i) s += sm->sc[t][sm->d.sel[t][i]];
-    sm->denom[t] = s;
-  }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    build_plan(a, sm);
+    build_prefetch_cmds(a, sm);
     // entry B's ring slot must have been consumed by the copy thread
     wait_ring_slot(a, 2 * sm->seq, &sm->st.ack_cache);
     sm->st.seq = sm->seq;
     if (layer == L - 1) sm->st.it = it + 1;
   }
-  __syncthreads();
-  fill_items(a, sm);
   if (threadIdx.x == 0) {
     MOEB_T(t_plan);
     t_plan_g = t_plan;
@@ -658,25 +695,9 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     (void)t_entry; (void)t_gate; (void)t_elect; (void)t_staged; (void)t_decided; (void)t_plan;
   }
   __syncthreads();
-  // publish: plan -> global, commands -> mapped host ring, state write-back
+  // publish: prefetch commands -> mapped host ring, state write-back (the
+  // plan went out in EarlyPublish::plan_ready)
   {
-    Plan* gp = a.plan;
-    const uint32_t n_items = sm->plan.n_items;
-    const uint64_t* src = reinterpret_cast<const uint64_t*>(&sm->plan);
-    uint64_t* dst = reinterpret_cast<uint64_t*>(gp);
-    const size_t words = (offsetof(Plan, items) + n_items * sizeof(Item)) / 8;
-    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
-    const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + sm->plan.n_d2d * sizeof(D2D) / 8;
-    for (uint32_t i = d0 + threadIdx.x; i < d1; i += blockDim.x) dst[i] = src[i];
-    if (a.spec_plan) {
-      // the FFN kernel (already running its speculative items) takes the
-      // final plan from this flag instead of waiting for this kernel to
-      // complete: every writer fences, then one release
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0)
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 1), "r"((uint32_t)sm->seq) : "memory");
-    }
     MailEntry* me = &a.ring[(2 * sm->seq) % kRing];
     const uint32_t nc = sm->n_cmds;
     const uint64_t* cs = reinterpret_cast<const uint64_t*>(sm->cmd);
@@ -1160,7 +1181,6 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     a.plan = S->plan.p;
     a.spec_plan = S->spec ? S->spec_plan.p : nullptr;
     a.spec_flag = S->spec_flag.p;
-    a.spec_late = getenv("MOEB_SPEC_LATE") != nullptr;
     a.ffn_ctr = S->ffn_ctr.p;
     a.copies_done = S->copies_done.p;
     a.ring = S->ring_dev;
