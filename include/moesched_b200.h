@@ -69,6 +69,11 @@ typedef struct moeb_model {
 #define MOEB_MODEL_LOG_STEPS 1u     /* record per-step decision records */
 #define MOEB_MODEL_TIME_KERNELS 2u  /* CUDA-event timing of every gate/decide/FFN launch */
 #define MOEB_MODEL_TRACE_TIMELINE 4u /* device-clock timeline of every layer-step (moeb_get_timeline) */
+/* Host pool layout: for batch > 1 each expert is [gate ffn x d][up ffn x d]
+ * [down d x ffn] (the HF layouts); batch-1 stacks with d_model <= 2048 (the
+ * split-K FFN) store it row-interleaved, [ffn][3][d]: gate row r, up row r,
+ * down column r. A caller-supplied pool declares that layout with this flag. */
+#define MOEB_MODEL_DOWN_T 8u
 
 typedef struct moeb_engine moeb_engine; /* decision engine only (simulate path) */
 typedef struct moeb_stack moeb_stack;   /* full MoE decode stack */
@@ -252,6 +257,8 @@ int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction,
  * (8-11: CTA 0). Diagnostics only. */
 int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n);
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes);
+/* MOEB_MODEL_DOWN_T when the stack's pool is row-interleaved (batch 1). */
+int moeb_host_pool_flags(moeb_stack* s, uint32_t* flags);
 
 #ifdef __cplusplus
 }

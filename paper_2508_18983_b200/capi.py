@@ -297,6 +297,11 @@ class Stack:
             wp = None
         elif isinstance(weights_host, tuple):
             wp = C.c_void_p(weights_host[0])
+            owner = weights_host[1] if len(weights_host) > 1 else None
+            if isinstance(owner, Stack):  # a pool shared from another stack: same layout
+                fl = C.c_uint32(0)
+                check(lib().moeb_host_pool_flags(owner.h, C.byref(fl)))
+                m.flags |= fl.value
         else:
             wp = C.c_void_p(weights_host.ctypes.data)
         check(lib().moeb_create(C.byref(cfg), C.byref(m), wp, C.c_int(device), C.byref(h)))

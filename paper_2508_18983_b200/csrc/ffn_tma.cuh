@@ -34,7 +34,8 @@ constexpr int kFfnGuCtr = kMaxItems + 2;        // dynamic gate_up chunks, final
 constexpr int kFfnReadyDoneCtr = kMaxItems + 3;  // CTAs done with the final plan's ready gate_up
 constexpr int kFfnSpecGuCtr = kMaxItems + 4;     // dynamic gate_up chunks, speculative plan
 constexpr int kFfnSpecDoneCtr = kMaxItems + 5;   // CTAs done with the speculative gate_up
-constexpr int kFfnCtrWords = kMaxItems + 6;
+constexpr int kFfnRedCtr = kMaxItems + 6;        // end-of-kernel reduction barrier (split-K kernel)
+constexpr int kFfnCtrWords = kMaxItems + 7;
 constexpr int kTlWords = 16;  // timeline record words per layer-step
 constexpr size_t kPlanSmem = (sizeof(Plan) + 15) & ~(size_t)15;  // plan copy in smem, 16 B aligned
 
@@ -108,6 +109,7 @@ struct FfnTArgs {
   const Plan* spec_plan;   // speculative plan (null: none); published when *spec_flag == seq
   const uint32_t* spec_flag;
   uint32_t seq;
+  uint32_t unit_rows;      // split-K kernel: intermediate rows per grid-counter grab (0: default)
 };
 
 // Row range of CTA c out of G over n rows.

@@ -31,6 +31,7 @@
 #include "host_common.h"
 #include "layer.cuh"
 #include "ffn_tma.cuh"
+#include "ffn_splitk.cuh"
 #include "weights.cuh"
 
 namespace moeb {
@@ -780,6 +781,8 @@ struct moeb_stack {
   DevBuf<Plan> plan, spec_plan;
   DevBuf<uint32_t> spec_flag;
   bool spec = false;
+  bool splitk = false;  // batch-1 split-K FFN; experts stored row-interleaved [F][3][d]
+  uint32_t unit_rows = 0, ffn_dbg = 0;
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
   DevBuf<StepRec> recs;
   DevBuf<uint64_t> timeline;  // [rec_cap][kTlWords] (MOEB_MODEL_TRACE_TIMELINE)
@@ -931,6 +934,24 @@ static void synth(uint16_t* dst, uint64_t n, uint64_t seed, uint64_t tensor, uin
   MOEB_CUDA(cudaGetLastError());
 }
 
+static void synth_t(uint16_t* dst, uint32_t rows, uint32_t cols, uint64_t seed, uint64_t tensor, float scale,
+                    cudaStream_t s) {
+  const uint64_t n = (uint64_t)rows * cols;
+  if (!n) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  synth_t_kernel<<<grid, 256, 0, s>>>(dst, rows, cols, seed, tensor, scale);
+  MOEB_CUDA(cudaGetLastError());
+}
+
+static void synth_rows(uint16_t* dst, uint32_t F, uint32_t d, uint64_t seed, uint64_t t0, uint64_t t1, uint64_t t2,
+                       float s_in, float s_down, cudaStream_t s) {
+  const uint64_t n = 3ull * F * d;
+  if (!n) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  synth_rows_kernel<<<grid, 256, 0, s>>>(dst, F, d, seed, t0, t1, t2, s_in, s_down);
+  MOEB_CUDA(cudaGetLastError());
+}
+
 static float fan_scale(uint32_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
 
 // (Re)initialise the decision state and upload the initial residents. The
@@ -998,6 +1019,13 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   const cudaStream_t s = S->stream;
   const uint32_t L = S->L, E = S->E, B = S->B, d = S->d, F = S->F, Sh = S->S;
   const uint64_t seed = m.weight_seed;
+  // batch 1: split-K FFN over row-interleaved experts ([F][3][d])
+  S->splitk = B == 1 && d <= 2048 && getenv("MOEB_NO_SPLITK") == nullptr;
+  if (const char* ur = getenv("MOEB_SK_UNIT")) S->unit_rows = (uint32_t)atoi(ur);
+  if (const char* fd = getenv("MOEB_FFN_DBG")) S->ffn_dbg = (uint32_t)atoi(fd);  // microbenchmark knob
+  if (weights_host && S->splitk != ((m.flags & MOEB_MODEL_DOWN_T) != 0))
+    throw Error(1, S->splitk ? "model: a batch-1 stack needs a row-interleaved host pool (MOEB_MODEL_DOWN_T)"
+                             : "model: this stack needs a host pool in the [gate][up][down] layout (no MOEB_MODEL_DOWN_T)");
   // resident (HBM) weights: router, shared expert, shared gate
   S->gate_w.alloc((size_t)L * E * d);
   for (uint32_t l = 0; l < L; ++l) synth(S->gate_w.p + (size_t)l * E * d, (uint64_t)E * d, seed, tid_router(l), 0, fan_scale(d), s);
@@ -1005,9 +1033,13 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
     S->shared_w.alloc((size_t)L * 3 * Sh * d);
     for (uint32_t l = 0; l < L; ++l) {
       uint16_t* base = S->shared_w.p + (size_t)l * 3 * Sh * d;
-      synth(base, (uint64_t)Sh * d, seed, tid_shared(l, 0), 0, fan_scale(d), s);
-      synth(base + (size_t)Sh * d, (uint64_t)Sh * d, seed, tid_shared(l, 1), 0, fan_scale(d), s);
-      synth(base + 2 * (size_t)Sh * d, (uint64_t)Sh * d, seed, tid_shared(l, 2), 0, fan_scale(Sh), s);
+      if (S->splitk) {
+        synth_rows(base, Sh, d, seed, tid_shared(l, 0), tid_shared(l, 1), tid_shared(l, 2), fan_scale(d), fan_scale(Sh), s);
+      } else {
+        synth(base, (uint64_t)Sh * d, seed, tid_shared(l, 0), 0, fan_scale(d), s);
+        synth(base + (size_t)Sh * d, (uint64_t)Sh * d, seed, tid_shared(l, 1), 0, fan_scale(d), s);
+        synth(base + 2 * (size_t)Sh * d, (uint64_t)Sh * d, seed, tid_shared(l, 2), 0, fan_scale(Sh), s);
+      }
     }
   }
   if (m.shared_gate) {
@@ -1033,9 +1065,14 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
     for (uint64_t i = 0; i < (uint64_t)L * E; ++i) {
       const uint32_t l = (uint32_t)(i / E), e = (uint32_t)(i % E);
       uint16_t* buf = tmp.p + (i & 1) * S->expert_elems;
-      synth(buf, (uint64_t)F * d, seed, tid_expert(l, e, 0), 0, fan_scale(d), s);
-      synth(buf + (size_t)F * d, (uint64_t)F * d, seed, tid_expert(l, e, 1), 0, fan_scale(d), s);
-      synth(buf + 2 * (size_t)F * d, (uint64_t)F * d, seed, tid_expert(l, e, 2), 0, fan_scale(F), s);
+      if (S->splitk) {
+        synth_rows(buf, F, d, seed, tid_expert(l, e, 0), tid_expert(l, e, 1), tid_expert(l, e, 2), fan_scale(d),
+                   fan_scale(F), s);
+      } else {
+        synth(buf, (uint64_t)F * d, seed, tid_expert(l, e, 0), 0, fan_scale(d), s);
+        synth(buf + (size_t)F * d, (uint64_t)F * d, seed, tid_expert(l, e, 1), 0, fan_scale(d), s);
+        synth(buf + 2 * (size_t)F * d, (uint64_t)F * d, seed, tid_expert(l, e, 2), 0, fan_scale(F), s);
+      }
       MOEB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(S->pool) + i * eb, buf, eb, cudaMemcpyDeviceToHost, s));
     }
     MOEB_CUDA(cudaStreamSynchronize(s));
@@ -1088,7 +1125,8 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // kernel resources: FFN launch shape (ring stages, h staging, accumulators)
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  S->ffn = ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
+  S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k)
+                     : ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
   if (S->ffn.stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
   S->ticket.alloc(1);
   S->ticket.zero(s);
@@ -1221,6 +1259,8 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     f.spec_plan = a.spec_plan;
     f.spec_flag = S->spec_flag.p;
     f.seq = (uint32_t)a.seq;
+    f.unit_rows = S->unit_rows;
+    f.dbg = S->ffn_dbg;
     f.x_smem = S->ffn.x_smem;
     launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s, &f);
     S->n_launch_layers += 1;
@@ -1421,6 +1461,11 @@ int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n) {
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes) {
   *pool = s->pool;
   *expert_bytes = s->expert_elems * 2;
+  return 0;
+}
+
+int moeb_host_pool_flags(moeb_stack* s, uint32_t* flags) {
+  *flags = s->splitk ? MOEB_MODEL_DOWN_T : 0u;
   return 0;
 }
 

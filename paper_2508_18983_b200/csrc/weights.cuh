@@ -49,4 +49,30 @@ __global__ void synth_kernel(uint16_t* __restrict__ dst, uint64_t n, uint64_t se
     dst[i] = synth_weight(seed, tensor, offset + i, scale);
 }
 
+// The same tensor stored transposed: logical [rows][cols] -> dst [cols][rows]
+// (element (r, c), counter index r*cols + c, lands at c*rows + r).
+__global__ void synth_t_kernel(uint16_t* __restrict__ dst, uint32_t rows, uint32_t cols, uint64_t seed,
+                               uint64_t tensor, float scale) {
+  const uint64_t n = (uint64_t)rows * cols;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = p / rows, r = p % rows;
+    dst[p] = synth_weight(seed, tensor, r * cols + c, scale);
+  }
+}
+
+// One expert (or shared expert) in the row-interleaved layout of the batch-1
+// split-K FFN: for every intermediate row r, [gate row r | up row r | down
+// column r] (3 x d contiguous bf16), i.e. dst[F][3][d]. Element values are
+// the logical tensors' (gate/up [F][d], down [d][F]) counter-based weights.
+__global__ void synth_rows_kernel(uint16_t* __restrict__ dst, uint32_t F, uint32_t d, uint64_t seed, uint64_t t_gate,
+                                  uint64_t t_up, uint64_t t_down, float s_in, float s_down) {
+  const uint64_t n = 3ull * F * d;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = p / (3ull * d), m = (p / d) % 3, c = p % d;
+    dst[p] = m == 0 ? synth_weight(seed, t_gate, r * d + c, s_in)
+           : m == 1 ? synth_weight(seed, t_up, r * d + c, s_in)
+                    : synth_weight(seed, t_down, c * F + r, s_down);
+  }
+}
+
 }  // namespace moeb

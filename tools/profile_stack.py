@@ -66,7 +66,7 @@ def main():
         print("decide end->ffn start", us(tl[:, 0] - tl[:, 5]))
         rel = lambda i: us((tl[:, i] - tl[:, 3])[tl[:, i] != 0]) if (tl[:, i] != 0).any() else None
         print("rel. decide entry: spec gu done", rel(8), "final gu done", rel(9), "down starts", rel(10),
-              "cta0 done", rel(11), "final plan published", rel(12), "ffn main start", rel(0), "decide end", rel(5))
+              "cta0 done", rel(11), "last cta done", rel(13), "cta0 past end barrier", rel(14), "ffn end", rel(2), "final plan published", rel(12), "ffn main start", rel(0), "decide end", rel(5))
         print("ffn CTA0 entry rel. decide entry", us(tl[:, 7] - tl[:, 3]), "spec plan seen rel. decide entry",
               us((tl[:, 6] - tl[:, 3])[tl[:, 6] != 0]) if (tl[:, 6] != 0).any() else None)
         print("ffn start->end (no uploads)", us((tl[:, 2] - tl[:, 0])[~miss]))
