@@ -57,13 +57,43 @@ __device__ __forceinline__ float sk_h(const uint16_t* gs, const uint16_t* us_row
   return __fdiv_rn(gu.x, 1.0f + expf(-gu.x)) * gu.y;
 }
 
-__global__ void __launch_bounds__(kSkThreads, 1) ffn_splitk_kernel(FfnTArgs a) {
-  constexpr int NC = kSkConsumers;
+// the same with the activation's B fragments read from shared memory
+__device__ __forceinline__ float sk_h_smem(const uint16_t* gs, const uint16_t* us_row, const uint32_t* su,
+                                           uint32_t d) {
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc2[4] = {0.f, 0.f, 0.f, 0.f};
+  const int lane = lane_id();
+  const uint32_t base = diag_addr(smem_u32(gs), smem_u32(us_row));
+  const uint32_t nb = d / 128;
+#pragma unroll
+  for (int b = 0; b < 16; b += 2) {  // d <= 2048
+    if ((uint32_t)b < nb) {
+      uint32_t a[4];
+      ldsm_x4(base + b * 256, a);
+      mma16816(acc, a, su[b * 64 + lane], su[b * 64 + 32 + lane]);
+    }
+    if ((uint32_t)b + 1 < nb) {
+      uint32_t a[4];
+      ldsm_x4(base + (b + 1) * 256, a);
+      mma16816(acc2, a, su[(b + 1) * 64 + lane], su[(b + 1) * 64 + 32 + lane]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] += acc2[q];
+  const float2 gu = diag_reduce(acc);
+  return __fdiv_rn(gu.x, 1.0f + expf(-gu.x)) * gu.y;
+}
+
+// NC consumer warps; XREG: the activation's B fragments live in registers
+// (else in shared memory, which leaves the registers for more warps)
+template <int NC, bool XREG>
+__global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kSkStages], empty_bar[kSkStages];
   __shared__ uint32_t s_hdr[kSkStages][2];  // {item << 16 | 1, row} or {0, 0} = end
   __shared__ uint32_t s_pre[kMaxItems + 1];  // row prefix of a phase's items
   __shared__ uint32_t s_next;                // next ring step a consumer warp claims
+  __shared__ uint32_t s_u[1024];             // the activation (bf16 pairs), d <= 2048
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
   const uint32_t G = gridDim.x, c = blockIdx.x;
@@ -172,10 +202,17 @@ __global__ void __launch_bounds__(kSkThreads, 1) ffn_splitk_kernel(FfnTArgs a) {
       }
       __syncwarp();
     };
+    auto load_u = [&]() {  // all lanes of warp 0; u is valid once a plan is
+      if (!XREG)
+        for (uint32_t i = lane; i < d / 2; i += 32) s_u[i] = __ldcg(reinterpret_cast<const uint32_t*>(a.u) + i);
+      __syncwarp();
+    };
     uint32_t n_spec = 0;
+    if (!spec) load_u();
     if (spec) {
       // the certain items while the decision runs
       wait_flag(a.spec_flag, 6);
+      load_u();
       n_spec = ld_acquire_u32(&a.spec_plan->n_spec);
       fetch(a.spec_plan, 0, (uint32_t)((offsetof(Plan, items) + n_spec * sizeof(Item)) / 8));
       stream(0, n_spec, kFfnSpecGuCtr, false);
@@ -220,7 +257,7 @@ __global__ void __launch_bounds__(kSkThreads, 1) ffn_splitk_kernel(FfnTArgs a) {
     for (int j = 0; j < kSkMaxYChunks; ++j)
 #pragma unroll
       for (int q = 0; q < 8; ++q) y[j][q] = 0.f;
-    uint32_t xb[kXrBlocks][2];
+    uint32_t xb[XREG ? kXrBlocks : 1][2];
     bool have_x = false;
     for (;;) {
       // the next ring step goes to whichever warp is free (no head-of-line
@@ -237,10 +274,10 @@ __global__ void __launch_bounds__(kSkThreads, 1) ffn_splitk_kernel(FfnTArgs a) {
         if (lane == 0) mbar_arrive(&empty_bar[st]);
         break;
       }
-      if (!have_x) {  // u: the gate phase wrote it before either plan was released
+      if (XREG && !have_x) {  // u: the gate phase wrote it before either plan was released
         const uint32_t* u32w = reinterpret_cast<const uint32_t*>(a.u);
 #pragma unroll
-        for (int b = 0; b < kXrBlocks; ++b) {
+        for (int b = 0; b < (XREG ? kXrBlocks : 1); ++b) {
           const bool in = (uint32_t)b < d / 128;
           xb[b][0] = in ? __ldcg(u32w + b * 64 + lane) : 0u;
           xb[b][1] = in ? __ldcg(u32w + b * 64 + 32 + lane) : 0u;
@@ -250,7 +287,10 @@ __global__ void __launch_bounds__(kSkThreads, 1) ffn_splitk_kernel(FfnTArgs a) {
       const Item& it = p->items[h0 >> 16];
       const uint16_t* base = reinterpret_cast<const uint16_t*>(ring + st * SB);
       if (!(a.dbg & 1)) {
-        const float s = it.wt[0] * sk_h(base, base + d, xb, d);
+        float hv;
+        if constexpr (XREG) hv = sk_h(base, base + d, xb, d);
+        else hv = sk_h_smem(base, base + d, s_u, d);
+        const float s = it.wt[0] * hv;
         const uint4* wd = reinterpret_cast<const uint4*>(base + 2 * d);
 #pragma unroll
         for (int j = 0; j < kSkMaxYChunks; ++j) {
@@ -364,10 +404,15 @@ __global__ void __launch_bounds__(kSkThreads, 1) ffn_splitk_kernel(FfnTArgs a) {
 
 // Launch shape: the ring (kSkStages stages of 3 rows), the plan copy, and
 // the reduction scratch (aliases the ring).
-inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k) {
+inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int consumers) {
   FfnLaunch L{};
-  L.fn = ffn_splitk_kernel;
-  L.threads = kSkThreads;
+  if (consumers == 12) {
+    L.fn = ffn_splitk_kernel<12, false>;
+    L.threads = 32 * 13;
+  } else {
+    L.fn = ffn_splitk_kernel<8, true>;
+    L.threads = 32 * 9;
+  }
   L.stage_bytes = 3 * 2 * d;
   L.stages = kSkStages;
   const uint32_t max_items = 1 + std::min(E, top_k);
@@ -375,7 +420,7 @@ inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k) {
   L.x_smem = 0;
   L.acc_rows = 0;
   L.hbuf_bytes = 0;
-  const size_t ring = std::max<size_t>((size_t)L.stages * L.stage_bytes, (size_t)kSkConsumers * d * 4);
+  const size_t ring = std::max<size_t>((size_t)L.stages * L.stage_bytes, (size_t)(L.threads / 32 - 1) * d * 4);
   L.stage_bytes = (uint32_t)(ring / L.stages);  // the scratch must fit in the ring
   L.smem = ring + L.plan_smem;
   return L;
