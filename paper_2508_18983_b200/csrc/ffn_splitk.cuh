@@ -26,7 +26,7 @@ namespace moeb {
 
 constexpr int kSkConsumers = 8;
 constexpr int kSkThreads = 32 * (1 + kSkConsumers);
-constexpr int kSkStages = 18;        // > kSkConsumers (consumers claim steps dynamically); 216 KB at d = 2048
+constexpr int kSkStages = 16;        // a multiple of the consumer warps (2 stages each); 192 KB at d = 2048
 constexpr int kSkMaxYChunks = 8;     // d <= 2048: 8 columns x 8 chunks per lane
 constexpr uint32_t kSkUnitRows = 16;  // rows per grab in the first tier (same-address atomics serialise: keep grabs few)
 
@@ -92,7 +92,6 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   __shared__ __align__(8) uint64_t full_bar[kSkStages], empty_bar[kSkStages];
   __shared__ uint32_t s_hdr[kSkStages][2];  // {item << 16 | 1, row} or {0, 0} = end
   __shared__ uint32_t s_pre[kMaxItems + 1];  // row prefix of a phase's items
-  __shared__ uint32_t s_next;                // next ring step a consumer warp claims
   __shared__ uint32_t s_u[1024];             // the activation (bf16 pairs), d <= 2048
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
@@ -104,7 +103,6 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   uint32_t dlo, dhi;
   share(d, c, G, dlo, dhi);
   if (threadIdx.x == 0) {
-    s_next = 0;
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -167,12 +165,14 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         const uint32_t n2 = small_units ? 0 : (rows * 95 / 100 > e1 ? rows * 95 / 100 - e1 : 0) / 8, e2 = e1 + n2 * 8;
         const uint32_t n_units = n1 + n2 + (rows - e2 + 1) / 2;
         uint32_t* ctr = a.ctr + ci;
-        uint32_t u0 = atomicAdd(ctr, 1u), u1 = atomicAdd(ctr, 1u);
+        // deterministic mode: unit u belongs to CTA u % G (no counter)
+        const bool det = a.deterministic != 0;
+        uint32_t u0 = det ? c : atomicAdd(ctr, 1u), u1 = det ? c + G : atomicAdd(ctr, 1u);
         uint32_t ii = i0;
         while (u0 < n_units) {
           const uint32_t cur = u0;
           u0 = u1;
-          u1 = atomicAdd(ctr, 1u);
+          u1 = det ? u1 + G : atomicAdd(ctr, 1u);
           uint32_t r0, r1;
           if (cur < n1) { r0 = cur * ub; r1 = r0 + ub; }
           else if (cur < n1 + n2) { r0 = e1 + (cur - n1) * 8; r1 = r0 + 8; }
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
     }
   } else {
     // ------------------------------------------------------------ consumers
-    // ring steps are claimed through a shared counter (s_next)
+    // ring step k belongs to warp k % NC
     const uint32_t cw = warp - 1, ych = d / 256;
     float y[kSkMaxYChunks][8];
 #pragma unroll
@@ -259,13 +259,14 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       for (int q = 0; q < 8; ++q) y[j][q] = 0.f;
     uint32_t xb[XREG ? kXrBlocks : 1][2];
     bool have_x = false;
+    uint32_t k_det = cw;
     for (;;) {
-      // the next ring step goes to whichever warp is free (no head-of-line
-      // blocking behind a busy warp); at most NC steps are claimed at once
-      // and NC < S, so a claimed step's slot parity is never ambiguous
-      uint32_t k = 0;
-      if (lane == 0) k = atomicAdd(&s_next, 1u);
-      k = __shfl_sync(0xffffffffu, k, 0);
+      // step k belongs to warp k % NC and the stage count is a multiple of
+      // NC: a slot always has the same warp, which consumes its phases in
+      // order, so a parity wait can never match a stale phase (a dynamic
+      // claim could, if an older copy into that slot completed late)
+      const uint32_t k = k_det;
+      k_det += NC;
       const uint32_t st = k % S;
       mbar_wait(&full_bar[st], (k / S) & 1);
       const uint32_t h0 = s_hdr[st][0];
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
 
 // Launch shape: the ring (kSkStages stages of 3 rows), the plan copy, and
 // the reduction scratch (aliases the ring).
-inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int consumers) {
+inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int consumers, bool deterministic) {
   FfnLaunch L{};
   if (consumers == 12) {
     L.fn = ffn_splitk_kernel<12, false>;
@@ -414,7 +415,10 @@ inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int c
     L.threads = 32 * 9;
   }
   L.stage_bytes = 3 * 2 * d;
-  L.stages = kSkStages;
+  // step k -> warp k % NC: the stage count is a multiple of NC
+  (void)deterministic;
+  const uint32_t nc = L.threads / 32 - 1;
+  L.stages = std::max<uint32_t>(nc, kSkStages / nc * nc);
   const uint32_t max_items = 1 + std::min(E, top_k);
   L.plan_smem = (uint32_t)((offsetof(Plan, items) + (size_t)max_items * sizeof(Item) + 15) & ~(size_t)15);
   L.x_smem = 0;

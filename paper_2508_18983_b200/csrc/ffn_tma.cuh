@@ -110,6 +110,7 @@ struct FfnTArgs {
   const uint32_t* spec_flag;
   uint32_t seq;
   uint32_t unit_rows;      // split-K kernel: intermediate rows per grid-counter grab (0: default)
+  uint32_t deterministic;  // split-K kernel: static row -> (CTA, warp) assignment (bitwise-reproducible sums)
 };
 
 // Row range of CTA c out of G over n rows.

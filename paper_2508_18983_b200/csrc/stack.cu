@@ -1125,7 +1125,8 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // kernel resources: FFN launch shape (ring stages, h staging, accumulators)
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k, getenv("MOEB_SK_NC") ? atoi(getenv("MOEB_SK_NC")) : 8)
+  S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k, getenv("MOEB_SK_NC") ? atoi(getenv("MOEB_SK_NC")) : 8,
+                                          (m.flags & MOEB_MODEL_DETERMINISTIC) != 0)
                      : ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
   if (S->ffn.stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
   S->ticket.alloc(1);
@@ -1260,6 +1261,7 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     f.spec_flag = S->spec_flag.p;
     f.seq = (uint32_t)a.seq;
     f.unit_rows = S->unit_rows;
+    f.deterministic = (S->model.flags & MOEB_MODEL_DETERMINISTIC) ? 1u : 0u;
     f.dbg = S->ffn_dbg;
     f.x_smem = S->ffn.x_smem;
     launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s, &f);
