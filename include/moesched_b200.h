@@ -74,11 +74,9 @@ typedef struct moeb_model {
  * split-K FFN) store it row-interleaved, [ffn][3][d]: gate row r, up row r,
  * down column r. A caller-supplied pool declares that layout with this flag. */
 #define MOEB_MODEL_DOWN_T 8u
-/* Bitwise-reproducible layer outputs at batch 1: the split-K FFN hands its
- * rows out statically instead of dynamically (the fp32 partial sums otherwise
- * depend on which SM and warp took which row; decisions are unaffected in
- * trace-driven mode). Slower: the static split does not absorb per-SM
- * bandwidth differences. */
+/* Bitwise-reproducible layer outputs. Always the case now (the batch-1
+ * split-K FFN deals its rows round-robin, a fixed assignment); the flag is
+ * accepted for API stability. */
 #define MOEB_MODEL_DETERMINISTIC 16u
 
 typedef struct moeb_engine moeb_engine; /* decision engine only (simulate path) */

@@ -20,14 +20,18 @@
 // and the uploaded experts follow on the same ring without any barrier.
 #pragma once
 
+#include <cstdlib>
+
 #include "ffn_tma.cuh"
 
 namespace moeb {
 
 constexpr int kSkConsumers = 8;
 constexpr int kSkThreads = 32 * (1 + kSkConsumers);
+constexpr int kSkMaxStages = 24;
 constexpr int kSkStages = 16;        // a multiple of the consumer warps (2 stages each); 192 KB at d = 2048
 constexpr int kSkMaxYChunks = 8;     // d <= 2048: 8 columns x 8 chunks per lane
+constexpr uint32_t kSkStaticUnitRows = 4;  // rows per unit when dealt round-robin (default)
 constexpr uint32_t kSkUnitRows = 16;  // rows per grab in the first tier (same-address atomics serialise: keep grabs few)
 
 // silu(g.u) * (u_r.u) for one gate/up row pair in shared memory; every lane
@@ -89,8 +93,8 @@ __device__ __forceinline__ float sk_h_smem(const uint16_t* gs, const uint16_t* u
 template <int NC, bool XREG>
 __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kSkStages], empty_bar[kSkStages];
-  __shared__ uint32_t s_hdr[kSkStages][2];  // {item << 16 | 1, row} or {0, 0} = end
+  __shared__ __align__(8) uint64_t full_bar[kSkMaxStages], empty_bar[kSkMaxStages];
+  __shared__ uint32_t s_hdr[kSkMaxStages][2];  // {item << 16 | 1, row} or {0, 0} = end
   __shared__ uint32_t s_pre[kMaxItems + 1];  // row prefix of a phase's items
   __shared__ uint32_t s_u[1024];             // the activation (bf16 pairs), d <= 2048
   asm volatile("griddepcontrol.launch_dependents;");
@@ -160,13 +164,15 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         // runs out of work within about a microsecond of the others
         // (an uploaded expert alone — ~10 rows per SM — goes out in 2-row
         // units: its completion is on the critical path after the upload)
-        const uint32_t ub = a.unit_rows ? a.unit_rows : kSkUnitRows;
-        const uint32_t n1 = small_units ? 0 : (rows * 70 / 100) / ub, e1 = n1 * ub;
-        const uint32_t n2 = small_units ? 0 : (rows * 95 / 100 > e1 ? rows * 95 / 100 - e1 : 0) / 8, e2 = e1 + n2 * 8;
+        const bool det = a.deterministic != 0;
+        const uint32_t ub = a.unit_rows ? a.unit_rows : (det ? kSkStaticUnitRows : kSkUnitRows);
+        const uint32_t n1 = small_units ? 0 : det ? rows / ub : (rows * 70 / 100) / ub, e1 = n1 * ub;
+        const uint32_t n2 = small_units || det ? 0 : (rows * 95 / 100 > e1 ? rows * 95 / 100 - e1 : 0) / 8, e2 = e1 + n2 * 8;
         const uint32_t n_units = n1 + n2 + (rows - e2 + 1) / 2;
         uint32_t* ctr = a.ctr + ci;
-        // deterministic mode: unit u belongs to CTA u % G (no counter)
-        const bool det = a.deterministic != 0;
+        // static mode (default): unit u belongs to CTA u % G — units of the
+        // same size, dealt round-robin, balance the SMs without counter atomics
+        // and give bitwise-reproducible partial sums
         uint32_t u0 = det ? c : atomicAdd(ctr, 1u), u1 = det ? c + G : atomicAdd(ctr, 1u);
         uint32_t ii = i0;
         while (u0 < n_units) {
@@ -410,6 +416,12 @@ inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int c
   if (consumers == 12) {
     L.fn = ffn_splitk_kernel<12, false>;
     L.threads = 32 * 13;
+  } else if (consumers == 4) {
+    L.fn = ffn_splitk_kernel<4, true>;
+    L.threads = 32 * 5;
+  } else if (consumers == 6) {
+    L.fn = ffn_splitk_kernel<6, true>;
+    L.threads = 32 * 7;
   } else {
     L.fn = ffn_splitk_kernel<8, true>;
     L.threads = 32 * 9;
@@ -418,7 +430,7 @@ inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int c
   // step k -> warp k % NC: the stage count is a multiple of NC
   (void)deterministic;
   const uint32_t nc = L.threads / 32 - 1;
-  L.stages = std::max<uint32_t>(nc, kSkStages / nc * nc);
+  L.stages = std::max<uint32_t>(nc, (getenv("MOEB_SK_STAGES") ? atoi(getenv("MOEB_SK_STAGES")) : kSkStages) / nc * nc);
   const uint32_t max_items = 1 + std::min(E, top_k);
   L.plan_smem = (uint32_t)((offsetof(Plan, items) + (size_t)max_items * sizeof(Item) + 15) & ~(size_t)15);
   L.x_smem = 0;
