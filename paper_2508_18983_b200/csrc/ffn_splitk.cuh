@@ -353,6 +353,13 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 2u); break; }
     }
     if (a.tl && c == 0) a.tl[14] = globaltimer_ns();
+    // every CTA has finished reading expert slots (it passed its consumer
+    // loop before arriving): without deferred copies, ffn_done can be
+    // released now instead of after a second exit barrier
+    if (c == 0 && p->n_d2d == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ffn_done), "r"(p->seq) : "memory");
+    }
   }
   __syncthreads();
   // outputs [dlo, dhi): sum of the CTA partials in CTA order, residual.
@@ -399,13 +406,17 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (n_d2d) __threadfence();
-    const uint32_t prev = atomicAdd(&a.ctr[kFfnExitCtr], 1u);
-    if (prev == G - 1) {
+    if (n_d2d) {
+      // the staging -> slot copies must be visible before ffn_done releases
+      // the copy stream's prefetches into those slots: last CTA out signals
       __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ffn_done), "r"(p->seq) : "memory");
-      if (a.tl) a.tl[2] = globaltimer_ns();
+      const uint32_t prev = atomicAdd(&a.ctr[kFfnExitCtr], 1u);
+      if (prev == G - 1) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ffn_done), "r"(p->seq) : "memory");
+      }
     }
+    if (a.tl && c == 0) a.tl[2] = globaltimer_ns();
   }
 }
 
