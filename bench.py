@@ -178,6 +178,42 @@ def measure_pcie_gbs(torch):
     return n / best / 1e6
 
 
+def open_shared_pool(capi, local, torch, dist, coll_dev):
+    """The node's expert pool as a /dev/shm segment: local rank 0 creates and
+    fills it (its stack generates the weights into it), the other ranks map it
+    after a barrier and pass its layout flags. Returns ptr / map / flags and a
+    hook to run after the stack exists (barrier, flag broadcast, unlink)."""
+    L, E, d, F = CFG["num_layers"], CFG["experts"], MODEL["d_model"], MODEL["ffn"]
+    nbytes = L * E * 3 * F * d * 2
+    tag = os.environ.get("TORCHELASTIC_RUN_ID", "run") + "_" + os.environ.get("MASTER_PORT", "0")
+    path = f"/dev/shm/moeb_pool_{tag}"
+    info = {}
+    if local == 0:
+        with open(path, "wb") as f:
+            f.truncate(nbytes)
+    dist.barrier()
+    mm = np.memmap(path, dtype=np.uint8, mode="r+", shape=(nbytes,))
+    info["map"], info["ptr"] = mm, mm.ctypes.data
+    flags = torch.zeros(1, dtype=torch.int64, device=coll_dev)
+    info["flags"] = 0
+    if local != 0:
+        dist.broadcast(flags, src=0)  # rank 0 filled the pool and knows its layout
+        info["flags"] = int(flags.item())
+
+    def after_create(stack):
+        if local == 0:
+            fl = C.c_uint32(0)
+            capi.lib().moeb_host_pool_flags(stack.h, C.byref(fl))
+            flags.fill_(fl.value)
+            dist.broadcast(flags, src=0)
+        dist.barrier()
+        if local == 0:
+            os.unlink(path)  # the mappings stay valid
+
+    info["after_create"] = after_create
+    return info
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -186,9 +222,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # MOEB_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo (exercises the
+    # multi-rank path on a one-GPU box; not a scaling measurement)
+    share_gpu = os.environ.get("MOEB_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local = 0
     torch.cuda.set_device(local)
+    coll_dev = "cpu" if share_gpu else "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if world > 1:
@@ -198,14 +243,14 @@ def run_ours(args):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -226,7 +271,18 @@ def run_ours(args):
     # no per-kernel CUDA events in the timed stack (they would serialise the
     # programmatic dependent launches); the per-kernel split comes from the
     # device-clock timeline (globaltimer stamps written by the kernels)
-    stack = capi.Stack(cfg, weight_seed=7, trace_timeline=True, device=local, **MODEL)
+    shared_pool = None
+    if world > 1:
+        # one pinned host pool per node, in /dev/shm, mapped by every rank
+        # (28.8 GB instead of 28.8 GB x ranks): local rank 0 fills it
+        node_local = int(os.environ.get("LOCAL_RANK", "0"))
+        shared_pool = open_shared_pool(capi, node_local, torch, dist, coll_dev)
+        stack = capi.Stack(cfg, weight_seed=7, trace_timeline=True, device=local,
+                           weights_host=(shared_pool["ptr"], shared_pool["map"]), fill_pool=(node_local == 0),
+                           pool_flags=0 if node_local == 0 else shared_pool["flags"], **MODEL)
+        shared_pool["after_create"](stack)
+    else:
+        stack = capi.Stack(cfg, weight_seed=7, trace_timeline=True, device=local, **MODEL)
     create_s = time.time() - t0
     stack.set_logits_trace(logits, T)
     # a torch-owned stream for the stack's work: pinned-buffer copies recorded

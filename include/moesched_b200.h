@@ -78,6 +78,11 @@ typedef struct moeb_model {
  * split-K FFN deals its rows round-robin, a fixed assignment); the flag is
  * accepted for API stability. */
 #define MOEB_MODEL_DETERMINISTIC 16u
+/* weights_host is caller memory (e.g. a shared-memory segment every process
+ * of a node maps) to be FILLED with the synthetic weights in this stack's
+ * layout; later stacks then pass it without this flag (with
+ * MOEB_MODEL_DOWN_T when moeb_host_pool_flags says so). */
+#define MOEB_MODEL_FILL_POOL 32u
 
 typedef struct moeb_engine moeb_engine; /* decision engine only (simulate path) */
 typedef struct moeb_stack moeb_stack;   /* full MoE decode stack */

@@ -286,9 +286,9 @@ class Stack:
 
     def __init__(self, cfg: Config, d_model, ffn, shared_ffn=0, shared_gate=0, renormalize=0,
                  routed_scale=1.0, weight_seed=7, log_steps=False, device=0, weights_host=None,
-                 time_kernels=False, trace_timeline=False, deterministic=False):
+                 time_kernels=False, trace_timeline=False, deterministic=False, fill_pool=False, pool_flags=0):
         flags = (MODEL_LOG_STEPS if log_steps else 0) | (2 if time_kernels else 0) | (4 if trace_timeline else 0) | \
-            (16 if deterministic else 0)
+            (16 if deterministic else 0) | (32 if fill_pool else 0) | pool_flags
         m = Model(d_model=d_model, ffn=ffn, shared_ffn=shared_ffn, shared_gate=shared_gate,
                   renormalize=renormalize, routed_scale=routed_scale, weight_seed=weight_seed,
                   max_batch=cfg.batch, flags=flags)

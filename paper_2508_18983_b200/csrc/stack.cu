@@ -1023,7 +1023,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   S->splitk = B == 1 && d <= 2048 && getenv("MOEB_NO_SPLITK") == nullptr;
   if (const char* ur = getenv("MOEB_SK_UNIT")) S->unit_rows = (uint32_t)atoi(ur);
   if (const char* fd = getenv("MOEB_FFN_DBG")) S->ffn_dbg = (uint32_t)atoi(fd);  // microbenchmark knob
-  if (weights_host && S->splitk != ((m.flags & MOEB_MODEL_DOWN_T) != 0))
+  if (weights_host && !(m.flags & MOEB_MODEL_FILL_POOL) && S->splitk != ((m.flags & MOEB_MODEL_DOWN_T) != 0))
     throw Error(1, S->splitk ? "model: a batch-1 stack needs a row-interleaved host pool (MOEB_MODEL_DOWN_T)"
                              : "model: this stack needs a host pool in the [gate][up][down] layout (no MOEB_MODEL_DOWN_T)");
   // resident (HBM) weights: router, shared expert, shared gate
@@ -1049,6 +1049,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // pinned host pool of every routed expert
   const uint64_t eb = S->expert_elems * 2;
   const uint64_t pool_bytes = (uint64_t)L * E * eb;
+  const bool fill = weights_host && (m.flags & MOEB_MODEL_FILL_POOL);
   if (weights_host) {
     S->pool = const_cast<uint16_t*>(static_cast<const uint16_t*>(weights_host));
     cudaPointerAttributes pa{};
@@ -1060,6 +1061,8 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   } else {
     MOEB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->pool), pool_bytes, cudaHostAllocPortable));
     S->own_pool = true;
+  }
+  if (!weights_host || fill) {
     // generate on the device, expert by expert, then D2H into the pool
     DevBuf<uint16_t> tmp(2 * S->expert_elems);
     for (uint64_t i = 0; i < (uint64_t)L * E; ++i) {
