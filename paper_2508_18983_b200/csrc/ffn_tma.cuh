@@ -227,7 +227,7 @@ __device__ inline void gu_compute(const uint16_t* gs, const uint16_t* us_rows, c
 
 template <int NT>
 __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_t hstride, uint32_t F,
-                                  const Item& it, float* acc_row) {
+                                  const Item& it, float* acc_row, uint32_t t0 = 0) {
   const int lane = lane_id();
   const uint32_t nvec = F / 8;
   float a[NT];
@@ -240,8 +240,8 @@ __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_
       const uint4 wv = reinterpret_cast<const uint4*>(ws)[c];
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        if ((uint32_t)t < it.n_tok) {
-          const float4* hp = reinterpret_cast<const float4*>(hsrc + (size_t)t * hstride + c * 8);
+        if ((uint32_t)t + t0 < it.n_tok) {
+          const float4* hp = reinterpret_cast<const float4*>(hsrc + (size_t)(t + t0) * hstride + c * 8);
           a[t] += dot8f(wv, hp[0], hp[1]);
         }
       }
@@ -257,8 +257,8 @@ __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_
         wv[j] = reinterpret_cast<const uint4*>(ws)[c];
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
-          if ((uint32_t)t < it.n_tok) {
-            const float4* hp = reinterpret_cast<const float4*>(hsrc + (size_t)t * hstride + c * 8);
+          if ((uint32_t)t + t0 < it.n_tok) {
+            const float4* hp = reinterpret_cast<const float4*>(hsrc + (size_t)(t + t0) * hstride + c * 8);
             h0[j][t] = hp[0];
             h1[j][t] = hp[1];
           }
@@ -274,7 +274,7 @@ __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_
       if (c < nvec) {
 #pragma unroll
         for (int t = 0; t < NT; ++t)
-          if ((uint32_t)t < it.n_tok) dot8_f2(a2[t], wv[j], h0[j][t], h1[j][t]);
+          if ((uint32_t)t + t0 < it.n_tok) dot8_f2(a2[t], wv[j], h0[j][t], h1[j][t]);
       }
     }
 #pragma unroll
@@ -283,11 +283,11 @@ __device__ inline void dn_compute(const uint16_t* ws, const float* hsrc, uint32_
   }
 #pragma unroll
   for (int t = 0; t < NT; ++t) {
-    if ((uint32_t)t < it.n_tok) {
+    if ((uint32_t)t + t0 < it.n_tok) {
       const float s = warp_sum(a[t]);
       if (lane == 0) {
-        const uint32_t tok = it.tok[t];
-        acc_row[tok] = fmaf(it.wt[t], s, acc_row[tok]);
+        const uint32_t tok = it.tok[t + t0];
+        acc_row[tok] = fmaf(it.wt[t + t0], s, acc_row[tok]);
       }
     }
   }
@@ -401,6 +401,42 @@ __device__ inline void gu_pair_mma(const uint16_t* gs, const uint16_t* us_rows, 
     *h_out = silu * gu.y;
   }
 }
+// gate_up row pair for up to NT tokens of an item (tokens [t0, t0+NT)) with
+// the bf16 activations in shared memory ([B][d]): the diagonal mapping with
+// one ldmatrix per 128-column block shared by the tokens and one mma per
+// token (B fragments straight from the token's smem row).
+template <int NT>
+__device__ inline void gu_pair_mma_tok(const uint16_t* gs, const uint16_t* us_rows, const uint16_t* xs, uint32_t d,
+                                       const Item& it, uint32_t t0, uint32_t r, float* h_item, uint32_t Fmax) {
+  const int lane = lane_id();
+  const uint32_t nt = min((uint32_t)NT, it.n_tok - t0);
+  float acc[NT][4];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[t][q] = 0.f;
+  const uint32_t* xw[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+    xw[t] = reinterpret_cast<const uint32_t*>(xs + (size_t)it.tok[t0 + ((uint32_t)t < nt ? t : 0)] * d) + lane;
+  const uint32_t base = diag_addr(smem_u32(gs), smem_u32(us_rows));
+  const uint32_t nb = d / 128;
+  for (uint32_t b = 0; b < nb; ++b) {
+    uint32_t a[4];
+    ldsm_x4(base + b * 256, a);
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+      if ((uint32_t)t < nt) mma16816(acc[t], a, xw[t][b * 64], xw[t][b * 64 + 32]);
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    if ((uint32_t)t < nt) {
+      const float2 gu = diag_reduce(acc[t]);
+      if (lane == 0) h_item[(size_t)(t0 + t) * Fmax + r] = __fdiv_rn(gu.x, 1.0f + expf(-gu.x)) * gu.y;
+    }
+  }
+}
+
 // down rows r0 / r1 (smem) against h split as bf16 hi + lo (smem words:
 // hi32[F/2] then lo32[F/2]); returns the two dots on every lane
 __device__ inline float2 dn_pair_mma(const uint16_t* w0, const uint16_t* w1, const uint32_t* hw, uint32_t F) {
@@ -470,7 +506,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
   unsigned char* ring = smem_raw;                                   // S * SB
   uint16_t* us = reinterpret_cast<uint16_t*>(smem_raw + S * SB);  // [B][d] bf16, or [B][d] fp32 when B <= 4
   float* u32 = reinterpret_cast<float*>(us);
-  constexpr bool kF32U = NTMAX <= 4;
+  constexpr bool kF32U = false;  // activations stay bf16 in smem (tensor-core gate_up)
   // the plan header + items live in shared memory for the whole launch
   Plan* p = reinterpret_cast<Plan*>(smem_raw + S * SB + a.x_smem);
   float* acc_s = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(p) + a.plan_smem);  // [NG][acc_rows][B]
@@ -592,13 +628,16 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
     const uint32_t nt = it.n_tok;
     const uint16_t* gs = reinterpret_cast<const uint16_t*>(src) + (size_t)wg * d;
     const uint16_t* ur = reinterpret_cast<const uint16_t*>(src + n * d * 2) + (size_t)wg * d;
-    if (NTMAX == 1) gu_pair_mma(gs, ur, xb, d, h_item + r + wg);
-    else if (kF32U) {
-      if (nt <= 1) gu_compute_f32<1>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
-      else gu_compute_f32<(NTMAX < 4 ? NTMAX : 4)>(gs, ur, u32, d, it, r + wg, h_item, a.Fmax);
+    if (NTMAX == 1) {
+      gu_pair_mma(gs, ur, xb, d, h_item + r + wg);
+    } else {
+      // tensor cores, tokens in groups of (up to) 4
+      (void)u32;
+      for (uint32_t t0 = 0; t0 < nt; t0 += 4) {
+        if (nt - t0 <= 1) gu_pair_mma_tok<1>(gs, ur, us, d, it, t0, r + wg, h_item, a.Fmax);
+        else gu_pair_mma_tok<4>(gs, ur, us, d, it, t0, r + wg, h_item, a.Fmax);
+      }
     }
-    else if (NTMAX <= 8 || nt <= 8) gu_compute<(NTMAX < 8 ? NTMAX : 8)>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
-    else gu_compute<NTMAX>(gs, ur, us, d, it, r + wg, h_item, a.Fmax);
   };
   auto signal = [&](uint32_t si, uint32_t ci) {  // this warp finished its share; last warp of the CTA signals
     __syncwarp();
@@ -688,10 +727,12 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_tma_kernel(FfnTArgs a) {
       for (uint32_t q = first; q < n; q += kGroupWarps) {
         const uint16_t* ws = reinterpret_cast<const uint16_t*>(src) + (size_t)q * F;
         float* acc_row = acc_g + (size_t)(r + q - dlo) * B;
-        if (NTMAX == 1 || nt <= 1) dn_compute<1>(ws, hsrc, hstride, F, it, acc_row);
-        else if (NTMAX <= 4 || nt <= 4) dn_compute<(NTMAX < 4 ? NTMAX : 4)>(ws, hsrc, hstride, F, it, acc_row);
-        else if (NTMAX <= 8 || nt <= 8) dn_compute<(NTMAX < 8 ? NTMAX : 8)>(ws, hsrc, hstride, F, it, acc_row);
-        else dn_compute<NTMAX>(ws, hsrc, hstride, F, it, acc_row);
+        // tokens in groups of (up to) 8: no 32-wide accumulator arrays
+        for (uint32_t t0 = 0; t0 < nt; t0 += 8) {
+          if (NTMAX == 1 || nt - t0 <= 1) dn_compute<1>(ws, hsrc, hstride, F, it, acc_row, t0);
+          else if (NTMAX <= 4 || nt - t0 <= 4) dn_compute<(NTMAX < 4 ? NTMAX : 4)>(ws, hsrc, hstride, F, it, acc_row, t0);
+          else dn_compute<(NTMAX < 8 ? NTMAX : 8)>(ws, hsrc, hstride, F, it, acc_row, t0);
+        }
       }
     }
   };
@@ -989,7 +1030,7 @@ inline FfnLaunch ffn_launch_config(uint32_t B, uint32_t d, uint32_t F, uint32_t 
   const uint32_t ng = nc / kGroupWarps;
   const uint32_t max_items = 1 + std::min(E, B * top_k);
   L.plan_smem = (uint32_t)((offsetof(Plan, items) + (size_t)max_items * sizeof(Item) + 15) & ~(size_t)15);
-  L.x_smem = (B == 1 && d <= 2048) ? 0u : (uint32_t)((((size_t)B * d * (B <= 4 ? 4 : 2)) + 15) & ~(size_t)15);
+  L.x_smem = (B == 1 && d <= 2048) ? 0u : (uint32_t)((((size_t)B * d * 2) + 15) & ~(size_t)15);
   L.acc_rows = (d + sms - 1) / sms;
   const size_t accb = ((size_t)ng * L.acc_rows * B + 3) / 4 * 16;
   const size_t fixed = L.x_smem + L.plan_smem + accb;
