@@ -280,7 +280,10 @@ struct EarlyPublish {
 #endif
       if (n) __threadfence_system();
       me->seq = (mseq << 8) | n;
-      if (A.tl) A.tl[4] = globaltimer_ns();
+      if (A.tl) {
+        A.tl[4] = globaltimer_ns();
+        A.tl[15] = n;  // uploads published by this step
+      }
 #ifdef MOEB_PROFILE_PHASES
       st->prof[13] += gtimer() - tf0;
 #endif
@@ -864,7 +867,10 @@ struct moeb_stack {
       MailEntry* me = &ring[expect % kRing];
       const uint64_t sv = me->seq;
       if ((sv >> 8) != expect) {
-        if (++spins > 2000) std::this_thread::yield();
+        // a dedicated poller: the mailbox is the decode loop's critical path
+        // (publish -> copy start); yield only after a long idle stretch
+        if (++spins > (1u << 20)) std::this_thread::yield();
+        else __builtin_ia32_pause();
         continue;
       }
       spins = 0;
@@ -877,24 +883,28 @@ struct moeb_stack {
           copier_msg = "cuStreamWaitValue32 failed";
           copier_error = 5;
         }
-        std::lock_guard<std::mutex> g(io_mu);
+        // submit first, account after: the copy's start is what the GPU waits for
         const int ei = ev_next;
         ev_next = (ev_next + 1) % kEv;
-        harvest(ei);
+        {
+          std::lock_guard<std::mutex> g(io_mu);
+          harvest(ei);  // recorded kEv uploads ago: long complete
+        }
         cudaEventRecord(ev_a[ei], copy_stream);
         const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(c.dst),
                                                reinterpret_cast<const char*>(pool) + c.src_off, c.bytes,
                                                cudaMemcpyHostToDevice, copy_stream);
-        cudaEventRecord(ev_b[ei], copy_stream);
-        ev_live[ei] = true;
-        if (ce != cudaSuccess) {
-          copier_msg = std::string("upload failed: ") + cudaGetErrorString(ce);
-          copier_error = 5;
-        }
         if (p_write32(copy_stream, done_ptr, c.id, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
           copier_msg = "cuStreamWriteValue32 failed";
           copier_error = 5;
         }
+        cudaEventRecord(ev_b[ei], copy_stream);
+        if (ce != cudaSuccess) {
+          copier_msg = std::string("upload failed: ") + cudaGetErrorString(ce);
+          copier_error = 5;
+        }
+        std::lock_guard<std::mutex> g(io_mu);
+        ev_live[ei] = true;
         io.h2d_bytes += c.bytes;
         io.h2d_copies += 1;
       }

@@ -79,6 +79,15 @@ def main():
         for a, b in zip(idx[:-1], idx[1:]):
             gaps.append(tl[b, 4] - tl[a, 1])
         print("last upload seen -> next uploads published", us(np.array(gaps)))
+        # single-upload steps whose copy engine was idle at publish: publish -> landed minus the copy time
+        eb = 3 * 1408 * 2048 * 2
+        lat = []
+        for i in range(1, len(tl)):
+            if tl[i, 15] == 1 and tl[i, 1] != 0 and tl[i - 1, 1] != 0 and tl[i - 1, 1] < tl[i, 4]:
+                lat.append(tl[i, 1] - tl[i, 4] - eb / 54.4e9 * 1e9)
+        if lat:
+            print("single-upload steps", len(lat), "publish->landed minus 17.3MB@54.4GB/s: median us",
+                  round(float(np.median(lat)) / 1e3, 2), "p10", round(float(np.percentile(lat, 10)) / 1e3, 2))
     st.close()
 
 
