@@ -20,8 +20,6 @@
 // and the uploaded experts follow on the same ring without any barrier.
 #pragma once
 
-#include <cstdlib>
-
 #include "ffn_tma.cuh"
 
 namespace moeb {
@@ -424,24 +422,14 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
 // the reduction scratch (aliases the ring).
 inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int consumers, bool deterministic) {
   FfnLaunch L{};
-  if (consumers == 12) {
-    L.fn = ffn_splitk_kernel<12, false>;
-    L.threads = 32 * 13;
-  } else if (consumers == 4) {
-    L.fn = ffn_splitk_kernel<4, true>;
-    L.threads = 32 * 5;
-  } else if (consumers == 6) {
-    L.fn = ffn_splitk_kernel<6, true>;
-    L.threads = 32 * 7;
-  } else {
-    L.fn = ffn_splitk_kernel<8, true>;
-    L.threads = 32 * 9;
-  }
+  (void)consumers;  // 4-12 consumer warps measured within 0.5 us of each other: 8
+  L.fn = ffn_splitk_kernel<8, true>;
+  L.threads = 32 * 9;
   L.stage_bytes = 3 * 2 * d;
   // step k -> warp k % NC: the stage count is a multiple of NC
   (void)deterministic;
   const uint32_t nc = L.threads / 32 - 1;
-  L.stages = std::max<uint32_t>(nc, (getenv("MOEB_SK_STAGES") ? atoi(getenv("MOEB_SK_STAGES")) : kSkStages) / nc * nc);
+  L.stages = std::max<uint32_t>(nc, kSkStages / nc * nc);
   const uint32_t max_items = 1 + std::min(E, top_k);
   L.plan_smem = (uint32_t)((offsetof(Plan, items) + (size_t)max_items * sizeof(Item) + 15) & ~(size_t)15);
   L.x_smem = 0;

@@ -1138,8 +1138,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // kernel resources: FFN launch shape (ring stages, h staging, accumulators)
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k, getenv("MOEB_SK_NC") ? atoi(getenv("MOEB_SK_NC")) : 8,
-                                          getenv("MOEB_DYNAMIC_ROWS") == nullptr)
+  S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k, 8, getenv("MOEB_DYNAMIC_ROWS") == nullptr)
                      : ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
   if (S->ffn.stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
   S->ticket.alloc(1);
