@@ -74,6 +74,11 @@ typedef struct moeb_model {
  * split-K FFN) store it row-interleaved, [ffn][3][d]: gate row r, up row r,
  * down column r. A caller-supplied pool declares that layout with this flag. */
 #define MOEB_MODEL_DOWN_T 8u
+/* Host pool layout of batch 2..32 stacks whose ffn and shared_ffn are
+ * multiples of 128 (the tensor-core FFN): every expert is a sequence of 16 KB
+ * [128 x 64] bf16 tiles in the SWIZZLE_128B K-major order, gate_up
+ * [ffn/128][d/64][gate | up] then down [d/128][ffn/128][2 K-blocks]. */
+#define MOEB_MODEL_TILED 64u
 /* Bitwise-reproducible layer outputs. Always the case now (the batch-1
  * split-K FFN deals its rows round-robin, a fixed assignment); the flag is
  * accepted for API stability. */
@@ -266,7 +271,8 @@ int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction,
  * (8-11: CTA 0). Diagnostics only. */
 int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n);
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes);
-/* MOEB_MODEL_DOWN_T when the stack's pool is row-interleaved (batch 1). */
+/* MOEB_MODEL_DOWN_T when the stack's pool is row-interleaved (batch 1),
+ * MOEB_MODEL_TILED when it is UMMA-tiled (batched tensor-core FFN). */
 int moeb_host_pool_flags(moeb_stack* s, uint32_t* flags);
 
 #ifdef __cplusplus

@@ -1,0 +1,504 @@
+// ffn_umma.cuh — batched-decode (B = 2..32) grouped SwiGLU FFN on the 5th-gen
+// tensor cores (tcgen05.mma, accumulators in TMEM, operands staged in shared
+// memory by cp.async.bulk), sm_100a.
+//
+// Why tensor cores here and not at B = 1: with B tokens per step an expert's
+// weight tile is multiplied by up to B activation vectors, a [128 x K] x
+// [K x N] contraction with N = the batch. It is still HBM-bound (every weight
+// byte is read once per step), so the MMA computes ALL B token columns for
+// every expert — tokens not routed to an expert get a zero combine weight in
+// the epilogue — which removes every gather/scatter and keeps one B operand
+// (the batch's activations) for all experts.
+//
+// Weights are stored "UMMA-tiled" (weights.cuh synth_tiled_kernel): every
+// 16 KB block is a [128 rows x 64 K] bf16 tile already in the canonical
+// SWIZZLE_128B K-major layout the MMA reads, so one 1-D bulk copy per stage
+// lands a ready operand (no tensor maps: the expert pointer comes from the
+// device-side plan, slot or staging buffer alike).
+//   gate_up section: unit u (128 intermediate rows) x K-block kb (64 of d):
+//                    [gate tile 16 KB][up tile 16 KB]
+//   down section:    unit m (128 output rows) x K-pair kp (128 of F):
+//                    [down tile kb = 2kp][down tile kb = 2kp + 1]
+//
+// Work units (grid-dynamic, one atomic grab per unit):
+//   gate_up (item, u): 32 KB stages over d/64 K-blocks; two accumulators
+//     (gate, up: N = Nx columns each); the epilogue thread of TMEM lane j owns
+//     intermediate row j of the unit: h = w_tok * silu(g) * up for every
+//     token column, split into bf16 hi + lo (h = hi + lo to 2^-17), stored as
+//     the down pass's B operand ([K-block][2 Bp rows][128 B], SW128).
+//   down (item, m): 32 KB weight stage + the item's h K-pair (from L2), one
+//     accumulator of N = 2 Bp columns (hi rows, lo rows); the epilogue writes
+//     the item's partial y[tok][row] (hi + lo) to part[item].
+// A down unit waits for its item's gate_up units (per-item grid counter).
+// Items whose weights are still on the PCIe copy stream are gated on
+// copies_done by the producer. End: grid barrier, each CTA sums its output
+// rows over the items in plan order (deterministic: no atomics on data),
+// residual, bf16 hidden for the next layer.
+//
+// Roles: warp 0 producer (one lane), warp 1 TMEM owner + MMA issuer (one
+// lane), warps 2..5 epilogue (TMEM lane quadrant = warp % 4).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ffn_tma.cuh"
+
+namespace moeb {
+
+constexpr uint32_t kUmBlk = 16384;          // one [128 x 64] bf16 tile
+constexpr uint32_t kUmA = 2 * kUmBlk;       // weight bytes per stage
+constexpr uint32_t kUmRec = 4;              // unit records in flight
+constexpr uint32_t kUmMaxStages = 8;
+constexpr uint32_t kUmThreads = 6 * 32;
+constexpr uint32_t kUmTmemCols = 128;       // two accumulator buffers of <= 64 columns
+// grid counters reused from the split-K / speculative kernels (B > 1 has no
+// speculative phase): activation tiles written, CTAs done with their units
+constexpr int kUmXCtr = kFfnSpecGuCtr;
+constexpr int kUmDoneCtr = kFfnSpecDoneCtr;
+
+struct UmArgs {
+  FfnTArgs f;
+  uint16_t* xt;     // activations, SW128-tiled: [d/64][Nx][64] bf16
+  float* part;      // per-item partial outputs [kMaxItems][B][d] fp32
+  uint32_t Nx;      // token rows of the gate_up B operand (multiple of 16)
+  uint32_t Bp;      // token rows of each hi / lo half of the down B operand (multiple of 8)
+  uint32_t stages;
+  uint32_t stage_bytes;
+};
+
+// ------------------------------------------------------------ tcgen05 PTX
+__device__ __forceinline__ uint64_t um_desc(uint32_t saddr) {
+  // SWIZZLE_128B K-major: SBO = 1024 B (8-row groups), LBO unused (1),
+  // descriptor version 1 (sm_100), layout type 2 (128 B swizzle)
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// kind::f16 instruction descriptor: bf16 A/B, fp32 D, both K-major, M = 128
+__host__ __device__ constexpr uint32_t um_idesc(uint32_t N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void um_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void um_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void um_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void um_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void um_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void um_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void um_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void wait_ctr_ge(const uint32_t* p, uint32_t v, uint32_t code) {
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_u32(p) < v) {
+    __nanosleep(32);
+    if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, code); break; }
+  }
+}
+// byte offset of element (r, k) of a [rows x 64] bf16 SW128 K-major tile
+__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t k) {
+  return (r >> 3) * 1024u + (r & 7u) * 128u + ((((k >> 3) ^ r) & 7u) << 4) + (k & 7u) * 2u;
+}
+
+struct UmRec {
+  uint32_t kind;   // 0 gate_up, 1 down, 2 end
+  uint32_t item;
+  uint32_t idx;    // gate_up unit u / down unit m
+  uint32_t n_st;   // stages of the unit
+};
+
+__global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_constant__ UmArgs ua) {
+  const FfnTArgs& a = ua.f;
+  extern __shared__ unsigned char um_smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kUmMaxStages], empty_bar[kUmMaxStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t rfull_bar[kUmRec], rempty_bar[kUmRec];
+  __shared__ UmRec recs[kUmRec];
+  __shared__ uint32_t s_tmem;
+  __shared__ uint32_t s_pre[kMaxItems + 2];  // unit prefix over the plan (see below)
+  __shared__ uint32_t s_total, s_ni, s_nr;
+
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
+  const uint32_t G = gridDim.x, c = blockIdx.x;
+  const uint32_t d = a.d, B = a.B, S = ua.stages, SB = ua.stage_bytes, Nx = ua.Nx, Bp = ua.Bp, Ndn = 2 * Bp;
+  const int warp = warp_id(), lane = lane_id();
+  // 1 KB-aligned ring (the SW128 atoms need it)
+  const uint32_t raw_addr = smem_u32(um_smem_raw);
+  unsigned char* ring = um_smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  const uint32_t ring_addr = smem_u32(ring);
+  const uint32_t nkb = d / 64, nm = d / 128;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    for (uint32_t j = 0; j < kUmRec; ++j) {
+      mbar_init(&rfull_bar[j], 1);
+      mbar_init(&rempty_bar[j], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "n"(kUmTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    um_fence_before();
+  }
+  // PDL: plan, u and x_in come from the kernels launched before
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // activations -> SW128 tiles (CTA c < d/64 writes K-block c; rows >= B zero)
+  if (c < nkb) {
+    const uint32_t chunks = Nx * 8;  // 16 B chunks of the block
+    for (uint32_t i = threadIdx.x; i < chunks; i += blockDim.x) {
+      const uint32_t r = i >> 3, ch = i & 7;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (r < B) v = __ldcg(reinterpret_cast<const uint4*>(a.u + (size_t)r * d + c * 64 + ch * 8));
+      *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(ua.xt) + (size_t)c * Nx * 128 +
+                                sw128_off(r, ch * 8)) = v;
+    }
+    fence_proxy_async_global();
+  }
+  if (threadIdx.x == 0) {
+    // unit sequence: [gate_up of the ready items][down of the ready items]
+    // then per waiting item [gate_up][down]. s_pre[i] = first unit of item i's
+    // gate_up (ready items: within the first segment; waiting: its block).
+    const uint32_t ni = a.plan->n_items, nr = a.plan->n_ready;
+    uint32_t acc = 0;
+    for (uint32_t i = 0; i < nr; ++i) {
+      s_pre[i] = acc;
+      acc += a.plan->items[i].F / 128;
+    }
+    s_pre[nr] = acc;          // first down unit of the ready items
+    acc += nr * nm;
+    for (uint32_t i = nr; i < ni; ++i) {
+      s_pre[i + 1] = acc;
+      acc += a.plan->items[i].F / 128 + nm;
+    }
+    s_total = acc;
+    s_ni = ni;
+    s_nr = nr;
+    if (a.tl && c == 0) a.tl[0] = globaltimer_ns();
+  }
+  __syncthreads();
+  if (c < nkb && threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&a.ctr[kUmXCtr], 1u);
+  }
+  um_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t total = s_total, nr = s_nr;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol = l2_evict_first_policy(), pol_keep = l2_evict_last_policy();
+      bool x_ready = false;
+      uint32_t k = 0;
+      uint32_t nxt = atomicAdd(&a.ctr[kFfnGuCtr], 1u);
+      for (uint32_t u = 0;; ++u) {
+        const uint32_t unit = nxt;
+        if (unit < total) nxt = atomicAdd(&a.ctr[kFfnGuCtr], 1u);
+        const uint32_t j = u % kUmRec;
+        mbar_wait(&rempty_bar[j], ((u / kUmRec) & 1) ^ 1);
+        UmRec r{2u, 0u, 0u, 0u};
+        if (unit < total) {
+          if (unit < s_pre[nr]) {
+            uint32_t i = 0;
+            while (s_pre[i + 1] <= unit) ++i;
+            r = UmRec{0u, i, unit - s_pre[i], nkb};
+          } else if (unit < s_pre[nr] + nr * nm) {
+            const uint32_t q = unit - s_pre[nr];
+            r = UmRec{1u, q / nm, q % nm, 0u};
+          } else {
+            uint32_t i = nr;
+            while (i + 1 < s_ni && s_pre[i + 2] <= unit) ++i;
+            const uint32_t q = unit - s_pre[i + 1], ngu = a.plan->items[i].F / 128;
+            r = q < ngu ? UmRec{0u, i, q, nkb} : UmRec{1u, i, q - ngu, 0u};
+          }
+          if (r.kind == 1) r.n_st = a.plan->items[r.item].F / 128;
+        }
+        recs[j] = r;
+        mbar_arrive(&rfull_bar[j]);
+        if (r.kind == 2) break;
+        const Item& it = a.plan->items[r.item];
+        const uint32_t F = it.F;
+        if (it.wait) {
+          const uint64_t t0 = globaltimer_ns();
+          while ((int32_t)(ld_acquire_u32(a.copies_done) - it.wait) < 0) {
+            __nanosleep(128);
+            if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 1u); break; }
+          }
+          if (a.tl && c == 0) a.tl[1] = globaltimer_ns();
+          fence_proxy_async_global();
+        }
+        const unsigned char* w = reinterpret_cast<const unsigned char*>(it.w);
+        if (r.kind == 0) {
+          if (!x_ready) {
+            wait_ctr_ge(&a.ctr[kUmXCtr], nkb, 7u);
+            fence_proxy_async_global();
+            x_ready = true;
+          }
+          const unsigned char* src = w + (size_t)r.idx * nkb * kUmA;
+          const unsigned char* xs = reinterpret_cast<const unsigned char*>(ua.xt);
+          const uint32_t xb = Nx * 128;
+          for (uint32_t s = 0; s < nkb; ++s, ++k) {
+            const uint32_t st = k % S;
+            mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
+            mbar_expect_tx(&full_bar[st], kUmA + xb);
+            bulk_g2s(ring + st * SB, src + (size_t)s * kUmA, kUmA, &full_bar[st], pol);
+            bulk_g2s(ring + st * SB + kUmA, xs + (size_t)s * xb, xb, &full_bar[st], pol_keep);
+          }
+        } else {
+          // h of the item: every gate_up unit must have landed
+          wait_ctr_ge(&a.ctr[r.item], F / 128, 8u);
+          fence_proxy_async_global();
+          const unsigned char* src = w + 2 * (size_t)F * d * 2 + (size_t)r.idx * (F / 128) * kUmA;
+          const unsigned char* hs =
+              reinterpret_cast<const unsigned char*>(a.h + (size_t)r.item * kMaxB * a.Fmax);
+          const uint32_t hb = 2 * Ndn * 128;
+          for (uint32_t s = 0; s < r.n_st; ++s, ++k) {
+            const uint32_t st = k % S;
+            mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
+            mbar_expect_tx(&full_bar[st], kUmA + hb);
+            bulk_g2s(ring + st * SB, src + (size_t)s * kUmA, kUmA, &full_bar[st], pol);
+            bulk_g2s(ring + st * SB + kUmA, hs + (size_t)s * hb, hb, &full_bar[st], pol_keep);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t id_gu = um_idesc(Nx), id_dn = um_idesc(Ndn);
+      uint32_t k = 0;
+      for (uint32_t u = 0;; ++u) {
+        const uint32_t j = u % kUmRec;
+        mbar_wait(&rfull_bar[j], (u / kUmRec) & 1);
+        const UmRec r = recs[j];
+        if (r.kind == 2) break;
+        const uint32_t b = u & 1;
+        mbar_wait(&tempty_bar[b], ((u >> 1) & 1) ^ 1);
+        um_fence_after();
+        const uint32_t acc0 = tmem + b * 64;
+        const uint32_t n_st = r.kind == 0 ? nkb : r.n_st;
+        for (uint32_t s = 0; s < n_st; ++s, ++k) {
+          const uint32_t st = k % S;
+          mbar_wait(&full_bar[st], (k / S) & 1);
+          um_fence_after();
+          const uint32_t sa = ring_addr + st * SB;
+          if (r.kind == 0) {
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk) {
+              const uint64_t bx = um_desc(sa + kUmA + kk * 32);
+              um_mma(acc0, um_desc(sa + kk * 32), bx, id_gu, (s | kk) != 0);
+              um_mma(acc0 + Nx, um_desc(sa + kUmBlk + kk * 32), bx, id_gu, (s | kk) != 0);
+            }
+          } else {
+#pragma unroll
+            for (uint32_t hf = 0; hf < 2; ++hf)
+#pragma unroll
+              for (uint32_t kk = 0; kk < 4; ++kk)
+                um_mma(acc0, um_desc(sa + hf * kUmBlk + kk * 32), um_desc(sa + kUmA + hf * Ndn * 128 + kk * 32),
+                       id_dn, (s | hf | kk) != 0);
+          }
+          um_commit(&empty_bar[st]);  // frees the stage once these MMAs have read it
+        }
+        um_commit(&tfull_bar[b]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint32_t et = (warp - 2) * 32 + lane;
+    for (uint32_t u = 0;; ++u) {
+      const uint32_t j = u % kUmRec;
+      mbar_wait(&rfull_bar[j], (u / kUmRec) & 1);
+      const UmRec r = recs[j];
+      if (r.kind == 2) break;
+      const uint32_t b = u & 1;
+      const Item& it = a.plan->items[r.item];
+      // combine weight of every token column (0: not routed to this item)
+      float wl = 0.f;
+      const uint32_t nt = it.n_tok;
+      for (uint32_t t = 0; t < nt; ++t)
+        if (it.tok[t] == (uint32_t)lane) wl = it.wt[t];
+      mbar_wait(&tfull_bar[b], (u >> 1) & 1);
+      um_fence_after();
+      const uint32_t ta = tmem + ((q * 32) << 16) + b * 64;
+      if (r.kind == 0) {
+        float g[32], up[32];
+        um_ld16(ta, g);
+        um_ld16(ta + Nx, up);
+        if (Nx > 16) {
+          um_ld16(ta + 16, g + 16);
+          um_ld16(ta + Nx + 16, up + 16);
+        }
+        um_ld_wait();
+        um_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[b]);
+        // intermediate row jr of the item -> down K-block jr / 64, column jr % 64
+        const uint32_t jr = r.idx * 128 + q * 32 + lane;
+        unsigned char* hb = reinterpret_cast<unsigned char*>(a.h + (size_t)r.item * kMaxB * a.Fmax) +
+                            (size_t)(jr >> 6) * Ndn * 128;
+        const uint32_t col = jr & 63;
+#pragma unroll
+        for (uint32_t n = 0; n < 32; ++n) {
+          if (n >= Bp) break;
+          const float wn = __shfl_sync(0xffffffffu, wl, n);
+          float h = 0.f;
+          if (n < Nx) h = wn * (g[n] / (1.f + __expf(-g[n]))) * up[n];
+          const uint16_t hi = f32_to_bf16_rne(h);
+          const uint16_t lo = f32_to_bf16_rne(h - bf2f(hi));
+          *reinterpret_cast<uint16_t*>(hb + sw128_off(n, col)) = hi;
+          *reinterpret_cast<uint16_t*>(hb + sw128_off(Bp + n, col)) = lo;
+        }
+        fence_proxy_async_global();
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(&a.ctr[r.item], 1u);
+          mbar_arrive(&rempty_bar[j]);
+        }
+      } else {
+        float vh[32], vl[32];  // hi / lo columns of every token
+#pragma unroll
+        for (uint32_t cc = 0; cc < 4; ++cc)
+          if (cc * 8 < Bp) {
+            um_ld8(ta + cc * 8, vh + cc * 8);
+            um_ld8(ta + Bp + cc * 8, vl + cc * 8);
+          }
+        um_ld_wait();
+        um_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[b]);
+        const uint32_t row = r.idx * 128 + q * 32 + lane;
+        float* pp = ua.part + (size_t)r.item * B * d + row;
+#pragma unroll
+        for (uint32_t n = 0; n < 32; ++n) {
+          if (n >= B) break;
+          pp[(size_t)n * d] = vh[n] + vl[n];
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (et == 0) mbar_arrive(&rempty_bar[j]);
+      }
+    }
+    // this CTA's units are complete
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    if (et == 0) {
+      __threadfence();
+      atomicAdd(&a.ctr[kUmDoneCtr], 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    wait_ctr_ge(&a.ctr[kUmDoneCtr], G, 9u);
+    if (a.tl && c == 0) a.tl[11] = globaltimer_ns();
+  }
+  __syncthreads();
+  // epilogue: y[tok][row] = sum over the items in plan order, residual
+  {
+    uint32_t dlo, dhi;
+    share(d, c, G, dlo, dhi);
+    const uint32_t rows = dhi - dlo, ni = s_ni;
+    for (uint32_t i = threadIdx.x; i < rows * B; i += blockDim.x) {
+      const uint32_t t = i / rows, o = dlo + i % rows;
+      const float* pp = ua.part + (size_t)t * d + o;
+      float y = 0.f;
+      for (uint32_t it = 0; it < ni; ++it) y += __ldcg(pp + (size_t)it * B * d);
+      const float xo = bf2f(a.x_in[(size_t)t * d + o]) + y;
+      a.x_out[(size_t)t * d + o] = f32_to_bf16_rne(xo);
+      a.y_out[(size_t)t * d + o] = y;
+    }
+  }
+  if (warp == 1) {
+    um_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kUmTmemCols));
+  }
+  // deferred admissions: staging -> slot once every CTA finished reading
+  const uint32_t n_d2d = a.plan->n_d2d;
+  if (n_d2d) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&a.ctr[kFfnD2dCtr], 1u);
+      wait_ctr_ge(&a.ctr[kFfnD2dCtr], G, 3u);
+    }
+    __syncthreads();
+    const Plan* gp = a.plan;
+    const uint64_t nv = gp->d2d_elems / 8;
+    for (uint32_t j = 0; j < n_d2d; ++j) {
+      const uint4* src = reinterpret_cast<const uint4*>(gp->d2d[j].src);
+      uint4* dst = reinterpret_cast<uint4*>(gp->d2d[j].dst);
+      for (uint64_t v = c * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)G * blockDim.x)
+        dst[v] = ldg_cg(src + v);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (n_d2d) __threadfence();
+    const uint32_t prev = atomicAdd(&a.ctr[kFfnExitCtr], 1u);
+    if (prev == G - 1) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ffn_done), "r"(a.plan->seq) : "memory");
+      if (a.tl) a.tl[2] = globaltimer_ns();
+    }
+  }
+}
+
+// Shared-memory ring for a batch: stages of 32 KB of weights + the largest
+// B operand (down: two K-blocks of 2 Bp rows). Returns stages == 0 when the
+// shapes do not fit.
+struct UmLaunch {
+  uint32_t Nx, Bp, stages, stage_bytes;
+  size_t smem;
+};
+inline UmLaunch umma_launch_config(uint32_t B) {
+  UmLaunch L{};
+  L.Nx = B <= 16 ? 16u : 32u;
+  L.Bp = (B + 7) / 8 * 8;
+  const uint32_t bmax = std::max(L.Nx * 128, 2 * (2 * L.Bp) * 128);
+  L.stage_bytes = (kUmA + bmax + 1023) / 1024 * 1024;
+  const size_t budget = 224 * 1024 - 1024;  // + 1 KB alignment slack
+  L.stages = (uint32_t)std::min<size_t>(kUmMaxStages, budget / L.stage_bytes);
+  L.smem = (size_t)L.stages * L.stage_bytes + 1024;
+  if (B < 2 || B > 32) L.stages = 0;
+  return L;
+}
+
+}  // namespace moeb

@@ -32,6 +32,7 @@
 #include "layer.cuh"
 #include "ffn_tma.cuh"
 #include "ffn_splitk.cuh"
+#include "ffn_umma.cuh"
 #include "weights.cuh"
 
 namespace moeb {
@@ -785,6 +786,11 @@ struct moeb_stack {
   DevBuf<uint32_t> spec_flag;
   bool spec = false;
   bool splitk = false;  // batch-1 split-K FFN; experts stored row-interleaved [F][3][d]
+  bool umma = false;    // batched tensor-core FFN (ffn_umma.cuh); experts stored UMMA-tiled
+  UmLaunch um{};
+  DevBuf<uint16_t> xt;  // activations, SW128-tiled (umma)
+  DevBuf<float> part;   // per-item partial outputs (umma)
+  uint32_t layout_flags() const { return splitk ? MOEB_MODEL_DOWN_T : umma ? MOEB_MODEL_TILED : 0u; }
   uint32_t unit_rows = 0, ffn_dbg = 0;
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
   DevBuf<StepRec> recs;
@@ -962,6 +968,15 @@ static void synth_rows(uint16_t* dst, uint32_t F, uint32_t d, uint64_t seed, uin
   MOEB_CUDA(cudaGetLastError());
 }
 
+static void synth_tiled(uint16_t* dst, uint32_t F, uint32_t d, uint64_t seed, uint64_t t0, uint64_t t1, uint64_t t2,
+                        float s_in, float s_down, cudaStream_t s) {
+  const uint64_t n = 3ull * F * d;
+  if (!n) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  synth_tiled_kernel<<<grid, 256, 0, s>>>(dst, F, d, seed, t0, t1, t2, s_in, s_down);
+  MOEB_CUDA(cudaGetLastError());
+}
+
 static float fan_scale(uint32_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
 
 // (Re)initialise the decision state and upload the initial residents. The
@@ -1033,7 +1048,14 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   S->splitk = B == 1 && d <= 2048 && getenv("MOEB_NO_SPLITK") == nullptr;
   if (const char* ur = getenv("MOEB_SK_UNIT")) S->unit_rows = (uint32_t)atoi(ur);
   if (const char* fd = getenv("MOEB_FFN_DBG")) S->ffn_dbg = (uint32_t)atoi(fd);  // microbenchmark knob
-  if (weights_host && !(m.flags & MOEB_MODEL_FILL_POOL) && S->splitk != ((m.flags & MOEB_MODEL_DOWN_T) != 0))
+  // batch 2..32: tensor-core FFN over UMMA-tiled experts, when the shapes
+  // tile (ffn, shared_ffn multiples of 128) and the pool is ours to lay out
+  // (or a caller pool declares the tiled layout). MOEB_NO_UMMA=1 selects the
+  // CUDA-core FFN over HF layouts.
+  const bool own_layout = !weights_host || (m.flags & MOEB_MODEL_FILL_POOL);
+  S->umma = B >= 2 && B <= 32 && F % 128 == 0 && Sh % 128 == 0 && d / 64 <= 148 &&
+            (own_layout || (m.flags & MOEB_MODEL_TILED)) && getenv("MOEB_NO_UMMA") == nullptr;
+  if (weights_host && !own_layout && S->layout_flags() != (m.flags & (MOEB_MODEL_DOWN_T | MOEB_MODEL_TILED)))
     throw Error(1, S->splitk ? "model: a batch-1 stack needs a row-interleaved host pool (MOEB_MODEL_DOWN_T)"
                              : "model: this stack needs a host pool in the [gate][up][down] layout (no MOEB_MODEL_DOWN_T)");
   // resident (HBM) weights: router, shared expert, shared gate
@@ -1045,6 +1067,8 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
       uint16_t* base = S->shared_w.p + (size_t)l * 3 * Sh * d;
       if (S->splitk) {
         synth_rows(base, Sh, d, seed, tid_shared(l, 0), tid_shared(l, 1), tid_shared(l, 2), fan_scale(d), fan_scale(Sh), s);
+      } else if (S->umma) {
+        synth_tiled(base, Sh, d, seed, tid_shared(l, 0), tid_shared(l, 1), tid_shared(l, 2), fan_scale(d), fan_scale(Sh), s);
       } else {
         synth(base, (uint64_t)Sh * d, seed, tid_shared(l, 0), 0, fan_scale(d), s);
         synth(base + (size_t)Sh * d, (uint64_t)Sh * d, seed, tid_shared(l, 1), 0, fan_scale(d), s);
@@ -1081,6 +1105,9 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
       if (S->splitk) {
         synth_rows(buf, F, d, seed, tid_expert(l, e, 0), tid_expert(l, e, 1), tid_expert(l, e, 2), fan_scale(d),
                    fan_scale(F), s);
+      } else if (S->umma) {
+        synth_tiled(buf, F, d, seed, tid_expert(l, e, 0), tid_expert(l, e, 1), tid_expert(l, e, 2), fan_scale(d),
+                    fan_scale(F), s);
       } else {
         synth(buf, (uint64_t)F * d, seed, tid_expert(l, e, 0), 0, fan_scale(d), s);
         synth(buf + (size_t)F * d, (uint64_t)F * d, seed, tid_expert(l, e, 1), 0, fan_scale(d), s);
@@ -1138,8 +1165,20 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // kernel resources: FFN launch shape (ring stages, h staging, accumulators)
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  if (S->umma) {
+    S->um = umma_launch_config(B);
+    S->xt.alloc((size_t)(d / 64) * S->um.Nx * 64);
+    S->part.alloc((size_t)kMaxItems * B * d);
+  }
   S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k, 8, getenv("MOEB_DYNAMIC_ROWS") == nullptr)
                      : ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
+  if (S->umma) {
+    S->ffn.fn = reinterpret_cast<void (*)(FfnTArgs)>(ffn_umma_kernel);
+    S->ffn.threads = kUmThreads;
+    S->ffn.stages = S->um.stages;
+    S->ffn.stage_bytes = S->um.stage_bytes;
+    S->ffn.smem = S->um.smem;
+  }
   if (S->ffn.stages < 2) throw Error(1, "model: batch * d_model too large for the FFN pipeline");
   S->ticket.alloc(1);
   S->ticket.zero(s);
@@ -1279,7 +1318,21 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     f.deterministic = getenv("MOEB_DYNAMIC_ROWS") ? 0u : 1u;
     f.dbg = S->ffn_dbg;
     f.x_smem = S->ffn.x_smem;
-    launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s, &f);
+    if (S->umma) {
+      UmArgs ua{};
+      ua.f = f;
+      ua.xt = S->xt.p;
+      ua.part = S->part.p;
+      ua.Nx = S->um.Nx;
+      ua.Bp = S->um.Bp;
+      ua.stages = S->um.stages;
+      ua.stage_bytes = S->um.stage_bytes;
+      launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s,
+                 &ua);
+    } else {
+      launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s,
+                 &f);
+    }
     S->n_launch_layers += 1;
     MOEB_CUDA(cudaGetLastError());
     if (S->timing) S->tick(s);
@@ -1482,7 +1535,7 @@ int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes) {
 }
 
 int moeb_host_pool_flags(moeb_stack* s, uint32_t* flags) {
-  *flags = s->splitk ? MOEB_MODEL_DOWN_T : 0u;
+  *flags = s->layout_flags();
   return 0;
 }
 

@@ -75,4 +75,39 @@ __global__ void synth_rows_kernel(uint16_t* __restrict__ dst, uint32_t F, uint32
   }
 }
 
+// One expert (or shared expert) in the UMMA-tiled layout of the batched
+// tensor-core FFN (ffn_umma.cuh): 16 KB [128 rows x 64 K] bf16 tiles in the
+// SWIZZLE_128B K-major order (row r, 16 B chunk j stored at chunk j ^ (r % 8)
+// of its 128 B line), grouped in 32 KB stages:
+//   gate_up: [F/128 units][d/64 K-blocks][gate tile | up tile]
+//   down:    [d/128 units][F/128 K-pairs][tile kb = 2p | tile kb = 2p + 1]
+// Element values are the logical tensors' (gate/up [F][d], down [d][F]).
+__host__ __device__ inline void tiled_coords(uint64_t p, uint32_t F, uint32_t d, uint32_t& m, uint64_t& idx) {
+  const uint64_t gu = 2ull * F * d;
+  const uint64_t q = p < gu ? p : p - gu;
+  const uint64_t blk = q / 16384, e = q % 16384;
+  const uint32_t half = (uint32_t)(e / 8192), off = (uint32_t)(e % 8192) * 2u;
+  const uint32_t r = (off / 1024u) * 8u + (off % 1024u) / 128u;
+  const uint32_t k = ((((off % 128u) / 16u) ^ r) & 7u) * 8u + (off % 16u) / 2u;
+  if (p < gu) {
+    const uint64_t u = blk / (d / 64), kb = blk % (d / 64);
+    m = half;  // 0 gate, 1 up
+    idx = (u * 128 + r) * d + kb * 64 + k;
+  } else {
+    const uint64_t mt = blk / (F / 128), kp = blk % (F / 128);
+    m = 2;
+    idx = (mt * 128 + r) * F + kp * 128 + half * 64 + k;
+  }
+}
+__global__ void synth_tiled_kernel(uint16_t* __restrict__ dst, uint32_t F, uint32_t d, uint64_t seed, uint64_t t_gate,
+                                   uint64_t t_up, uint64_t t_down, float s_in, float s_down) {
+  const uint64_t n = 3ull * F * d;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t m;
+    uint64_t idx;
+    tiled_coords(p, F, d, m, idx);
+    dst[p] = synth_weight(seed, m == 0 ? t_gate : m == 1 ? t_up : t_down, idx, m == 2 ? s_down : s_in);
+  }
+}
+
 }  // namespace moeb

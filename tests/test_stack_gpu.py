@@ -77,6 +77,10 @@ CASES = {
     "baseline_stages": (2, 16, 4, 1, 256, 128, 256, 4, 30, {"stages": (0, 0, 0, 0)}),
     "lru_seeded_b32": (2, 64, 6, 32, 256, 64, 128, 24, 12, {"stages": (0, 1, 1, 1), "init_fill": 1}),
     "window_beyond_smem": (2, 64, 6, 2, 256, 64, 128, 16, 20, {"window": 40}),
+    # batched tensor-core FFN (ffn_umma.cuh): ffn / shared_ffn multiples of 128
+    "umma_b32": (2, 64, 6, 32, 256, 128, 256, 24, 12, {"stages": (0, 1, 1, 1), "init_fill": 1}),
+    "umma_b17_d512": (2, 16, 4, 17, 512, 256, 128, 8, 12, {}),
+    "umma_b2_renorm": (2, 16, 2, 2, 256, 128, 0, 4, 20, {"renorm": 1}),
 }
 
 

@@ -35,7 +35,8 @@ def main():
     L, E, B, d = args.layers, 64, args.batch, 2048
     cfg = capi.Config.make(num_layers=L, experts=E, top_k=6, batch=B, alpha=0.25, seed=7,
                            slots=E if args.allhit else 16)
-    st = capi.Stack(cfg, 2048, 1408, 2816, weight_seed=7, time_kernels=args.time, trace_timeline=args.timeline)
+    st = capi.Stack(cfg, 2048, 1408, 2816, weight_seed=7, time_kernels=args.time, trace_timeline=args.timeline,
+                    log_steps=args.timeline)
     T = args.tokens
     st.set_logits_trace(capi.trace_logits(capi.generate_trace(L, E, B, T, 7)), T)
     x = torch.randn(T, B, d).to(torch.bfloat16).cuda()
@@ -70,6 +71,17 @@ def main():
         print("ffn CTA0 entry rel. decide entry", us(tl[:, 7] - tl[:, 3]), "spec plan seen rel. decide entry",
               us((tl[:, 6] - tl[:, 3])[tl[:, 6] != 0]) if (tl[:, 6] != 0).any() else None)
         print("ffn start->end (no uploads)", us((tl[:, 2] - tl[:, 0])[~miss]))
+        # algorithmic weight bytes per layer-step: distinct experts selected by
+        # the batch (after substitution) + the shared expert
+        dec = st.decisions()
+        eb = 3 * 1408 * 2048 * 2
+        nexp = [len({e for t in r["tok"] for e in t["sel"]}) for r in dec]
+        nexp = np.array(nexp[len(nexp) - len(tl):] if len(nexp) >= len(tl) else nexp, dtype=np.float64)
+        wbytes = nexp * eb + 2 * eb
+        ffn_ns = (tl[:, 2] - tl[:, 0]).astype(np.float64)
+        if len(nexp) == len(tl) and (~miss).any():
+            print("distinct experts per layer-step", round(float(nexp.mean()), 2), "weight MB", round(float(wbytes.mean()) / 1e6, 1),
+                  "ffn GB/s (bytes / start->end, no uploads)", round(float(wbytes[~miss].sum() / ffn_ns[~miss].sum()), 1))
         print("ffn last upload seen->end (uploads)", us((tl[:, 2] - tl[:, 1])[miss]))
         print("ffn end->next decide entry", us(nxt[:, 3] - cur[:, 2]))
         print("layer period", us(nxt[:, 3] - cur[:, 3]))
