@@ -40,6 +40,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ffn_tma.cuh"
@@ -52,15 +53,18 @@ constexpr uint32_t kUmRec = 4;              // unit records in flight
 constexpr uint32_t kUmMaxStages = 8;
 constexpr uint32_t kUmThreads = 6 * 32;
 constexpr uint32_t kUmTmemCols = 128;       // two accumulator buffers of <= 64 columns
-// grid counters reused from the split-K / speculative kernels (B > 1 has no
-// speculative phase): activation tiles written, CTAs done with their units
-constexpr int kUmXCtr = kFfnSpecGuCtr;
+// grid counter reused from the speculative kernel (B > 1 has no speculative
+// phase): CTAs done with their units
 constexpr int kUmDoneCtr = kFfnSpecDoneCtr;
 
 struct UmArgs {
   FfnTArgs f;
-  uint16_t* xt;     // activations, SW128-tiled: [d/64][Nx][64] bf16
-  float* part;      // per-item partial outputs [kMaxItems][B][d] fp32
+  uint16_t* xt;     // activations, SW128-tiled: [d/64][Nx][64] bf16 (written by the gate phase)
+  float* part;      // partial outputs [item, down split][B][d] fp32
+  float* gpart;     // gate_up K-split partials [tile][split][2 Nx][128] fp32
+  uint32_t* gcnt;   // per-tile split arrivals (monotonic: +KS per tile per launch)
+  uint32_t KS;      // gate_up K-splits (divides d/64)
+  uint32_t dn_st;   // K-pair stages per down unit
   uint32_t Nx;      // token rows of the gate_up B operand (multiple of 16)
   uint32_t Bp;      // token rows of each hi / lo half of the down B operand (multiple of 8)
   uint32_t stages;
@@ -132,7 +136,9 @@ __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t k) {
 struct UmRec {
   uint32_t kind;   // 0 gate_up, 1 down, 2 end
   uint32_t item;
-  uint32_t idx;    // gate_up unit u / down unit m
+  uint32_t idx;    // gate_up tile u / down row tile m
+  uint32_t split;  // gate_up K-split / down K-split
+  uint32_t s0;     // first K-block (gate_up) / K-pair (down) of the unit
   uint32_t n_st;   // stages of the unit
 };
 
@@ -144,8 +150,10 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   __shared__ __align__(8) uint64_t rfull_bar[kUmRec], rempty_bar[kUmRec];
   __shared__ UmRec recs[kUmRec];
   __shared__ uint32_t s_tmem;
-  __shared__ uint32_t s_pre[kMaxItems + 2];  // unit prefix over the plan (see below)
-  __shared__ uint32_t s_total, s_ni, s_nr;
+  // per item (plan order): first gate_up unit, first down unit, first tile,
+  // first down partial
+  __shared__ uint32_t s_gu0[kMaxItems + 1], s_dn0[kMaxItems + 1], s_tb[kMaxItems + 1], s_pb[kMaxItems + 1];
+  __shared__ uint32_t s_total, s_ni, s_last;
 
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
@@ -156,7 +164,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   const uint32_t raw_addr = smem_u32(um_smem_raw);
   unsigned char* ring = um_smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   const uint32_t ring_addr = smem_u32(ring);
-  const uint32_t nkb = d / 64, nm = d / 128;
+  const uint32_t nkb = d / 64, nm = d / 128, KS = ua.KS, kst = nkb / ua.KS, dn_st = ua.dn_st;
 
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < S; ++s) {
@@ -181,53 +189,50 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   }
   // PDL: plan, u and x_in come from the kernels launched before
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  // activations -> SW128 tiles (CTA c < d/64 writes K-block c; rows >= B zero)
-  if (c < nkb) {
-    const uint32_t chunks = Nx * 8;  // 16 B chunks of the block
-    for (uint32_t i = threadIdx.x; i < chunks; i += blockDim.x) {
-      const uint32_t r = i >> 3, ch = i & 7;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r < B) v = __ldcg(reinterpret_cast<const uint4*>(a.u + (size_t)r * d + c * 64 + ch * 8));
-      *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(ua.xt) + (size_t)c * Nx * 128 +
-                                sw128_off(r, ch * 8)) = v;
-    }
-    fence_proxy_async_global();
-  }
   if (threadIdx.x == 0) {
     // unit sequence: [gate_up of the ready items][down of the ready items]
-    // then per waiting item [gate_up][down]. s_pre[i] = first unit of item i's
-    // gate_up (ready items: within the first segment; waiting: its block).
+    // then per waiting item [gate_up][down]. An item has F/128 tiles x KS
+    // gate_up units (tile-major) and d/128 row tiles x DS down units, DS =
+    // ceil(tiles / dn_st).
     const uint32_t ni = a.plan->n_items, nr = a.plan->n_ready;
+    uint32_t tb = 0, pb = 0;
+    for (uint32_t i = 0; i < ni; ++i) {
+      s_tb[i] = tb;
+      s_pb[i] = pb;
+      const uint32_t t = a.plan->items[i].F / 128;
+      tb += t;
+      pb += (t + dn_st - 1) / dn_st;
+    }
+    s_tb[ni] = tb;
+    s_pb[ni] = pb;
     uint32_t acc = 0;
     for (uint32_t i = 0; i < nr; ++i) {
-      s_pre[i] = acc;
-      acc += a.plan->items[i].F / 128;
+      s_gu0[i] = acc;
+      acc += (s_tb[i + 1] - s_tb[i]) * KS;
     }
-    s_pre[nr] = acc;          // first down unit of the ready items
-    acc += nr * nm;
+    for (uint32_t i = 0; i < nr; ++i) {
+      s_dn0[i] = acc;
+      acc += nm * (s_pb[i + 1] - s_pb[i]);
+    }
     for (uint32_t i = nr; i < ni; ++i) {
-      s_pre[i + 1] = acc;
-      acc += a.plan->items[i].F / 128 + nm;
+      s_gu0[i] = acc;
+      acc += (s_tb[i + 1] - s_tb[i]) * KS;
+      s_dn0[i] = acc;
+      acc += nm * (s_pb[i + 1] - s_pb[i]);
     }
     s_total = acc;
     s_ni = ni;
-    s_nr = nr;
     if (a.tl && c == 0) a.tl[0] = globaltimer_ns();
   }
   __syncthreads();
-  if (c < nkb && threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(&a.ctr[kUmXCtr], 1u);
-  }
   um_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t total = s_total, nr = s_nr;
+  const uint32_t total = s_total, ni_all = s_ni;
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = l2_evict_first_policy(), pol_keep = l2_evict_last_policy();
-      bool x_ready = false;
       uint32_t k = 0;
       uint32_t nxt = atomicAdd(&a.ctr[kFfnGuCtr], 1u);
       for (uint32_t u = 0;; ++u) {
@@ -235,22 +240,21 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         if (unit < total) nxt = atomicAdd(&a.ctr[kFfnGuCtr], 1u);
         const uint32_t j = u % kUmRec;
         mbar_wait(&rempty_bar[j], ((u / kUmRec) & 1) ^ 1);
-        UmRec r{2u, 0u, 0u, 0u};
+        UmRec r{2u, 0u, 0u, 0u, 0u, 0u};
         if (unit < total) {
-          if (unit < s_pre[nr]) {
-            uint32_t i = 0;
-            while (s_pre[i + 1] <= unit) ++i;
-            r = UmRec{0u, i, unit - s_pre[i], nkb};
-          } else if (unit < s_pre[nr] + nr * nm) {
-            const uint32_t q = unit - s_pre[nr];
-            r = UmRec{1u, q / nm, q % nm, 0u};
-          } else {
-            uint32_t i = nr;
-            while (i + 1 < s_ni && s_pre[i + 2] <= unit) ++i;
-            const uint32_t q = unit - s_pre[i + 1], ngu = a.plan->items[i].F / 128;
-            r = q < ngu ? UmRec{0u, i, q, nkb} : UmRec{1u, i, q - ngu, 0u};
+          for (uint32_t i = 0; i < ni_all; ++i) {
+            const uint32_t tiles = s_tb[i + 1] - s_tb[i], DS = s_pb[i + 1] - s_pb[i];
+            if (unit >= s_gu0[i] && unit < s_gu0[i] + tiles * KS) {
+              const uint32_t q = unit - s_gu0[i];
+              r = UmRec{0u, i, q / KS, q % KS, (q % KS) * kst, kst};
+              break;
+            }
+            if (unit >= s_dn0[i] && unit < s_dn0[i] + nm * DS) {
+              const uint32_t q = unit - s_dn0[i], ds = q % DS;
+              r = UmRec{1u, i, q / DS, ds, ds * dn_st, min(dn_st, tiles - ds * dn_st)};
+              break;
+            }
           }
-          if (r.kind == 1) r.n_st = a.plan->items[r.item].F / 128;
         }
         recs[j] = r;
         mbar_arrive(&rfull_bar[j]);
@@ -268,15 +272,10 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         }
         const unsigned char* w = reinterpret_cast<const unsigned char*>(it.w);
         if (r.kind == 0) {
-          if (!x_ready) {
-            wait_ctr_ge(&a.ctr[kUmXCtr], nkb, 7u);
-            fence_proxy_async_global();
-            x_ready = true;
-          }
-          const unsigned char* src = w + (size_t)r.idx * nkb * kUmA;
-          const unsigned char* xs = reinterpret_cast<const unsigned char*>(ua.xt);
+          const unsigned char* src = w + ((size_t)r.idx * nkb + r.s0) * kUmA;
           const uint32_t xb = Nx * 128;
-          for (uint32_t s = 0; s < nkb; ++s, ++k) {
+          const unsigned char* xs = reinterpret_cast<const unsigned char*>(ua.xt) + (size_t)r.s0 * xb;
+          for (uint32_t s = 0; s < r.n_st; ++s, ++k) {
             const uint32_t st = k % S;
             mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
             mbar_expect_tx(&full_bar[st], kUmA + xb);
@@ -287,10 +286,10 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
           // h of the item: every gate_up unit must have landed
           wait_ctr_ge(&a.ctr[r.item], F / 128, 8u);
           fence_proxy_async_global();
-          const unsigned char* src = w + 2 * (size_t)F * d * 2 + (size_t)r.idx * (F / 128) * kUmA;
-          const unsigned char* hs =
-              reinterpret_cast<const unsigned char*>(a.h + (size_t)r.item * kMaxB * a.Fmax);
+          const unsigned char* src = w + 2 * (size_t)F * d * 2 + ((size_t)r.idx * (F / 128) + r.s0) * kUmA;
           const uint32_t hb = 2 * Ndn * 128;
+          const unsigned char* hs =
+              reinterpret_cast<const unsigned char*>(a.h + (size_t)r.item * kMaxB * a.Fmax) + (size_t)r.s0 * hb;
           for (uint32_t s = 0; s < r.n_st; ++s, ++k) {
             const uint32_t st = k % S;
             mbar_wait(&empty_bar[st], ((k / S) & 1) ^ 1);
@@ -315,7 +314,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         mbar_wait(&tempty_bar[b], ((u >> 1) & 1) ^ 1);
         um_fence_after();
         const uint32_t acc0 = tmem + b * 64;
-        const uint32_t n_st = r.kind == 0 ? nkb : r.n_st;
+        const uint32_t n_st = r.n_st;
         for (uint32_t s = 0; s < n_st; ++s, ++k) {
           const uint32_t st = k % S;
           mbar_wait(&full_bar[st], (k / S) & 1);
@@ -372,6 +371,49 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         um_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty_bar[b]);
+        if (KS > 1) {
+          // K-split: publish this split's partial dots; the last split of
+          // the tile sums all of them in split order (deterministic)
+          const uint32_t T = s_tb[r.item] + r.idx;
+          float* gp = ua.gpart + (size_t)T * KS * 2 * Nx * 128 + q * 32 + lane;
+          float* mine = gp + (size_t)r.split * 2 * Nx * 128;
+#pragma unroll
+          for (uint32_t n = 0; n < 32; ++n) {
+            if (n >= Nx) break;
+            __stcg(mine + n * 128, g[n]);
+            __stcg(mine + (Nx + n) * 128, up[n]);
+          }
+          __threadfence();
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (et == 0) s_last = (atomicAdd(&ua.gcnt[T], 1u) + 1) % KS == 0;
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+          if (!s_last) {
+            if (et == 0) mbar_arrive(&rempty_bar[j]);
+            continue;
+          }
+          __threadfence();
+          // every split's 2 Nx values in flight at once, summed in split order
+#pragma unroll
+          for (uint32_t n = 0; n < 32; ++n) g[n] = up[n] = 0.f;
+          for (uint32_t ks = 0; ks < KS; ++ks) {
+            const float* src = gp + (size_t)ks * 2 * Nx * 128;
+#pragma unroll
+            for (uint32_t n0 = 0; n0 < 32; n0 += 16) {
+              if (n0 >= Nx) break;
+              float tg[16], tu[16];
+#pragma unroll
+              for (uint32_t n = 0; n < 16; ++n) {
+                tg[n] = __ldcg(src + (n0 + n) * 128);
+                tu[n] = __ldcg(src + (Nx + n0 + n) * 128);
+              }
+#pragma unroll
+              for (uint32_t n = 0; n < 16; ++n) {
+                g[n0 + n] += tg[n];
+                up[n0 + n] += tu[n];
+              }
+            }
+          }
+        }
         // intermediate row jr of the item -> down K-block jr / 64, column jr % 64
         const uint32_t jr = r.idx * 128 + q * 32 + lane;
         unsigned char* hb = reinterpret_cast<unsigned char*>(a.h + (size_t)r.item * kMaxB * a.Fmax) +
@@ -408,7 +450,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty_bar[b]);
         const uint32_t row = r.idx * 128 + q * 32 + lane;
-        float* pp = ua.part + (size_t)r.item * B * d + row;
+        float* pp = ua.part + (size_t)(s_pb[r.item] + r.split) * B * d + row;
 #pragma unroll
         for (uint32_t n = 0; n < 32; ++n) {
           if (n >= B) break;
@@ -435,12 +477,28 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   {
     uint32_t dlo, dhi;
     share(d, c, G, dlo, dhi);
-    const uint32_t rows = dhi - dlo, ni = s_ni;
+    const uint32_t rows = dhi - dlo, np = s_pb[s_ni];
     for (uint32_t i = threadIdx.x; i < rows * B; i += blockDim.x) {
       const uint32_t t = i / rows, o = dlo + i % rows;
       const float* pp = ua.part + (size_t)t * d + o;
+      // 16 partials in flight per thread, summed in plan order
       float y = 0.f;
-      for (uint32_t it = 0; it < ni; ++it) y += __ldcg(pp + (size_t)it * B * d);
+      uint32_t it = 0;
+      for (; it + 16 <= np; it += 16) {
+        float v[16];
+#pragma unroll
+        for (uint32_t q2 = 0; q2 < 16; ++q2) v[q2] = __ldcg(pp + (size_t)(it + q2) * B * d);
+#pragma unroll
+        for (uint32_t q2 = 0; q2 < 16; ++q2) y += v[q2];
+      }
+      {
+        float v[16];
+#pragma unroll
+        for (uint32_t q2 = 0; q2 < 16; ++q2) v[q2] = it + q2 < np ? __ldcg(pp + (size_t)(it + q2) * B * d) : 0.f;
+#pragma unroll
+        for (uint32_t q2 = 0; q2 < 16; ++q2)
+          if (it + q2 < np) y += v[q2];
+      }
       const float xo = bf2f(a.x_in[(size_t)t * d + o]) + y;
       a.x_out[(size_t)t * d + o] = f32_to_bf16_rne(xo);
       a.y_out[(size_t)t * d + o] = y;
@@ -485,11 +543,22 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
 // B operand (down: two K-blocks of 2 Bp rows). Returns stages == 0 when the
 // shapes do not fit.
 struct UmLaunch {
-  uint32_t Nx, Bp, stages, stage_bytes;
+  uint32_t Nx, Bp, stages, stage_bytes, KS, dn_st;
   size_t smem;
 };
-inline UmLaunch umma_launch_config(uint32_t B) {
+inline UmLaunch umma_launch_config(uint32_t B, uint32_t d) {
   UmLaunch L{};
+  // ~16 x 32 KB stages per gate_up unit, <= 4 per down unit: enough units to
+  // spread a few experts over every SM with a short tail
+  const uint32_t nkb = d / 64;
+  L.KS = 1;
+  while (L.KS < 8 && nkb % (2 * L.KS) == 0 && nkb / (2 * L.KS) >= 16) L.KS *= 2;
+  L.dn_st = 4;
+  if (const char* e = getenv("MOEB_UMMA_KS")) {  // tuning knobs
+    const uint32_t ks = (uint32_t)atoi(e);
+    if (ks >= 1 && nkb % ks == 0) L.KS = ks;
+  }
+  if (const char* e = getenv("MOEB_UMMA_DNST")) L.dn_st = std::max(1, atoi(e));
   L.Nx = B <= 16 ? 16u : 32u;
   L.Bp = (B + 7) / 8 * 8;
   const uint32_t bmax = std::max(L.Nx * 128, 2 * (2 * L.Bp) * 128);

@@ -126,6 +126,9 @@ struct GateArgs {
   const uint16_t* wg;      // [E][d] router weights of this layer
   const uint16_t* wsg;     // [d] Qwen shared-expert gate row (nullable)
   uint16_t* u;             // [B][d] normalised input (written by CTA 0)
+  uint16_t* ut;            // the same, SW128-tiled [d/64][ut_rows][64] for the batched
+                           // tensor-core FFN (nullable; written by CTA 1, rows >= B stay 0)
+  uint32_t ut_rows;
   float* logits;           // [B][E + 1]; column E = shared-gate logit
   uint32_t B, d, E;
 };
@@ -169,6 +172,11 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
     const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
     reinterpret_cast<uint4*>(us + (size_t)t * d)[c] = ov;
     if (blockIdx.x == 0) reinterpret_cast<uint4*>(a.u + (size_t)t * d)[c] = ov;
+    if (a.ut && blockIdx.x == (gridDim.x > 1 ? 1u : 0u)) {
+      // 16 B chunk (c % 8) of K-block c / 8, row t: chunk position (c ^ t) % 8
+      const uint32_t off = (c >> 3) * a.ut_rows * 128u + (t >> 3) * 1024u + (t & 7u) * 128u + (((c ^ t) & 7u) << 4);
+      *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(a.ut) + off) = ov;
+    }
   }
   __syncthreads();
   const uint32_t rows = a.E + (a.wsg ? 1u : 0u);

@@ -789,7 +789,9 @@ struct moeb_stack {
   bool umma = false;    // batched tensor-core FFN (ffn_umma.cuh); experts stored UMMA-tiled
   UmLaunch um{};
   DevBuf<uint16_t> xt;  // activations, SW128-tiled (umma)
-  DevBuf<float> part;   // per-item partial outputs (umma)
+  DevBuf<float> part;   // partial outputs per (item, down split) (umma)
+  DevBuf<float> gpart;  // gate_up K-split partials (umma)
+  DevBuf<uint32_t> gcnt;
   uint32_t layout_flags() const { return splitk ? MOEB_MODEL_DOWN_T : umma ? MOEB_MODEL_TILED : 0u; }
   uint32_t unit_rows = 0, ffn_dbg = 0;
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
@@ -1166,9 +1168,16 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   if (S->umma) {
-    S->um = umma_launch_config(B);
+    S->um = umma_launch_config(B, d);
     S->xt.alloc((size_t)(d / 64) * S->um.Nx * 64);
-    S->part.alloc((size_t)kMaxItems * B * d);
+    S->xt.zero(s);  // token rows >= B stay zero
+    const uint64_t n_exp = std::min<uint64_t>(E, (uint64_t)B * cfg.top_k);
+    const uint64_t tiles = Sh / 128 + n_exp * (F / 128);
+    const uint64_t parts = (Sh / 128 + S->um.dn_st - 1) / S->um.dn_st + n_exp * ((F / 128 + S->um.dn_st - 1) / S->um.dn_st);
+    S->part.alloc(parts * B * d);
+    S->gpart.alloc(tiles * S->um.KS * 2 * S->um.Nx * 128);
+    S->gcnt.alloc(tiles);
+    S->gcnt.zero(s);
   }
   S->ffn = S->splitk ? ffn_splitk_config(d, E, cfg.top_k, 8, getenv("MOEB_DYNAMIC_ROWS") == nullptr)
                      : ffn_launch_config(B, d, F, Sh, E, cfg.top_k, S->spec ? sms - 1 : sms);
@@ -1241,6 +1250,8 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     g.wg = S->gate_w.p + (size_t)l * E * d;
     g.wsg = S->model.shared_gate ? S->sgate_w.p + (size_t)l * d : nullptr;
     g.u = S->u.p;
+    g.ut = S->umma ? S->xt.p : nullptr;
+    g.ut_rows = S->um.Nx;
     g.logits = S->logits.p;
     g.B = B;
     g.d = d;
@@ -1327,6 +1338,10 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
       ua.Bp = S->um.Bp;
       ua.stages = S->um.stages;
       ua.stage_bytes = S->um.stage_bytes;
+      ua.gpart = S->gpart.p;
+      ua.gcnt = S->gcnt.p;
+      ua.KS = S->um.KS;
+      ua.dn_st = S->um.dn_st;
       launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s,
                  &ua);
     } else {

@@ -81,6 +81,7 @@ CASES = {
     "umma_b32": (2, 64, 6, 32, 256, 128, 256, 24, 12, {"stages": (0, 1, 1, 1), "init_fill": 1}),
     "umma_b17_d512": (2, 16, 4, 17, 512, 256, 128, 8, 12, {}),
     "umma_b2_renorm": (2, 16, 2, 2, 256, 128, 0, 4, 20, {"renorm": 1}),
+    "umma_b32_ksplit_dsplit": (1, 16, 4, 32, 1024, 640, 256, 8, 8, {}),
 }
 
 
