@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   // first down partial
   __shared__ uint32_t s_gu0[kMaxItems + 1], s_dn0[kMaxItems + 1], s_tb[kMaxItems + 1], s_pb[kMaxItems + 1];
   __shared__ uint32_t s_total, s_ni, s_last;
+  __shared__ uint32_t s_F[kMaxItems], s_wait[kMaxItems];
+  __shared__ const unsigned char* s_w[kMaxItems];
 
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   const uint32_t raw_addr = smem_u32(um_smem_raw);
   unsigned char* ring = um_smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
   const uint32_t ring_addr = smem_u32(ring);
+  float* s_wv = reinterpret_cast<float*>(ring + (size_t)S * SB);  // [item][B] combine weight per token column
   const uint32_t nkb = d / 64, nm = d / 128, KS = ua.KS, kst = nkb / ua.KS, dn_st = ua.dn_st;
 
   if (threadIdx.x == 0) {
@@ -189,6 +192,24 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   }
   // PDL: plan, u and x_in come from the kernels launched before
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  {
+    // the plan's item table -> shared memory (parallel loads): F, weights,
+    // upload dependency, and each item's combine weight per token column
+    const uint32_t ni = a.plan->n_items;
+    for (uint32_t i = threadIdx.x; i < ni; i += blockDim.x) {
+      s_F[i] = a.plan->items[i].F;
+      s_wait[i] = a.plan->items[i].wait;
+      s_w[i] = reinterpret_cast<const unsigned char*>(a.plan->items[i].w);
+    }
+    for (uint32_t i = threadIdx.x; i < ni * B; i += blockDim.x) s_wv[i] = 0.f;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < ni * kMaxB; i += blockDim.x) {
+      const Item& it = a.plan->items[i / kMaxB];
+      const uint32_t jt = i % kMaxB;
+      if (jt < it.n_tok) s_wv[(i / kMaxB) * B + it.tok[jt]] = it.wt[jt];
+    }
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     // unit sequence: [gate_up of the ready items][down of the ready items]
     // then per waiting item [gate_up][down]. An item has F/128 tiles x KS
@@ -199,7 +220,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
     for (uint32_t i = 0; i < ni; ++i) {
       s_tb[i] = tb;
       s_pb[i] = pb;
-      const uint32_t t = a.plan->items[i].F / 128;
+      const uint32_t t = s_F[i] / 128;
       tb += t;
       pb += (t + dn_st - 1) / dn_st;
     }
@@ -259,18 +280,17 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         recs[j] = r;
         mbar_arrive(&rfull_bar[j]);
         if (r.kind == 2) break;
-        const Item& it = a.plan->items[r.item];
-        const uint32_t F = it.F;
-        if (it.wait) {
+        const uint32_t F = s_F[r.item], wait_id = s_wait[r.item];
+        if (wait_id) {
           const uint64_t t0 = globaltimer_ns();
-          while ((int32_t)(ld_acquire_u32(a.copies_done) - it.wait) < 0) {
+          while ((int32_t)(ld_acquire_u32(a.copies_done) - wait_id) < 0) {
             __nanosleep(128);
             if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 1u); break; }
           }
           if (a.tl && c == 0) a.tl[1] = globaltimer_ns();
           fence_proxy_async_global();
         }
-        const unsigned char* w = reinterpret_cast<const unsigned char*>(it.w);
+        const unsigned char* w = s_w[r.item];
         if (r.kind == 0) {
           const unsigned char* src = w + ((size_t)r.idx * nkb + r.s0) * kUmA;
           const uint32_t xb = Nx * 128;
@@ -350,12 +370,8 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
       const UmRec r = recs[j];
       if (r.kind == 2) break;
       const uint32_t b = u & 1;
-      const Item& it = a.plan->items[r.item];
       // combine weight of every token column (0: not routed to this item)
-      float wl = 0.f;
-      const uint32_t nt = it.n_tok;
-      for (uint32_t t = 0; t < nt; ++t)
-        if (it.tok[t] == (uint32_t)lane) wl = it.wt[t];
+      const float wl = (uint32_t)lane < B ? s_wv[r.item * B + lane] : 0.f;
       mbar_wait(&tfull_bar[b], (u >> 1) & 1);
       um_fence_after();
       const uint32_t ta = tmem + ((q * 32) << 16) + b * 64;
@@ -546,7 +562,7 @@ struct UmLaunch {
   uint32_t Nx, Bp, stages, stage_bytes, KS, dn_st;
   size_t smem;
 };
-inline UmLaunch umma_launch_config(uint32_t B, uint32_t d) {
+inline UmLaunch umma_launch_config(uint32_t B, uint32_t d, uint32_t max_items) {
   UmLaunch L{};
   // ~16 x 32 KB stages per gate_up unit, <= 4 per down unit: enough units to
   // spread a few experts over every SM with a short tail
@@ -563,9 +579,10 @@ inline UmLaunch umma_launch_config(uint32_t B, uint32_t d) {
   L.Bp = (B + 7) / 8 * 8;
   const uint32_t bmax = std::max(L.Nx * 128, 2 * (2 * L.Bp) * 128);
   L.stage_bytes = (kUmA + bmax + 1023) / 1024 * 1024;
-  const size_t budget = 224 * 1024 - 1024;  // + 1 KB alignment slack
+  const size_t wv = (size_t)max_items * B * 4;  // per-item token combine weights
+  const size_t budget = 224 * 1024 - 1024 - wv;  // + 1 KB alignment slack
   L.stages = (uint32_t)std::min<size_t>(kUmMaxStages, budget / L.stage_bytes);
-  L.smem = (size_t)L.stages * L.stage_bytes + 1024;
+  L.smem = (size_t)L.stages * L.stage_bytes + 1024 + wv;
   if (B < 2 || B > 32) L.stages = 0;
   return L;
 }

@@ -1168,7 +1168,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   int sms = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   if (S->umma) {
-    S->um = umma_launch_config(B, d);
+    S->um = umma_launch_config(B, d, 1 + std::min(E, B * cfg.top_k));
     S->xt.alloc((size_t)(d / 64) * S->um.Nx * 64);
     S->xt.zero(s);  // token rows >= B stay zero
     const uint64_t n_exp = std::min<uint64_t>(E, (uint64_t)B * cfg.top_k);
