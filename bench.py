@@ -214,6 +214,69 @@ def open_shared_pool(capi, local, torch, dist, coll_dev):
     return info
 
 
+def batched_section(capi, torch, local, hbm_peak, batches=(8, 32), n_warm=8, n_timed=32):
+    """Config C5 (independent decode streams, DeepSeek-V2-Lite shape) at
+    batch B on one GPU: the batched tensor-core FFN (ffn_umma.cuh). Per B:
+    ms/step and tokens/s with the 16/64 cache (PCIe uploads), and the FFN
+    kernel's HBM roofline on the all-resident configuration (CUDA events
+    around every FFN launch, algorithmic bytes = every selected expert's
+    weights once)."""
+    L, E, d = CFG["num_layers"], CFG["experts"], MODEL["d_model"]
+    T = n_warm + n_timed
+    out = {}
+    pool = None  # the UMMA-tiled host pool, generated once, shared by every batched stack
+    for B in batches:
+        scores = capi.generate_trace(L, E, B, T, 7)
+        logits = capi.trace_logits(scores)
+        x = torch.from_numpy(ar1_hidden(T, B, d, 7)).to(torch.bfloat16).cuda()
+        y = torch.empty((B, d), dtype=torch.bfloat16, device="cuda")
+        row = {}
+        for allhit in (False, True):
+            cfg = capi.Config.make(**dict(CFG, batch=B, slots=E if allhit else CFG["slots"]))
+            kw = dict(time_kernels=allhit)
+            if pool is not None:
+                kw["weights_host"] = pool
+            st = capi.Stack(cfg, weight_seed=7, device=local, **kw, **MODEL)
+            if pool is None:
+                pool = (st.host_pool()[0], st)
+            st.set_logits_trace(logits, T)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for i in range(n_warm):
+                    st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+                st.sync()
+                m0 = st.metrics()
+                st.reset_kernel_stats()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                for i in range(n_warm, T):
+                    st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+                e1.record(s)
+                e1.synchronize()
+                st.sync()
+            ms = e0.elapsed_time(e1) / n_timed
+            m1 = st.metrics()
+            if allhit:
+                k = st.kernel_stats()
+                gbs = k["ffn_bytes"] / (k["ffn_ms"] * 1e-3) / 1e9
+                row["all_resident"] = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B * 1e3 / ms, 1),
+                                       "ffn_us_per_launch": round(k["ffn_ms"] * 1e3 / max(k["ffn_launches"], 1), 2),
+                                       "ffn_mb_per_launch": round(k["ffn_bytes"] / max(k["ffn_launches"], 1) / 1e6, 1),
+                                       "ffn_achieved_gbs": round(gbs, 1), "ffn_frac": round(gbs / hbm_peak, 4)}
+            else:
+                sel = m1["selections"] - m0["selections"]
+                row["cache_16_of_64"] = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B * 1e3 / ms, 1),
+                                         "hit_rate": round((m1["hits"] - m0["hits"]) / max(sel, 1), 4)}
+            if st is not pool[1]:
+                st.close()
+        out[f"B{B}"] = row
+    pool[1].close()
+    out["note"] = ("config C5 shape, one GPU, steps " + str(n_timed) + " after " + str(n_warm) +
+                   " warm-up; FFN = tcgen05 kernel (UMMA-tiled experts); per-launch CUDA events "
+                   "(no PDL overlap in the all-resident pass)")
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -493,11 +556,16 @@ def run_ours(args):
     }
     if abl:
         result["ablation"] = abl
+    if rank == 0 and world == 1 and not args.no_batched:
+        stack.close()
+        stack = None
+        result["batched_c5"] = batched_section(capi, torch, local, hbm_peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(scores, x_host, args.cpu_sample_tokens)
     torch.cuda.synchronize()
     del x_pin, y_pin
-    stack.close()
+    if stack is not None:
+        stack.close()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
@@ -634,6 +702,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-ablation", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batched", action="store_true", help="skip the batched (config C5) tensor-core FFN section")
     ap.add_argument("--cpu-sample-tokens", type=int, default=12)
     args = ap.parse_args()
     if args.warmup < 3:
