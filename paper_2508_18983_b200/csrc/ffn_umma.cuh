@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
         } else {
           // h of the item: every gate_up unit must have landed
           wait_ctr_ge(&a.ctr[r.item], F / 128, 8u);
+          if (a.tl) atomicCAS(reinterpret_cast<unsigned long long*>(a.tl + 10), 0ull, (unsigned long long)globaltimer_ns());
           fence_proxy_async_global();
           const unsigned char* src = w + 2 * (size_t)F * d * 2 + ((size_t)r.idx * (F / 128) + r.s0) * kUmA;
           const uint32_t hb = 2 * Ndn * 128;
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
           __threadfence();
           atomicAdd(&a.ctr[r.item], 1u);
           mbar_arrive(&rempty_bar[j]);
+          if (a.tl) atomicMax(reinterpret_cast<unsigned long long*>(a.tl + 9), (unsigned long long)globaltimer_ns());
         }
       } else {
         float vh[32], vl[32];  // hi / lo columns of every token
@@ -481,6 +483,11 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
     if (et == 0) {
       __threadfence();
       atomicAdd(&a.ctr[kUmDoneCtr], 1u);
+      if (a.tl) {  // first and last CTA done with their units
+        const unsigned long long now = globaltimer_ns();
+        atomicCAS(reinterpret_cast<unsigned long long*>(a.tl + 14), 0ull, now);
+        atomicMax(reinterpret_cast<unsigned long long*>(a.tl + 13), now);
+      }
     }
   }
   __syncthreads();

@@ -142,9 +142,30 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
   const int lane = lane_id(), warp = warp_id();
   const uint32_t d = a.d, B = a.B;
   const uint32_t nvec = d / 8;
+  // x -> shared memory once, 8 independent 16 B loads in flight per thread
+  // (a strided one-load-per-iteration loop is L2-latency-bound at B = 32)
+  {
+    const uint32_t n = B * nvec;
+    const uint4* xg = reinterpret_cast<const uint4*>(a.x);
+    uint4* xs = reinterpret_cast<uint4*>(us);
+    for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+      uint4 v[8];
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j) {
+        const uint32_t i = i0 + j * blockDim.x;
+        if (i < n) v[j] = xg[i];
+      }
+#pragma unroll
+      for (uint32_t j = 0; j < 8; ++j) {
+        const uint32_t i = i0 + j * blockDim.x;
+        if (i < n) xs[i] = v[j];
+      }
+    }
+  }
+  __syncthreads();
   // RMSNorm (eps 1e-6, unit weight): one warp per token
   for (uint32_t t = warp; t < B; t += kGateThreads / 32) {
-    const uint4* xv = reinterpret_cast<const uint4*>(a.x + (size_t)t * d);
+    const uint4* xv = reinterpret_cast<const uint4*>(us + (size_t)t * d);
     float ss = 0.f;
     for (uint32_t c = lane; c < nvec; c += 32) {
       const uint4 v = xv[c];
@@ -156,7 +177,7 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < B * nvec; i += blockDim.x) {
     const uint32_t t = i / nvec, c = i % nvec;
-    const uint4 v = reinterpret_cast<const uint4*>(a.x + (size_t)t * d)[c];
+    const uint4 v = reinterpret_cast<const uint4*>(us + (size_t)t * d)[c];
     const float r = inv_rms[t];
     const uint32_t in[4] = {v.x, v.y, v.z, v.w};
     uint32_t o[4];
