@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   // per item (plan order): first gate_up unit, first down unit, first tile,
   // first down partial
   __shared__ uint32_t s_gu0[kMaxItems + 1], s_dn0[kMaxItems + 1], s_tb[kMaxItems + 1], s_pb[kMaxItems + 1];
-  __shared__ uint32_t s_total, s_ni, s_last;
+  __shared__ uint32_t s_ngu[kMaxItems + 1], s_ndn[kMaxItems + 1];
+  __shared__ uint32_t s_ni, s_last;
   __shared__ uint32_t s_F[kMaxItems], s_wait[kMaxItems];
   __shared__ const unsigned char* s_w[kMaxItems];
 
@@ -190,96 +191,96 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     um_fence_before();
   }
-  // PDL: plan, u and x_in come from the kernels launched before
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  {
-    // the plan's item table -> shared memory (parallel loads): F, weights,
-    // upload dependency, and each item's combine weight per token column
-    const uint32_t ni = a.plan->n_items;
-    for (uint32_t i = threadIdx.x; i < ni; i += blockDim.x) {
-      s_F[i] = a.plan->items[i].F;
-      s_wait[i] = a.plan->items[i].wait;
-      s_w[i] = reinterpret_cast<const unsigned char*>(a.plan->items[i].w);
-    }
-    for (uint32_t i = threadIdx.x; i < ni * B; i += blockDim.x) s_wv[i] = 0.f;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < ni * kMaxB; i += blockDim.x) {
-      const Item& it = a.plan->items[i / kMaxB];
-      const uint32_t jt = i % kMaxB;
-      if (jt < it.n_tok) s_wv[(i / kMaxB) * B + it.tok[jt]] = it.wt[jt];
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // unit sequence: [gate_up of the ready items][down of the ready items]
-    // then per waiting item [gate_up][down]. An item has F/128 tiles x KS
-    // gate_up units (tile-major) and d/128 row tiles x DS down units, DS =
-    // ceil(tiles / dn_st).
-    const uint32_t ni = a.plan->n_items, nr = a.plan->n_ready;
-    uint32_t tb = 0, pb = 0;
-    for (uint32_t i = 0; i < ni; ++i) {
-      s_tb[i] = tb;
-      s_pb[i] = pb;
-      const uint32_t t = s_F[i] / 128;
-      tb += t;
-      pb += (t + dn_st - 1) / dn_st;
-    }
-    s_tb[ni] = tb;
-    s_pb[ni] = pb;
-    uint32_t acc = 0;
-    for (uint32_t i = 0; i < nr; ++i) {
-      s_gu0[i] = acc;
-      acc += (s_tb[i + 1] - s_tb[i]) * KS;
-    }
-    for (uint32_t i = 0; i < nr; ++i) {
-      s_dn0[i] = acc;
-      acc += nm * (s_pb[i + 1] - s_pb[i]);
-    }
-    for (uint32_t i = nr; i < ni; ++i) {
-      s_gu0[i] = acc;
-      acc += (s_tb[i + 1] - s_tb[i]) * KS;
-      s_dn0[i] = acc;
-      acc += nm * (s_pb[i + 1] - s_pb[i]);
-    }
-    s_total = acc;
-    s_ni = ni;
-    if (a.tl && c == 0) a.tl[0] = globaltimer_ns();
-  }
-  __syncthreads();
+  __syncthreads();  // barriers initialised, TMEM allocated
   um_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t total = s_total, ni_all = s_ni;
+  // Speculative start (the decide kernel publishes the shared expert and
+  // the experts certain to be selected right after classification): their
+  // gate_up units run while the decision finishes — gate_up does not depend
+  // on the token lists (every token column is computed; the combine weights
+  // are applied per column in the down epilogue). The final plan lists them
+  // first, in the same order, and is taken from the decide kernel's release
+  // flag. Without a speculative plan: PDL wait for the decide kernel.
+  const bool spec = a.spec_plan != nullptr;
+  if (!spec) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      const uint64_t pol = l2_evict_first_policy(), pol_keep = l2_evict_last_policy();
-      uint32_t k = 0;
-      uint32_t nxt = atomicAdd(&a.ctr[kFfnGuCtr], 1u);
-      for (uint32_t u = 0;; ++u) {
+    // warp 0 stages the item tables (all lanes); lane 0 streams the units
+    const uint64_t pol = l2_evict_first_policy(), pol_keep = l2_evict_last_policy();
+    uint32_t k = 0, u = 0;  // ring step, unit record count
+    auto load_items = [&](const Plan* pl, uint32_t i0, uint32_t i1) {
+      for (uint32_t i = i0 + lane; i < i1; i += 32) {
+        s_F[i] = __ldcg(&pl->items[i].F);
+        s_wait[i] = __ldcg(&pl->items[i].wait);
+        s_w[i] = reinterpret_cast<const unsigned char*>(
+            __ldcg(reinterpret_cast<const unsigned long long*>(&pl->items[i].w)));
+      }
+    };
+    // unit tables of items [0, ni): gate_up units of items >= g0 (and of
+    // every item when gu_only), down units unless gu_only
+    auto build = [&](uint32_t ni, uint32_t nr, uint32_t g0, bool gu_only) -> uint32_t {
+      uint32_t tb = 0, pb = 0;
+      for (uint32_t i = 0; i < ni; ++i) {
+        s_tb[i] = tb;
+        s_pb[i] = pb;
+        const uint32_t t = s_F[i] / 128;
+        tb += t;
+        pb += (t + dn_st - 1) / dn_st;
+      }
+      s_tb[ni] = tb;
+      s_pb[ni] = pb;
+      uint32_t acc = 0;
+      // [gate_up of the ready items][down of the ready items], then per
+      // waiting item [gate_up][down]
+      for (uint32_t i = 0; i < nr; ++i) {
+        s_gu0[i] = acc;
+        s_ngu[i] = i >= g0 ? (s_tb[i + 1] - s_tb[i]) * KS : 0u;
+        acc += s_ngu[i];
+      }
+      for (uint32_t i = 0; i < nr; ++i) {
+        s_dn0[i] = acc;
+        s_ndn[i] = gu_only ? 0u : nm * (s_pb[i + 1] - s_pb[i]);
+        acc += s_ndn[i];
+      }
+      for (uint32_t i = nr; i < ni; ++i) {
+        s_gu0[i] = acc;
+        s_ngu[i] = (s_tb[i + 1] - s_tb[i]) * KS;
+        acc += s_ngu[i];
+        s_dn0[i] = acc;
+        s_ndn[i] = nm * (s_pb[i + 1] - s_pb[i]);
+        acc += s_ndn[i];
+      }
+      return acc;
+    };
+    auto publish = [&](const UmRec& r) {
+      const uint32_t j = u % kUmRec;
+      mbar_wait(&rempty_bar[j], ((u / kUmRec) & 1) ^ 1);
+      recs[j] = r;
+      mbar_arrive(&rfull_bar[j]);
+      ++u;
+    };
+    // units [0, total) of the current tables, grabbed from counter ctr_i
+    auto run_units = [&](uint32_t ctr_i, uint32_t total, uint32_t ni) {
+      uint32_t nxt = atomicAdd(&a.ctr[ctr_i], 1u);
+      while (nxt < total) {
         const uint32_t unit = nxt;
-        if (unit < total) nxt = atomicAdd(&a.ctr[kFfnGuCtr], 1u);
-        const uint32_t j = u % kUmRec;
-        mbar_wait(&rempty_bar[j], ((u / kUmRec) & 1) ^ 1);
+        nxt = atomicAdd(&a.ctr[ctr_i], 1u);
         UmRec r{2u, 0u, 0u, 0u, 0u, 0u};
-        if (unit < total) {
-          for (uint32_t i = 0; i < ni_all; ++i) {
+        for (uint32_t i = 0; i < ni; ++i) {
+          if (unit - s_gu0[i] < s_ngu[i]) {
+            const uint32_t q = unit - s_gu0[i];
+            r = UmRec{0u, i, q / KS, q % KS, (q % KS) * kst, kst};
+            break;
+          }
+          if (unit - s_dn0[i] < s_ndn[i]) {
             const uint32_t tiles = s_tb[i + 1] - s_tb[i], DS = s_pb[i + 1] - s_pb[i];
-            if (unit >= s_gu0[i] && unit < s_gu0[i] + tiles * KS) {
-              const uint32_t q = unit - s_gu0[i];
-              r = UmRec{0u, i, q / KS, q % KS, (q % KS) * kst, kst};
-              break;
-            }
-            if (unit >= s_dn0[i] && unit < s_dn0[i] + nm * DS) {
-              const uint32_t q = unit - s_dn0[i], ds = q % DS;
-              r = UmRec{1u, i, q / DS, ds, ds * dn_st, min(dn_st, tiles - ds * dn_st)};
-              break;
-            }
+            const uint32_t q = unit - s_dn0[i], ds = q % DS;
+            r = UmRec{1u, i, q / DS, ds, ds * dn_st, min(dn_st, tiles - ds * dn_st)};
+            break;
           }
         }
-        recs[j] = r;
-        mbar_arrive(&rfull_bar[j]);
-        if (r.kind == 2) break;
+        publish(r);
         const uint32_t F = s_F[r.item], wait_id = s_wait[r.item];
         if (wait_id) {
           const uint64_t t0 = globaltimer_ns();
@@ -320,6 +321,51 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
           }
         }
       }
+    };
+    uint32_t n_spec = 0;
+    if (spec) {
+      if (lane == 0) {
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_u32(a.spec_flag) != a.seq) {
+          __nanosleep(64);
+          if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 5u); break; }
+        }
+        if (a.tl && c == 0) a.tl[6] = globaltimer_ns();
+      }
+      __syncwarp();
+      n_spec = ld_acquire_u32(&a.spec_plan->n_spec);
+      load_items(a.spec_plan, 0, n_spec);
+      __syncwarp();
+      if (lane == 0) {
+        fence_proxy_async_global();  // the activation tiles (gate phase) are read by bulk copies
+        const uint32_t tot = build(n_spec, n_spec, 0, true);
+        run_units(kFfnSpecGuCtr, tot, n_spec);
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_u32(a.spec_flag + 1) != a.seq) {
+          __nanosleep(32);
+          if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 6u); break; }
+        }
+      }
+      __syncwarp();
+    }
+    // the final plan: items, and each item's combine weight per token column
+    const uint32_t ni = ld_acquire_u32(&a.plan->n_items), nr = __ldcg(&a.plan->n_ready);
+    load_items(a.plan, n_spec, ni);
+    for (uint32_t i = lane; i < ni * B; i += 32) s_wv[i] = 0.f;
+    __syncwarp();
+    for (uint32_t i = lane; i < ni * kMaxB; i += 32) {
+      const Item& it = a.plan->items[i / kMaxB];
+      const uint32_t jt = i % kMaxB;
+      if (jt < __ldcg(&it.n_tok)) s_wv[(i / kMaxB) * B + __ldcg(&it.tok[jt])] = __ldcg(&it.wt[jt]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (a.tl && c == 0) a.tl[0] = globaltimer_ns();
+      fence_proxy_async_global();
+      const uint32_t tot = build(ni, nr, n_spec, false);
+      s_ni = ni;
+      run_units(kFfnGuCtr, tot, ni);
+      publish(UmRec{2u, 0u, 0u, 0u, 0u, 0u});
     }
   } else if (warp == 1) {
     // ----------------------------------------------------------- MMA issuer
@@ -371,8 +417,6 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
       const UmRec r = recs[j];
       if (r.kind == 2) break;
       const uint32_t b = u & 1;
-      // combine weight of every token column (0: not routed to this item)
-      const float wl = (uint32_t)lane < B ? s_wv[r.item * B + lane] : 0.f;
       mbar_wait(&tfull_bar[b], (u >> 1) & 1);
       um_fence_after();
       const uint32_t ta = tmem + ((q * 32) << 16) + b * 64;
@@ -439,9 +483,10 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
 #pragma unroll
         for (uint32_t n = 0; n < 32; ++n) {
           if (n >= Bp) break;
-          const float wn = __shfl_sync(0xffffffffu, wl, n);
+          // token columns >= B (padding) stay 0; the combine weight is
+          // applied per column in the down epilogue
           float h = 0.f;
-          if (n < Nx) h = wn * (g[n] / (1.f + __expf(-g[n]))) * up[n];
+          if (n < B) h = (g[n] / (1.f + __expf(-g[n]))) * up[n];
           const uint16_t hi = f32_to_bf16_rne(h);
           const uint16_t lo = f32_to_bf16_rne(h - bf2f(hi));
           *reinterpret_cast<uint16_t*>(hb + sw128_off(n, col)) = hi;
@@ -472,7 +517,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
 #pragma unroll
         for (uint32_t n = 0; n < 32; ++n) {
           if (n >= B) break;
-          pp[(size_t)n * d] = vh[n] + vl[n];
+          pp[(size_t)n * d] = s_wv[r.item * B + n] * (vh[n] + vl[n]);
         }
         asm volatile("bar.sync 2, 128;" ::: "memory");
         if (et == 0) mbar_arrive(&rempty_bar[j]);

@@ -307,7 +307,11 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   if (!a.spec_plan) return;
   const DevCfg& cfg = sm->cfg;
   const LayerState* ls = &sm->ls;
-  const uint64_t certain = (cfg.er ? d->top[0] : d->act[0]) & ls->mask;
+  // batch: the union over the tokens (an expert no token ends up selecting
+  // stays in the final plan with no tokens: zero combine weights)
+  uint64_t certain = 0;
+  for (uint32_t t = 0; t < cfg.B; ++t) certain |= cfg.er ? d->top[t] : d->act[t];
+  certain &= ls->mask;
   Plan* sp = a.spec_plan;
   uint32_t n = 0;
   auto item = [&](const uint16_t* w, uint32_t F, uint32_t kind, uint32_t e, float wt) {
@@ -1138,7 +1142,9 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   reset_state(S, s);
   S->plan.alloc(1);
   // speculative FFN start (batch 1, combine weights known at classification)
-  S->spec = B == 1 && !m.renormalize && getenv("MOEB_NO_SPEC") == nullptr;
+  // (the batched tcgen05 FFN takes the combine weights from the final plan,
+  // so it also runs with renormalised weights)
+  S->spec = ((B == 1 && !m.renormalize) || S->umma) && getenv("MOEB_NO_SPEC") == nullptr;
   if (S->spec) {
     S->spec_plan.alloc(1);
     S->spec_flag.alloc(2);  // [0] speculative plan published, [1] final plan published
