@@ -152,6 +152,22 @@ __device__ inline void record_scores_warp(LayerState* ls, double* hist_l, uint32
   __syncwarp();
 }
 
+// Warp-wide: lane t < B holds token t's selection mask; cnt[e] = number of
+// tokens selecting e (masks exchanged through shared memory: B reads per lane).
+__device__ inline void batch_counts(uint64_t m, uint32_t B, uint32_t E, uint16_t* cnt) {
+  __shared__ uint64_t s_selm[kMaxB];
+  const uint32_t lane = lane_id();
+  __syncwarp();
+  if (lane < B) s_selm[lane] = m;
+  __syncwarp();
+  for (uint32_t e = lane; e < E; e += 32) {
+    uint32_t c = 0;
+    for (uint32_t t = 0; t < B; ++t) c += (uint32_t)(s_selm[t] >> e) & 1u;
+    cnt[e] = (uint16_t)c;
+  }
+  __syncwarp();
+}
+
 // --------------------------------------------------------- router parts
 // router.cpp:114-149: pass 2 for token t (executed by one lane).
 __device__ inline void route_token(DecideSmem* sm, uint32_t t, uint64_t resident, uint32_t E,
@@ -202,11 +218,14 @@ __device__ inline void route_token(DecideSmem* sm, uint32_t t, uint64_t resident
 __device__ inline void coalesce_warp(DecideSmem* sm, uint32_t B, uint32_t E, uint32_t k,
                                      uint64_t resident, uint16_t* cnt) {
   const int lane = lane_id();
-  for (uint32_t e = lane; e < E; e += 32) cnt[e] = 0;
-  __syncwarp();
-  if (lane == 0)
-    for (uint32_t t = 0; t < B; ++t)
-      for (uint32_t i = 0; i < sm->nsel[t]; ++i) cnt[sm->sel[t][i]]++;
+  // batch counts: a token's selection is a set, so cnt[e] = number of
+  // tokens (lanes, B <= 32) whose selection mask holds e
+  {
+    uint64_t m = 0;
+    if ((uint32_t)lane < B)
+      for (uint32_t i = 0; i < sm->nsel[lane]; ++i) m |= bit(sm->sel[lane][i]);
+    batch_counts(m, B, E, cnt);
+  }
   __syncwarp();
   bool changed = true;
   while (changed) {
@@ -601,23 +620,22 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   if (warp != 0) return;  // the rest is order-dependent: warp 0 in lock-step
 
   // ---- hit accounting + batch_of (pipeline.cpp:176-189)
-  for (uint32_t e = lane; e < E; e += 32) sc->cnt[e] = 0;
-  __syncwarp();
+  // lane t <-> token t (B <= 32): selection masks, counts by ballot
   uint64_t n_sel_total = 0, n_hits = 0, n_subs = 0, n_kept = 0;
-  for (uint32_t t = 0; t < B; ++t) {
-    for (uint32_t i = 0; i < sm->nsel[t]; ++i) {
-      const uint32_t e = sm->sel[t][i];
-      n_sel_total++;
-      n_hits += has(mask, e);
+  {
+    uint64_t m = 0;
+    uint32_t ns = 0, nb = 0, nk = 0;
+    if ((uint32_t)lane < B) {
+      ns = sm->nsel[lane];
+      for (uint32_t i = 0; i < ns; ++i) m |= bit(sm->sel[lane][i]);
+      nb = sm->nsub[lane];
+      nk = sm->nkept[lane];
     }
-    n_subs += sm->nsub[t];
-    n_kept += sm->nkept[t];
-  }
-  for (uint32_t e = lane; e < E; e += 32) {
-    uint32_t c = 0;
-    for (uint32_t t = 0; t < B; ++t)
-      for (uint32_t i = 0; i < sm->nsel[t]; ++i) c += sm->sel[t][i] == e;
-    sc->cnt[e] = (uint16_t)c;
+    n_sel_total = __reduce_add_sync(0xffffffffu, ns);
+    n_hits = __reduce_add_sync(0xffffffffu, (uint32_t)__popcll(m & mask));
+    n_subs = __reduce_add_sync(0xffffffffu, nb);
+    n_kept = __reduce_add_sync(0xffffffffu, nk);
+    batch_counts(m, B, E, sc->cnt);
   }
   // mean over tokens in token order (pipeline.cpp:79-91)
   for (uint32_t e = lane; e < E; e += 32) {

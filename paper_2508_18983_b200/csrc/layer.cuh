@@ -207,12 +207,40 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
     const uint16_t* w = row < a.E ? a.wg + (size_t)row * d : a.wsg;
     const uint4* wv = reinterpret_cast<const uint4*>(w);
     const uint32_t c0 = q * (nvec / 4), c1 = (q + 1) * (nvec / 4);
-    for (uint32_t t = 0; t < B; ++t) {
-      const uint4* uv = reinterpret_cast<const uint4*>(us + (size_t)t * d);
-      float s = 0.f;
-      for (uint32_t c = c0 + lane; c < c1; c += 32) s += dot8(__ldg(wv + c), uv[c]);
-      s = warp_sum(s);
-      if (lane == 0) part[q][warp & 1][t] = s;
+    if (B <= 4 || nvec / 4 != 64) {
+      for (uint32_t t = 0; t < B; ++t) {
+        const uint4* uv = reinterpret_cast<const uint4*>(us + (size_t)t * d);
+        float s = 0.f;
+        for (uint32_t c = c0 + lane; c < c1; c += 32) s += dot8(__ldg(wv + c), uv[c]);
+        s = warp_sum(s);
+        if (lane == 0) part[q][warp & 1][t] = s;
+      }
+    } else {
+      // d = 2048: the lane's two weight vectors stay in registers; per-lane
+      // partial dots of all tokens, then one transposed butterfly (31
+      // shuffles for 32 tokens instead of 5 per token): lane t ends with
+      // token t's sum
+      const uint4 w0 = __ldg(wv + c0 + lane), w1 = __ldg(wv + c0 + 32 + lane);
+      float p[32];
+#pragma unroll
+      for (uint32_t t = 0; t < 32; ++t) {
+        p[t] = 0.f;
+        if (t < B) {
+          const uint4* uv = reinterpret_cast<const uint4*>(us + (size_t)t * d);
+          p[t] = dot8(w0, uv[c0 + lane]) + dot8(w1, uv[c0 + 32 + lane]);
+        }
+      }
+#pragma unroll
+      for (uint32_t o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (uint32_t i = 0; i < o; ++i) {
+          const float send = up ? p[i] : p[i + o];
+          const float keep = up ? p[i + o] : p[i];
+          p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      if ((uint32_t)lane < B) part[q][warp & 1][lane] = p[0];
     }
   }
   __syncthreads();
