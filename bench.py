@@ -237,6 +237,12 @@ def batched_section(capi, torch, local, hbm_peak, batches=(8, 32), n_warm=8, n_t
             allhit = mode != "cache"
             cfg = capi.Config.make(**dict(CFG, batch=B, slots=E if allhit else CFG["slots"]))
             kw = dict(time_kernels=mode == "allhit_events")
+            # the event pass times the FFN standalone: no speculative phase
+            # (events serialise the launches, nothing to overlap with)
+            if mode == "allhit_events":
+                os.environ["MOEB_NO_SPEC"] = "1"
+            else:
+                os.environ.pop("MOEB_NO_SPEC", None)
             if pool is not None:
                 kw["weights_host"] = pool
             st = capi.Stack(cfg, weight_seed=7, device=local, **kw, **MODEL)
@@ -275,6 +281,7 @@ def batched_section(capi, torch, local, hbm_peak, batches=(8, 32), n_warm=8, n_t
             if st is not pool[1]:
                 st.close()
         out[f"B{B}"] = row
+    os.environ.pop("MOEB_NO_SPEC", None)
     pool[1].close()
     out["note"] = ("config C5 shape, one GPU, steps " + str(n_timed) + " after " + str(n_warm) +
                    " warm-up; FFN = tcgen05 kernel (UMMA-tiled experts); ms_per_step = the PDL "

@@ -23,12 +23,12 @@
 // Work units (grid-dynamic, one atomic grab per unit):
 //   gate_up (item, u): 32 KB stages over d/64 K-blocks; two accumulators
 //     (gate, up: N = Nx columns each); the epilogue thread of TMEM lane j owns
-//     intermediate row j of the unit: h = w_tok * silu(g) * up for every
+//     intermediate row j of the unit: h = silu(g) * up for every
 //     token column, split into bf16 hi + lo (h = hi + lo to 2^-17), stored as
 //     the down pass's B operand ([K-block][2 Bp rows][128 B], SW128).
 //   down (item, m): 32 KB weight stage + the item's h K-pair (from L2), one
 //     accumulator of N = 2 Bp columns (hi rows, lo rows); the epilogue writes
-//     the item's partial y[tok][row] (hi + lo) to part[item].
+//     the item's partial w_tok * (hi + lo) to part[item, split].
 // A down unit waits for its item's gate_up units (per-item grid counter).
 // Items whose weights are still on the PCIe copy stream are gated on
 // copies_done by the producer. End: grid barrier, each CTA sums its output
@@ -117,6 +117,11 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// store kept in L2 (evict_last): the down partials are read back by the
+// final sum after the rest of the weight stream has passed through L2
+__device__ __forceinline__ void st_keep(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void um_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -201,6 +206,9 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   // are applied per column in the down epilogue). The final plan lists them
   // first, in the same order, and is taken from the decide kernel's release
   // flag. Without a speculative plan: PDL wait for the decide kernel.
+  // (Running the speculative items' down units early as well, with the
+  // weights moved to the final sum, measured no faster in the pipeline and
+  // slower standalone.)
   const bool spec = a.spec_plan != nullptr;
   if (!spec) asm volatile("griddepcontrol.wait;" ::: "memory");
 
@@ -217,8 +225,8 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
             __ldcg(reinterpret_cast<const unsigned long long*>(&pl->items[i].w)));
       }
     };
-    // unit tables of items [0, ni): gate_up units of items >= g0 (and of
-    // every item when gu_only), down units unless gu_only
+    // unit tables of items [0, ni): gate_up units of items >= g0, down
+    // units unless gu_only
     auto build = [&](uint32_t ni, uint32_t nr, uint32_t g0, bool gu_only) -> uint32_t {
       uint32_t tb = 0, pb = 0;
       for (uint32_t i = 0; i < ni; ++i) {
@@ -410,6 +418,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   } else {
     // ------------------------------------------------------------- epilogue
     const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint64_t pol_part = l2_evict_last_policy();
     const uint32_t et = (warp - 2) * 32 + lane;
     for (uint32_t u = 0;; ++u) {
       const uint32_t j = u % kUmRec;
@@ -517,7 +526,7 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
 #pragma unroll
         for (uint32_t n = 0; n < 32; ++n) {
           if (n >= B) break;
-          pp[(size_t)n * d] = s_wv[r.item * B + n] * (vh[n] + vl[n]);
+          st_keep(pp + (size_t)n * d, s_wv[r.item * B + n] * (vh[n] + vl[n]), pol_part);
         }
         asm volatile("bar.sync 2, 128;" ::: "memory");
         if (et == 0) mbar_arrive(&rempty_bar[j]);
@@ -543,35 +552,32 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
   __syncthreads();
   // epilogue: y[tok][row] = sum over the items in plan order, residual
   {
-    uint32_t dlo, dhi;
-    share(d, c, G, dlo, dhi);
-    const uint32_t rows = dhi - dlo, np = s_pb[s_ni];
-    for (uint32_t i = threadIdx.x; i < rows * B; i += blockDim.x) {
-      const uint32_t t = i / rows, o = dlo + i % rows;
+    // CTA c owns a contiguous range of the flattened [B][d] outputs: every
+    // warp load is one 128 B line of a partial
+    uint32_t lo, hi;
+    share(B * d, c, G, lo, hi);
+    const uint32_t np = s_pb[s_ni];
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const uint32_t t = i / d, o = i % d;
       const float* pp = ua.part + (size_t)t * d + o;
-      // 16 partials in flight per thread, summed in plan order
+      const float xin = bf2f(a.x_in[(size_t)t * d + o]);  // issued before the partials
+      // partials in plan order, 32 loads in flight (branch-free: indices past
+      // the end reload the last partial and are not added)
       float y = 0.f;
-      uint32_t it = 0;
-      for (; it + 16 <= np; it += 16) {
-        float v[16];
+      for (uint32_t it = 0; it < np; it += 32) {
+        float v[32];
 #pragma unroll
-        for (uint32_t q2 = 0; q2 < 16; ++q2) v[q2] = __ldcg(pp + (size_t)(it + q2) * B * d);
+        for (uint32_t q2 = 0; q2 < 32; ++q2) v[q2] = __ldcg(pp + (size_t)min(it + q2, np - 1) * B * d);
 #pragma unroll
-        for (uint32_t q2 = 0; q2 < 16; ++q2) y += v[q2];
-      }
-      {
-        float v[16];
-#pragma unroll
-        for (uint32_t q2 = 0; q2 < 16; ++q2) v[q2] = it + q2 < np ? __ldcg(pp + (size_t)(it + q2) * B * d) : 0.f;
-#pragma unroll
-        for (uint32_t q2 = 0; q2 < 16; ++q2)
+        for (uint32_t q2 = 0; q2 < 32; ++q2)
           if (it + q2 < np) y += v[q2];
       }
-      const float xo = bf2f(a.x_in[(size_t)t * d + o]) + y;
+      const float xo = xin + y;
       a.x_out[(size_t)t * d + o] = f32_to_bf16_rne(xo);
       a.y_out[(size_t)t * d + o] = y;
     }
   }
+  if (a.tl && c == 0 && threadIdx.x == 0) a.tl[8] = globaltimer_ns();  // CTA 0's final sum done
   if (warp == 1) {
     um_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kUmTmemCols));
