@@ -627,6 +627,10 @@ inline UmLaunch umma_launch_config(uint32_t B, uint32_t d, uint32_t max_items) {
   const uint32_t nkb = d / 64;
   L.KS = 1;
   while (L.KS < 8 && nkb % (2 * L.KS) == 0 && nkb / (2 * L.KS) >= 16) L.KS *= 2;
+  // B > 16: more distinct experts (enough units) and twice the split-partial
+  // traffic: no K-split (B200, DSV2-Lite all-resident layer period, B = 32:
+  // KS 1 / 2 / 4 = 128 / 131 / 135 us; B = 8: 70 / 69 / 74 us)
+  if (B > 16) L.KS = 1;
   L.dn_st = 4;
   if (const char* e = getenv("MOEB_UMMA_KS")) {  // tuning knobs
     const uint32_t ks = (uint32_t)atoi(e);
