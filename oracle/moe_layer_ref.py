@@ -14,6 +14,10 @@ Expert choice is NOT recomputed here: the caller passes the device's
 bit-exact decisions (checked separately against oracle/moesched_oracle.c),
 and this module checks the arithmetic given those decisions.
 
+Pinned: tests/test_hf_pin.py runs the installed HF modules (transformers 5.5.0)
+on the same synthetic weights and activations and requires agreement within
+1e-5 relative L2 (observed ~1.5e-7), plus RMSNorm within one bf16 ulp.
+
 Weights are regenerated with the counter hash of
 paper_2508_18983_b200/csrc/weights.cuh (integer arithmetic, bit-exact).
 """
