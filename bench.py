@@ -615,6 +615,7 @@ def cpu_path(scores, x_host, n_tokens, nthreads):
     cm.cpu_moe_layer.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_int]
+    cm.cpu_bytes_touched.restype = C.c_uint64
     seed = 7
 
     def tid(l, e, m):
@@ -652,6 +653,7 @@ def cpu_path(scores, x_host, n_tokens, nthreads):
                 expert(l, e)
     logits = np.zeros(E, dtype=np.float32)
     y = np.zeros(d, dtype=np.float32)
+    cm.cpu_bytes_touched()
     t0 = time.perf_counter()
     for it in sample:
         x = np.ascontiguousarray(x_host[it, 0]).astype(np.float32)
@@ -666,19 +668,21 @@ def cpu_path(scores, x_host, n_tokens, nthreads):
                              xn.ctypes.data, nthreads)
             xb = xn
     arith_s = time.perf_counter() - t0
+    host_gbs = cm.cpu_bytes_touched() / arith_s / 1e9
     ms_token = arith_s * 1e3 / len(sample) + dec_ms_token
     kind = "reference" if use_ref else "port"
     sample_desc = (f"decisions: {'reference simulate() (oracle/_ref)' if use_ref else 'oracle C port'} over all "
                    f"{T} tokens ({dec_ms_token:.3f} ms/token, 1 thread); arithmetic: oracle/cpu_moe.c fp32 over "
                    f"bf16 host weights, last {len(sample)} tokens x {L} layers ({arith_s * 1e3 / len(sample):.1f} "
-                   f"ms/token, {nthreads} threads)")
-    return ms_token, kind, nthreads, sample_desc
+                   f"ms/token, {nthreads} threads, {host_gbs:.1f} GB/s of host weight reads)")
+    return ms_token, kind, nthreads, sample_desc, host_gbs
 
 
 def cpu_baseline(scores, x_host, n_tokens):
     nthreads = os.cpu_count() or 1
-    ms, kind, cores, sample = cpu_path(scores, x_host, n_tokens, nthreads)
-    return {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample}
+    ms, kind, cores, sample, gbs = cpu_path(scores, x_host, n_tokens, nthreads)
+    return {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample,
+            "host_weight_gbs": round(gbs, 1)}
 
 
 def run_reference(args):
@@ -693,7 +697,7 @@ def run_reference(args):
     scores = po.generate_trace(L, E, B, T, 7, use_ref=po.ref() is not None)
     x_host = ar1_hidden(T, B, d, 7)
     nthreads = os.cpu_count() or 1
-    ms, kind, cores, sample = cpu_path(scores, x_host, min(args.cpu_sample_tokens, K), nthreads)
+    ms, kind, cores, sample, gbs = cpu_path(scores, x_host, min(args.cpu_sample_tokens, K), nthreads)
     print(json.dumps({
         "impl": "reference",
         "metric": "MoE decode ms/token + expert cache hit rate, DeepSeek-V2-Lite shape",
@@ -702,7 +706,8 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "fp32 compute over bf16 weights; fp64 decisions", "data": "synthetic",
         "config": {"workload": "DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode, 512-token stream, "
                                "cache 16/64 experts per layer, CE+ER+Pre+BA alpha=0.25"},
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample,
+                         "host_weight_gbs": round(gbs, 1)},
         "e2e": {"value": round(ms, 3), "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -222,12 +222,20 @@ int moeb_set_logits_trace(moeb_stack* s, const float* logits, uint64_t n_steps,
  * x, y: device pointers, bf16 [B][d]; stream: cudaStream_t or NULL (the
  * stack's own stream). Asynchronous; the copy thread issues expert uploads. */
 int moeb_step(moeb_stack* s, const void* x, void* y, uint32_t B, void* stream);
-/* Synchronise the stack's streams. */
+/* Synchronise the stack's streams. A device wait that gave up (a lost
+ * upload, kSpinLimitNs) is reported here once as status 5 and cleared.
+ * Serial mode (MOEB_SERIAL=1, automatic under ncu / nsys / compute-sanitizer):
+ * upload dependencies become stream waits set up by the host after each
+ * decide kernel instead of in-kernel spins, so tools that serialise kernels
+ * see a correct, if slower, pipeline. Steps of different stacks on one
+ * device are ordered on the device (the FFN grids need every SM). */
 int moeb_sync(moeb_stack* s);
 
 /* Decision counters since create (same vocabulary as Metrics, pipeline.hpp:63-78). */
 int moeb_get_metrics(moeb_stack* s, moeb_metrics* m);
-/* Per-step decision records (MOEB_MODEL_LOG_STEPS): JSON array of
+/* Per-step decision records (MOEB_MODEL_LOG_STEPS), cumulative since create
+ * (first 16384 layer-steps; a longer log returns status 4 rather than a
+ * truncated array): JSON array of
  * {"it","layer","mask","tok":[{"sel","sub","kept"}],"load","cpu","pref","evict","completion"}
  * plus the fp32 router scores each step used (for oracle replay). */
 int moeb_get_decisions_json(moeb_stack* s, char** json);
@@ -262,14 +270,17 @@ int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction,
                         double persistence, double concentration, uint64_t iters, uint64_t seed,
                         double* out);
 
-/* Pinned host pool pointer and per-expert bytes (for the CPU oracle). */
 /* Device-clock (ns) timeline of the last <= 16384 layer-steps, 16 words each:
  * 0 FFN start, 1 FFN saw its last upload land (0: none), 2 FFN end,
- * 3 decide entry, 4 uploads published, 5 decide end, 6 FFN has the
- * speculative plan (batch 1), 7 FFN CTA 0 entry, 8 speculative gate_up done,
- * 9 final gate_up done, 10 down pass starts, 11 FFN CTA 0 compute done
- * (8-11: CTA 0). Diagnostics only. */
+ * 3 decide entry, 4 uploads published (mailbox entry A), 5 decide end,
+ * 6 FFN has the speculative plan, 7 FFN CTA 0 entry,
+ * 8 tcgen05 FFN: CTA 0 final sum done (other FFN kernels: unused),
+ * 9 unused, 10 CUDA-core FFN: down pass starts, 11 FFN CTA 0 compute done,
+ * 12 final plan released to the FFN, 13 last FFN CTA compute done (max over
+ * CTAs), 14 split-K FFN: reduction barrier passed, 15 number of uploads the
+ * step published (a count, not a time). Diagnostics only. */
 int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n);
+/* Pinned host pool pointer and per-expert bytes (for the CPU oracle). */
 int moeb_get_host_pool(moeb_stack* s, const void** pool, size_t* expert_bytes);
 /* MOEB_MODEL_DOWN_T when the stack's pool is row-interleaved (batch 1),
  * MOEB_MODEL_TILED when it is UMMA-tiled (batched tensor-core FFN). */

@@ -6,11 +6,29 @@
  * beside (the paper's CPU-offload baseline).
  * The reference has no layer arithmetic (it abstracts experts as t_gpu /
  * t_cpu_token tasks, pipeline.cpp:217-259); this follows the semantics in
- * oracle/moe_layer_ref.py. Used only by bench.py's cpu_baseline / --impl
- * reference legs; never linked into the product.
+ * oracle/moe_layer_ref.py (pinned to the HF modules by tests/test_hf_pin.py).
+ * Used only by bench.py's cpu_baseline / --impl reference legs and the tests;
+ * never linked into the product.
+ *
+ * Built to be a credible CPU baseline, i.e. host-memory-bandwidth bound:
+ *   * a persistent worker pool (threads created once, woken through a
+ *     generation counter they spin on; no create/join per GEMV);
+ *   * two parallel phases per layer: (1) the router rows and every
+ *     (gate row r, up row r) pair of the shared and selected experts, split
+ *     across threads by rows, each thread forming h_r = silu(g_r . u)(up_r . u)
+ *     for its rows directly; (2) the down projections, split by output row,
+ *     each thread summing every expert's weighted contribution to its rows;
+ *   * AVX2 + FMA bf16 dot products (bf16 -> fp32 is a 16-bit shift, 4
+ *     independent 8-wide accumulators), no -ffast-math (the weight generator
+ *     below must stay bit-exact with csrc/weights.cuh).
+ * cpu_bytes_touched() reports the weight bytes read, so bench.py can state the
+ * achieved host GB/s next to the baseline.
  */
+#include <immintrin.h>
 #include <math.h>
 #include <pthread.h>
+#include <sched.h>
+#include <stdatomic.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -32,86 +50,191 @@ static inline uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-typedef struct {
-  int kind; /* 0 synth, 1 gemv-gate-up, 2 gemv-down */
-  uint64_t seed, tensor, lo, hi;
-  float scale;
-  uint16_t* out;
-  /* gemv */
-  const uint16_t* w;
-  const float* x;
-  float* y;
-  uint32_t cols;
-} job_t;
+/* ------------------------------------------------------------ worker pool */
 
-static void* run_job(void* p) {
-  job_t* j = (job_t*)p;
-  if (j->kind == 0) {
-    for (uint64_t i = j->lo; i < j->hi; ++i) {
-      const uint64_t z = mix64(j->seed ^ (j->tensor * 0x9E3779B97F4A7C15ULL) ^ (i * 0xD1B54A32D192ED03ULL));
-      const float u = (float)(uint32_t)(z >> 40) * 5.9604644775390625e-08f;
-      j->out[i] = to_bf((2.0f * u - 1.0f) * j->scale);
+typedef void (*task_fn)(void* ctx, int tid, int nthreads);
+
+#define MAX_THREADS 256
+static struct {
+  int n;                    /* threads including the caller (tid 0) */
+  pthread_t th[MAX_THREADS];
+  _Atomic uint64_t gen;     /* bumped to start a phase */
+  _Atomic int remaining;    /* workers still running the phase */
+  task_fn fn;
+  void* ctx;
+  pthread_mutex_t mu;
+} g_pool = {.mu = PTHREAD_MUTEX_INITIALIZER};
+
+static uint64_t g_start_gen[MAX_THREADS];
+
+static void* worker(void* arg) {
+  const int tid = (int)(intptr_t)arg;
+  uint64_t seen = g_start_gen[tid];  /* the generation current when it was created */
+  for (;;) {
+    uint64_t g;
+    unsigned spins = 0;
+    while ((g = atomic_load_explicit(&g_pool.gen, memory_order_acquire)) == seen) {
+      if (++spins < (1u << 16)) _mm_pause();
+      else sched_yield();
     }
-  } else {
-    for (uint64_t r = j->lo; r < j->hi; ++r) {
-      const uint16_t* row = j->w + r * j->cols;
-      float s = 0.f;
-      for (uint32_t c = 0; c < j->cols; ++c) s += bf(row[c]) * j->x[c];
-      j->y[r] = s;
-    }
+    seen = g;
+    g_pool.fn(g_pool.ctx, tid, g_pool.n);
+    atomic_fetch_sub_explicit(&g_pool.remaining, 1, memory_order_acq_rel);
   }
   return NULL;
 }
 
-static void parallel(job_t* base, int nthreads, uint64_t n) {
-  pthread_t th[256];
-  job_t jobs[256];
-  if (nthreads > 256) nthreads = 256;
+static void pool_ensure(int nthreads) {
+  if (nthreads > MAX_THREADS) nthreads = MAX_THREADS;
   if (nthreads < 1) nthreads = 1;
-  for (int t = 0; t < nthreads; ++t) {
-    jobs[t] = *base;
-    jobs[t].lo = n * t / nthreads;
-    jobs[t].hi = n * (t + 1) / nthreads;
-    pthread_create(&th[t], NULL, run_job, &jobs[t]);
+  if (g_pool.n >= nthreads) return;
+  if (g_pool.n == 0) g_pool.n = 1;
+  for (int t = g_pool.n; t < nthreads; ++t) {
+    g_start_gen[t] = atomic_load(&g_pool.gen);
+    pthread_create(&g_pool.th[t], NULL, worker, (void*)(intptr_t)t);
+    pthread_detach(g_pool.th[t]);
   }
-  for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  g_pool.n = nthreads;
+}
+
+/* Run fn on every pool thread (the caller is tid 0) and wait for all. */
+static void pool_run(task_fn fn, void* ctx) {
+  g_pool.fn = fn;
+  g_pool.ctx = ctx;
+  atomic_store_explicit(&g_pool.remaining, g_pool.n - 1, memory_order_release);
+  atomic_fetch_add_explicit(&g_pool.gen, 1, memory_order_acq_rel);
+  fn(ctx, 0, g_pool.n);
+  while (atomic_load_explicit(&g_pool.remaining, memory_order_acquire) > 0) _mm_pause();
+}
+
+static inline void split(uint64_t n, int tid, int nt, uint64_t* lo, uint64_t* hi) {
+  *lo = n * (uint64_t)tid / (uint64_t)nt;
+  *hi = n * (uint64_t)(tid + 1) / (uint64_t)nt;
+}
+
+/* ------------------------------------------------- counter-based weights */
+
+typedef struct {
+  uint64_t seed, tensor, n;
+  float scale;
+  uint16_t* out;
+} synth_ctx;
+
+static void synth_task(void* p, int tid, int nt) {
+  const synth_ctx* c = (const synth_ctx*)p;
+  uint64_t lo, hi;
+  split(c->n, tid, nt, &lo, &hi);
+  for (uint64_t i = lo; i < hi; ++i) {
+    const uint64_t z = mix64(c->seed ^ (c->tensor * 0x9E3779B97F4A7C15ULL) ^ (i * 0xD1B54A32D192ED03ULL));
+    const float u = (float)(uint32_t)(z >> 40) * 5.9604644775390625e-08f;
+    const float w = 2.0f * u - 1.0f;
+    c->out[i] = to_bf(w * c->scale);
+  }
 }
 
 /* One tensor of the counter-based weights (weights.cuh), threaded. */
 void cpu_synth(uint64_t seed, uint64_t tensor, uint64_t n, uint32_t fan_in, uint16_t* out, int nthreads) {
-  job_t j;
-  memset(&j, 0, sizeof j);
-  j.kind = 0;
-  j.seed = seed;
-  j.tensor = tensor;
-  j.scale = (float)sqrt(3.0 / (double)fan_in);
-  j.out = out;
-  parallel(&j, nthreads, n);
+  pthread_mutex_lock(&g_pool.mu);
+  pool_ensure(nthreads);
+  synth_ctx c = {seed, tensor, n, (float)sqrt(3.0 / (double)fan_in), out};
+  pool_run(synth_task, &c);
+  pthread_mutex_unlock(&g_pool.mu);
 }
 
-static void gemv(const uint16_t* w, const float* x, float* y, uint64_t rows, uint32_t cols, int nthreads) {
-  job_t j;
-  memset(&j, 0, sizeof j);
-  j.kind = 1;
-  j.w = w;
-  j.x = x;
-  j.y = y;
-  j.cols = cols;
-  parallel(&j, nthreads, rows);
+/* ------------------------------------------------------------ bf16 dots */
+
+static inline __m256 bf8(const uint16_t* p) {
+  const __m128i h = _mm_loadu_si128((const __m128i*)p);
+  return _mm256_castsi256_ps(_mm256_slli_epi32(_mm256_cvtepu16_epi32(h), 16));
 }
 
-/* SwiGLU expert on one token: w = [gate F*d][up F*d][down d*F]; y += wt * out. */
-static void expert(const uint16_t* w, uint32_t d, uint32_t F, const float* u, float wt, float* y,
-                   float* scratch, int nthreads) {
-  float* g = scratch;
-  float* up = scratch + F;
-  float* o = scratch + 2 * (size_t)F;
-  gemv(w, u, g, F, d, nthreads);
-  gemv(w + (size_t)F * d, u, up, F, d, nthreads);
-  for (uint32_t i = 0; i < F; ++i) g[i] = g[i] / (1.0f + expf(-g[i])) * up[i];
-  gemv(w + 2 * (size_t)F * d, g, o, d, F, nthreads);
-  for (uint32_t i = 0; i < d; ++i) y[i] += wt * o[i];
+static inline float hsum(__m256 v) {
+  __m128 s = _mm_add_ps(_mm256_castps256_ps128(v), _mm256_extractf128_ps(v, 1));
+  s = _mm_add_ps(s, _mm_movehl_ps(s, s));
+  s = _mm_add_ss(s, _mm_shuffle_ps(s, s, 1));
+  return _mm_cvtss_f32(s);
 }
+
+/* dot(bf16 row[n], fp32 x[n]); n a multiple of 8 */
+static inline float dot_bf16(const uint16_t* w, const float* x, uint32_t n) {
+  __m256 a0 = _mm256_setzero_ps(), a1 = a0, a2 = a0, a3 = a0;
+  uint32_t i = 0;
+  for (; i + 32 <= n; i += 32) {
+    a0 = _mm256_fmadd_ps(bf8(w + i), _mm256_loadu_ps(x + i), a0);
+    a1 = _mm256_fmadd_ps(bf8(w + i + 8), _mm256_loadu_ps(x + i + 8), a1);
+    a2 = _mm256_fmadd_ps(bf8(w + i + 16), _mm256_loadu_ps(x + i + 16), a2);
+    a3 = _mm256_fmadd_ps(bf8(w + i + 24), _mm256_loadu_ps(x + i + 24), a3);
+  }
+  for (; i + 8 <= n; i += 8) a0 = _mm256_fmadd_ps(bf8(w + i), _mm256_loadu_ps(x + i), a0);
+  float s = hsum(_mm256_add_ps(_mm256_add_ps(a0, a1), _mm256_add_ps(a2, a3)));
+  for (; i < n; ++i) s += bf(w[i]) * x[i];
+  return s;
+}
+
+/* ------------------------------------------------------------- the layer */
+
+#define MAX_ITEMS 80
+typedef struct {
+  const uint16_t* w;  /* [gate F*d][up F*d][down d*F] */
+  uint32_t F;
+  float wt;
+  float* h;           /* [F] intermediate activations */
+  uint64_t row0;      /* first global row of this item in phase 1 */
+} item_t;
+
+typedef struct {
+  uint32_t d, E, n_items;
+  const uint16_t* router;
+  const float* u;
+  float* logits;
+  item_t it[MAX_ITEMS];
+  uint64_t rows1;     /* E + sum F */
+  float* y;
+} layer_ctx;
+
+static void phase1(void* p, int tid, int nt) {
+  layer_ctx* c = (layer_ctx*)p;
+  uint64_t lo, hi;
+  split(c->rows1, tid, nt, &lo, &hi);
+  const uint32_t d = c->d;
+  for (uint64_t r = lo; r < hi;) {
+    if (r < c->E) {  /* router rows */
+      c->logits[r] = dot_bf16(c->router + r * d, c->u, d);
+      ++r;
+      continue;
+    }
+    uint32_t k = 0;
+    while (k + 1 < c->n_items && c->it[k + 1].row0 <= r) ++k;
+    item_t* t = &c->it[k];
+    const uint64_t end = t->row0 + t->F < hi ? t->row0 + t->F : hi;
+    const uint16_t* g = t->w;
+    const uint16_t* up = t->w + (size_t)t->F * d;
+    for (; r < end; ++r) {
+      const uint64_t j = r - t->row0;
+      const float gv = dot_bf16(g + j * d, c->u, d);
+      const float uv = dot_bf16(up + j * d, c->u, d);
+      t->h[j] = gv / (1.0f + expf(-gv)) * uv;
+    }
+  }
+}
+
+static void phase2(void* p, int tid, int nt) {
+  layer_ctx* c = (layer_ctx*)p;
+  uint64_t lo, hi;
+  split(c->d, tid, nt, &lo, &hi);
+  const uint32_t d = c->d;
+  for (uint64_t i = lo; i < hi; ++i) {
+    float s = 0.f;
+    for (uint32_t k = 0; k < c->n_items; ++k) {
+      const item_t* t = &c->it[k];
+      const uint16_t* dn = t->w + 2 * (size_t)t->F * d;
+      s += t->wt * dot_bf16(dn + i * t->F, t->h, t->F);
+    }
+    c->y[i] = s;
+  }
+}
+
+static _Atomic uint64_t g_bytes;
 
 /* One MoE layer for one token (B = 1), all in fp32 over bf16 weights:
  * RMSNorm -> router GEMV (logits written out) -> shared expert (optionally
@@ -121,26 +244,50 @@ void cpu_moe_layer(const uint16_t* x, uint32_t d, uint32_t F, uint32_t S, uint32
                    const uint16_t* router, const uint16_t* shared, const uint16_t* shared_gate,
                    const uint16_t* const* experts, const float* wts, uint32_t n_sel, float* logits,
                    float* y, uint16_t* x_next, int nthreads) {
-  float* u = (float*)malloc(sizeof(float) * d);
-  const uint32_t fmax = F > S ? F : S;
-  float* scratch = (float*)malloc(sizeof(float) * (2 * (size_t)fmax + d + 8));
+  pthread_mutex_lock(&g_pool.mu);
+  pool_ensure(nthreads);
+  static layer_ctx c;  /* under g_pool.mu */
+  float* u = (float*)aligned_alloc(64, sizeof(float) * ((d + 15) & ~15u));
+  const uint32_t n_items = (S ? 1 : 0) + n_sel;
+  float* hbuf = (float*)malloc(sizeof(float) * ((size_t)S + (size_t)n_sel * F + 8));
   double ss = 0.0;
   for (uint32_t i = 0; i < d; ++i) ss += (double)bf(x[i]) * bf(x[i]);
   const float inv = (float)(1.0 / sqrt(ss / d + 1e-6));
   for (uint32_t i = 0; i < d; ++i) u[i] = bf(to_bf(bf(x[i]) * inv));
-  gemv(router, u, logits, E, d, nthreads);
-  memset(y, 0, sizeof(float) * d);
-  if (S) {
-    float gate = 1.0f;
-    if (shared_gate) {
-      float z = 0.f;
-      for (uint32_t i = 0; i < d; ++i) z += bf(shared_gate[i]) * u[i];
-      gate = 1.0f / (1.0f + expf(-z));
-    }
-    expert(shared, d, S, u, gate, y, scratch, nthreads);
+  float gate = 1.0f;
+  if (S && shared_gate) {
+    const float z = dot_bf16(shared_gate, u, d);
+    gate = 1.0f / (1.0f + expf(-z));
   }
-  for (uint32_t i = 0; i < n_sel; ++i) expert(experts[i], d, F, u, wts[i], y, scratch, nthreads);
+  c.d = d;
+  c.E = E;
+  c.router = router;
+  c.u = u;
+  c.logits = logits;
+  c.y = y;
+  c.n_items = n_items > MAX_ITEMS ? MAX_ITEMS : n_items;
+  uint64_t row = E, hoff = 0, bytes = (uint64_t)E * d * 2;
+  for (uint32_t k = 0; k < c.n_items; ++k) {
+    item_t* t = &c.it[k];
+    const int sh = S && k == 0;
+    t->w = sh ? shared : experts[k - (S ? 1 : 0)];
+    t->F = sh ? S : F;
+    t->wt = sh ? gate : wts[k - (S ? 1 : 0)];
+    t->h = hbuf + hoff;
+    t->row0 = row;
+    row += t->F;
+    hoff += t->F;
+    bytes += 3ull * t->F * d * 2;
+  }
+  c.rows1 = row;
+  pool_run(phase1, &c);
+  pool_run(phase2, &c);
   for (uint32_t i = 0; i < d; ++i) x_next[i] = to_bf(bf(x[i]) + y[i]);
+  atomic_fetch_add(&g_bytes, bytes);
+  pthread_mutex_unlock(&g_pool.mu);
   free(u);
-  free(scratch);
+  free(hbuf);
 }
+
+/* Weight bytes read by cpu_moe_layer since the last call (then reset). */
+uint64_t cpu_bytes_touched(void) { return atomic_exchange(&g_bytes, 0); }

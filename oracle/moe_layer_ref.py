@@ -63,6 +63,36 @@ def bf16_bits_to_f32(b):
     return (np.asarray(b, dtype=np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
 
 
+_CPUMOE = None
+
+
+def _cpumoe():
+    """oracle/libcpumoe.so's threaded generator (bit-exact with synth_tensor's
+    numpy path: tests/test_cpu_baseline.py), or None when not built."""
+    global _CPUMOE
+    if _CPUMOE is None:
+        import ctypes as C
+        import os
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libcpumoe.so")
+        try:
+            lib = C.CDLL(path)
+            lib.cpu_synth.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int]
+            _CPUMOE = lib
+        except OSError:
+            _CPUMOE = False
+    return _CPUMOE or None
+
+
+def synth_tensor_fast(seed, tensor, n, fan_in):
+    lib = _cpumoe()
+    if lib is None:
+        return synth_tensor(seed, tensor, n, fan_in)
+    import os
+    out = np.empty(n, dtype=np.uint16)
+    lib.cpu_synth(seed, tensor, n, fan_in, out.ctypes.data, min(16, os.cpu_count() or 1))
+    return out
+
+
 def synth_tensor(seed, tensor, n, fan_in, offset=0):
     """bf16 bits of tensor elements [offset, offset + n) (weights.cuh synth_weight)."""
     scale = np.float32(np.sqrt(3.0 / float(fan_in)))
@@ -94,9 +124,9 @@ class SynthModel:
         d, S = self.d, self.S
 
         def mk():
-            g = bf16_bits_to_f32(synth_tensor(self.seed, tid_shared(layer, 0), S * d, d)).reshape(S, d)
-            u = bf16_bits_to_f32(synth_tensor(self.seed, tid_shared(layer, 1), S * d, d)).reshape(S, d)
-            dn = bf16_bits_to_f32(synth_tensor(self.seed, tid_shared(layer, 2), S * d, S)).reshape(d, S)
+            g = bf16_bits_to_f32(synth_tensor_fast(self.seed, tid_shared(layer, 0), S * d, d)).reshape(S, d)
+            u = bf16_bits_to_f32(synth_tensor_fast(self.seed, tid_shared(layer, 1), S * d, d)).reshape(S, d)
+            dn = bf16_bits_to_f32(synth_tensor_fast(self.seed, tid_shared(layer, 2), S * d, S)).reshape(d, S)
             return g, u, dn
         return self._get(("s", layer), mk)
 
@@ -108,9 +138,9 @@ class SynthModel:
         d, F = self.d, self.F
 
         def mk():
-            g = bf16_bits_to_f32(synth_tensor(self.seed, tid_expert(layer, e, 0), F * d, d)).reshape(F, d)
-            u = bf16_bits_to_f32(synth_tensor(self.seed, tid_expert(layer, e, 1), F * d, d)).reshape(F, d)
-            dn = bf16_bits_to_f32(synth_tensor(self.seed, tid_expert(layer, e, 2), F * d, F)).reshape(d, F)
+            g = bf16_bits_to_f32(synth_tensor_fast(self.seed, tid_expert(layer, e, 0), F * d, d)).reshape(F, d)
+            u = bf16_bits_to_f32(synth_tensor_fast(self.seed, tid_expert(layer, e, 1), F * d, d)).reshape(F, d)
+            dn = bf16_bits_to_f32(synth_tensor_fast(self.seed, tid_expert(layer, e, 2), F * d, F)).reshape(d, F)
             return g, u, dn
         return self._get(("e", layer, e), mk)
 
@@ -135,11 +165,12 @@ def softmax32(logits):
 
 
 def swiglu(u, g, up, dn):
-    """silu(g.u) * (up.u) -> down; u fp32 [d]; weights fp32 (from bf16)."""
-    gv = g.astype(np.float64) @ u.astype(np.float64)
-    uv = up.astype(np.float64) @ u.astype(np.float64)
+    """silu(g.u) * (up.u) -> down; u fp32 [d] or [n, d]; weights fp32 (from bf16)."""
+    u64 = u.astype(np.float64)
+    gv = u64 @ g.astype(np.float64).T
+    uv = u64 @ up.astype(np.float64).T
     h = (gv / (1.0 + np.exp(-gv))) * uv
-    return dn.astype(np.float64) @ h
+    return h @ dn.astype(np.float64).T
 
 
 def layer_forward(model: SynthModel, layer, x_bits, sel, scores, renormalize=False, routed_scale=1.0):
@@ -160,12 +191,18 @@ def layer_forward(model: SynthModel, layer, x_bits, sel, scores, renormalize=Fal
                 z = float(model.shared_gate_row(layer).astype(np.float64) @ u[t].astype(np.float64))
                 ys = ys / (1.0 + np.exp(-z))
             y[t] += ys
+    # per expert, every token that selected it at once (same arithmetic)
+    users = {}
     for t in range(B):
         denom = sum(float(scores[t][e]) for e in sel[t]) if renormalize else 1.0
         for e in sel[t]:
-            w = float(scores[t][e]) / denom * routed_scale
-            g, up, dn = model.expert(layer, e)
-            y[t] += w * swiglu(u[t], g, up, dn)
+            users.setdefault(e, []).append((t, float(scores[t][e]) / denom * routed_scale))
+    for e in sorted(users):
+        toks = [t for t, _ in users[e]]
+        g, up, dn = model.expert(layer, e)
+        ye = swiglu(u[toks], g, up, dn)
+        for i, (t, w) in enumerate(users[e]):
+            y[t] += w * ye[i]
     return y
 
 

@@ -406,7 +406,7 @@ class _StackExt:
         return d
 
     def timeline(self):
-        """Device-clock (ns) timeline, one row of 8 words per layer-step (see moeb_get_timeline)."""
+        """Device-clock (ns) timeline, one row of 16 words per layer-step (word table: moeb_get_timeline in include/moesched_b200.h)."""
         n = C.c_size_t(0)
         check(lib().moeb_get_timeline(self.h, None, 0, C.byref(n)))
         out = np.zeros(n.value, dtype=np.uint64)

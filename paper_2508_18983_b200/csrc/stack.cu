@@ -25,6 +25,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>  // environ
+
 #include "../../include/moesched_b200.h"
 #include "decide.cuh"
 #include "engine_host.h"
@@ -820,6 +822,14 @@ struct moeb_stack {
   MailEntry* ring_dev = nullptr;
   uint64_t* ack_dev = nullptr;
   uint64_t host_it = 0, host_seq = 0;  // mirrors of EngineState::it / seq
+  // Serial (profiler-safe) mode: upload dependencies are stream waits on the
+  // compute stream (cuStreamWaitValue32) set up by the host after each decide
+  // kernel, never in-kernel spins on a concurrently running engine. Chosen
+  // with MOEB_SERIAL=1 or automatically under ncu / nsys / compute-sanitizer,
+  // which serialise kernels (and the copy thread's API calls) behind the one
+  // being measured, so an FFN spinning on copies_done could never see them.
+  bool serial = false;
+  uint32_t serial_need = 0;  // highest upload id the next FFN may depend on
   uint64_t n_launch_layers = 0;        // (gate+decide, FFN) launch pairs
   std::mutex io_mu;
   IoAcc io;
@@ -981,6 +991,20 @@ static void synth_tiled(uint16_t* dst, uint32_t F, uint32_t d, uint64_t seed, ui
   const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
   synth_tiled_kernel<<<grid, 256, 0, s>>>(dst, F, d, seed, t0, t1, t2, s_in, s_down);
   MOEB_CUDA(cudaGetLastError());
+}
+
+// Tools that serialise kernels inject themselves through these variables
+// (ncu/nsys: CUDA_INJECTION64_PATH + NV_COMPUTE_PROFILER_* / NSYS_*;
+// compute-sanitizer: its own injection); MOEB_SERIAL=0/1 overrides.
+static bool serial_mode_requested() {
+  if (const char* v = getenv("MOEB_SERIAL")) return v[0] != '0';
+  for (char** e = environ; e && *e; ++e) {
+    static const char* kPrefixes[] = {"CUDA_INJECTION64_PATH=", "NV_COMPUTE_PROFILER", "NSYS_", "NV_NSIGHT",
+                                      "NV_SANITIZER", "COMPUTE_SANITIZER"};
+    for (const char* pre : kPrefixes)
+      if (std::strncmp(*e, pre, std::strlen(pre)) == 0) return true;
+  }
+  return false;
 }
 
 static float fan_scale(uint32_t fan_in) { return (float)std::sqrt(3.0 / (double)fan_in); }
@@ -1213,6 +1237,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // the speculative start the FFN runs beside the deciding CTA, so one SM
   // is left to it
   S->ffn_grid = S->spec ? sms - 1 : sms;
+  S->serial = serial_mode_requested();
   MOEB_CUDA(cudaStreamSynchronize(s));
   S->copier = std::thread([S] { S->copy_loop(); });
 }
@@ -1226,7 +1251,8 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
 static const bool kUsePdl = getenv("MOEB_NO_PDL") == nullptr;
 
 template <class Args>
-static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args* args) {
+static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args* args,
+                       bool pdl = kUsePdl) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -1234,18 +1260,67 @@ static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaS
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = kUsePdl ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   void* kargs[] = {args};
   MOEB_CUDA(cudaLaunchKernelExC(&cfg, fn, kargs));
 }
 
+// Serial mode, after layer-step `seq`'s decide kernel was launched: wait for
+// it, read the upload commands it published (mailbox entries A = demand loads
+// and BA streams of this step, B = prefetches for later steps) and make the
+// compute stream wait for every upload the coming FFN may read. Upload ids
+// grow in publication order and the copy stream is FIFO, so one
+// copies_done >= id wait covers them; entry B's prefetches (which themselves
+// wait for this step's FFN) are only owed to later steps.
+static void serial_wait_uploads(moeb_stack* S, cudaStream_t s, uint64_t seq) {
+  MOEB_CUDA(cudaStreamSynchronize(s));
+  const MailEntry* ea = &S->ring[(2 * seq - 1) % kRing];
+  const MailEntry* eb = &S->ring[(2 * seq) % kRing];
+  const uint64_t va = ea->seq, vb = eb->seq;
+  if ((va >> 8) != 2 * seq - 1 || (vb >> 8) != 2 * seq)
+    throw Error(5, "serial mode: the decide kernel did not publish its upload commands");
+  if (va & 0xff) S->serial_need = std::max(S->serial_need, ea->cmd[(va & 0xff) - 1].id);
+  if (S->serial_need &&
+      p_wait32(s, (CUdeviceptr)S->copies_done.p, S->serial_need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    throw Error(5, "serial mode: cuStreamWaitValue32 failed");
+  if (vb & 0xff) S->serial_need = std::max(S->serial_need, eb->cmd[(vb & 0xff) - 1].id);
+}
+
+// The persistent FFN grids assume every CTA is co-resident (grid barriers,
+// one CTA per SM). Two stacks stepping on one GPU at the same time could each
+// end up partly resident, so the steps of all stacks of a device are ordered:
+// a stack's step waits (on the device, through an event) for the last step
+// any other stack of that device enqueued.
+struct DeviceOrder {
+  std::mutex mu;
+  cudaEvent_t ev = nullptr;
+  const moeb_stack* owner = nullptr;
+};
+static DeviceOrder& device_order(int dev) {
+  static DeviceOrder orders[64];
+  return orders[dev & 63];
+}
+
+static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B, cudaStream_t s);
+
 static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaStream_t user) {
   if (B != S->B) throw Error(1, "step: batch must equal the configured batch_size");
   if (S->copier_error) throw Error(5, S->copier_msg);
   if (S->cfg.pre && !S->trace.p) throw Error(1, "stage Pre needs a logits trace (moeb_set_logits_trace)");
   cudaStream_t s = user ? user : S->stream;
+  MOEB_CUDA(cudaSetDevice(S->device));
+  DeviceOrder& o = device_order(S->device);
+  std::lock_guard<std::mutex> lk(o.mu);
+  if (!o.ev) MOEB_CUDA(cudaEventCreateWithFlags(&o.ev, cudaEventDisableTiming));
+  if (o.owner && o.owner != S) MOEB_CUDA(cudaStreamWaitEvent(s, o.ev, 0));
+  step_stack_locked(S, x, y, B, s);
+  MOEB_CUDA(cudaEventRecord(o.ev, s));
+  o.owner = S;
+}
+
+static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B, cudaStream_t s) {
   const uint32_t L = S->L, E = S->E, d = S->d;
   MOEB_CUDA(cudaMemcpyAsync(S->hidden.p, x, (size_t)B * d * 2, cudaMemcpyDeviceToDevice, s));
   int cur = 0;
@@ -1302,8 +1377,9 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
     ga.ticket = S->ticket.p;
     if (S->timing) S->tick(s);
     launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3((rows + 1) / 2), dim3(kGdThreads),
-               S->gd_smem, s, &ga);
+               S->gd_smem, s, &ga, kUsePdl && !S->serial);
     MOEB_CUDA(cudaGetLastError());
+    if (S->serial) serial_wait_uploads(S, s, a.seq);
     if (S->timing) S->tick(s);
 
     FfnTArgs f{};
@@ -1349,10 +1425,10 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
       ua.KS = S->um.KS;
       ua.dn_st = S->um.dn_st;
       launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s,
-                 &ua);
+                 &ua, kUsePdl && !S->serial);
     } else {
       launch_pdl(reinterpret_cast<const void*>(S->ffn.fn), dim3(S->ffn_grid), dim3(S->ffn.threads), S->ffn.smem, s,
-                 &f);
+                 &f, kUsePdl && !S->serial);
     }
     S->n_launch_layers += 1;
     MOEB_CUDA(cudaGetLastError());
@@ -1365,10 +1441,25 @@ static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaSt
   S->io.steps += 1;
 }
 
-static uint32_t read_spin_timeout() {
+// The device raises g_spin_timeout when a bounded wait gives up. It is read
+// and cleared together: the failure is reported once (by the moeb_sync that
+// observes it) and does not poison later syncs of this or other stacks.
+static uint32_t take_spin_timeout() {
   uint32_t v = 0;
   cudaMemcpyFromSymbol(&v, g_spin_timeout, sizeof v);
+  if (v) {
+    const uint32_t zero = 0;
+    cudaMemcpyToSymbol(g_spin_timeout, &zero, sizeof zero);
+  }
   return v;
+}
+
+// The per-step logs hold the first rec_cap layer-steps since create; a
+// longer run fails loudly instead of returning a silently truncated log.
+static void check_log_capacity(const moeb_stack* s, uint64_t seq) {
+  if (seq > s->rec_cap)
+    throw Error(4, "decision log overflow: " + std::to_string(seq) + " layer-steps since create exceed the log "
+                   "capacity of " + std::to_string(s->rec_cap));
 }
 
 }  // namespace moeb
@@ -1418,7 +1509,7 @@ int moeb_sync(moeb_stack* s) {
     MOEB_CUDA(cudaSetDevice(s->device));
     MOEB_CUDA(cudaStreamSynchronize(s->stream));
     MOEB_CUDA(cudaDeviceSynchronize());
-    if (const uint32_t to = read_spin_timeout()) {
+    if (const uint32_t to = take_spin_timeout()) {
       throw Error(5, "device wait timed out (code " + std::to_string(to) + "): upload pipeline stalled");
     }
     if (s->copier_error) throw Error(5, s->copier_msg);
@@ -1440,6 +1531,7 @@ int moeb_get_decisions_json(moeb_stack* s, char** json) {
     MOEB_CUDA(cudaDeviceSynchronize());
     EngineState st;
     MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
+    check_log_capacity(s, st.seq);
     const size_t n = std::min<uint64_t>(st.seq, s->rec_cap);
     std::vector<StepRec> r(n);
     std::vector<TokRec> t(n * s->B);
@@ -1460,6 +1552,7 @@ int moeb_get_scores(moeb_stack* s, float* out, size_t cap, size_t* n) {
     MOEB_CUDA(cudaDeviceSynchronize());
     EngineState st;
     MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
+    check_log_capacity(s, st.seq);
     const size_t total = std::min<uint64_t>(st.seq, s->rec_cap) * s->B * s->E;
     const size_t k = std::min(total, cap);
     if (k) MOEB_CUDA(cudaMemcpy(out, s->scores_log.p, k * sizeof(float), cudaMemcpyDeviceToHost));
@@ -1495,6 +1588,7 @@ int moeb_reset(moeb_stack* s) {
     MOEB_CUDA(cudaStreamSynchronize(s->copy_stream));
     reset_state(s, s->stream);
     s->host_it = 0;
+    take_spin_timeout();
   });
 }
 
