@@ -49,6 +49,7 @@ CFG = dict(num_layers=26, experts=64, top_k=6, batch=1, alpha=0.25, slots=16, wi
            ce=1, er=1, pre=1, ba=1)
 MODEL = dict(d_model=2048, ffn=1408, shared_ffn=2816, shared_gate=0, renormalize=0, routed_scale=1.0)
 TOKENS = 512
+FFN_KERNEL_B1 = "ffn_splitk_kernel"  # the batch-1 FFN (csrc/ffn_splitk.cuh) the roofline line measures
 
 
 def peaks():
@@ -178,42 +179,6 @@ def measure_pcie_gbs(torch):
     return n / best / 1e6
 
 
-def open_shared_pool(capi, local, torch, dist, coll_dev):
-    """The node's expert pool as a /dev/shm segment: local rank 0 creates and
-    fills it (its stack generates the weights into it), the other ranks map it
-    after a barrier and pass its layout flags. Returns ptr / map / flags and a
-    hook to run after the stack exists (barrier, flag broadcast, unlink)."""
-    L, E, d, F = CFG["num_layers"], CFG["experts"], MODEL["d_model"], MODEL["ffn"]
-    nbytes = L * E * 3 * F * d * 2
-    tag = os.environ.get("TORCHELASTIC_RUN_ID", "run") + "_" + os.environ.get("MASTER_PORT", "0")
-    path = f"/dev/shm/moeb_pool_{tag}"
-    info = {}
-    if local == 0:
-        with open(path, "wb") as f:
-            f.truncate(nbytes)
-    dist.barrier()
-    mm = np.memmap(path, dtype=np.uint8, mode="r+", shape=(nbytes,))
-    info["map"], info["ptr"] = mm, mm.ctypes.data
-    flags = torch.zeros(1, dtype=torch.int64, device=coll_dev)
-    info["flags"] = 0
-    if local != 0:
-        dist.broadcast(flags, src=0)  # rank 0 filled the pool and knows its layout
-        info["flags"] = int(flags.item())
-
-    def after_create(stack):
-        if local == 0:
-            fl = C.c_uint32(0)
-            capi.lib().moeb_host_pool_flags(stack.h, C.byref(fl))
-            flags.fill_(fl.value)
-            dist.broadcast(flags, src=0)
-        dist.barrier()
-        if local == 0:
-            os.unlink(path)  # the mappings stay valid
-
-    info["after_create"] = after_create
-    return info
-
-
 def batched_section(capi, torch, local, hbm_peak, batches=(8, 32), n_warm=8, n_timed=32):
     """Config C5 (independent decode streams, DeepSeek-V2-Lite shape) at
     batch B on one GPU: the batched tensor-core FFN (ffn_umma.cuh). Per B:
@@ -290,10 +255,68 @@ def batched_section(capi, torch, local, hbm_peak, batches=(8, 32), n_warm=8, n_t
     return out
 
 
+def c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, B, tokens=16, n_requests=64,
+                   n_warm=3):
+    """Config C5 as specified: n_requests independent DeepSeek-V2-Lite decode
+    streams at batch B, stream-partitioned across the world's GPUs
+    (partition.partition: contiguous blocks of batch groups), each GPU with
+    its own 16/64 expert cache, copy stream and PCIe link, no collective on
+    the data path. Every rank decodes its groups back to back; the whole-job
+    time is the max over ranks. Collective over all ranks (setup + timing)."""
+    L, E, d = CFG["num_layers"], CFG["experts"], MODEL["d_model"]
+    groups = partition.partition(n_requests, B, world, rank)
+    scores = partition.sub_stream(capi, L, E, B, tokens, groups)
+    T = scores.shape[0]
+    cfg = capi.Config.make(**dict(CFG, batch=B))
+    pool_bytes = L * E * 3 * MODEL["ffn"] * d * 2
+    st = pools.stack(capi, cfg, "rows" if B == 1 else "tiled", pool_bytes, weight_seed=7, device=local, **MODEL)
+    st.set_logits_trace(capi.trace_logits(scores), T)
+    x = torch.from_numpy(np.concatenate([ar1_hidden(tokens, B, d, partition.group_seed(g)) for g in groups])) \
+        .to(torch.bfloat16).cuda()
+    y = torch.empty((B, d), dtype=torch.bfloat16, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for i in range(n_warm):  # first launches, then back to the initial state
+            st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+        st.sync()
+        st.reset()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for i in range(T):
+            st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+        e1.record(s)
+        e1.synchronize()
+        st.sync()
+    ms = e0.elapsed_time(e1)
+    m = st.metrics()
+    io = st.io_stats()
+    st.close()
+    mine = torch.tensor([ms, float(T * B), float(m["hits"]), float(m["selections"]), float(io["h2d_bytes"])],
+                        dtype=torch.float64)
+    if world > 1:
+        allv = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(allv, mine)
+    else:
+        allv = [mine]
+    allv = torch.stack(allv).numpy()
+    t_max = float(allv[:, 0].max())
+    toks = float(allv[:, 1].sum())
+    return {"batch": B, "requests": n_requests, "tokens_per_request": tokens, "gpus": world,
+            "groups_per_gpu": len(groups), "whole_job_ms": round(t_max, 2),
+            "tokens_per_s": round(toks / (t_max * 1e-3), 1),
+            "per_gpu_tokens_per_s": [round(float(r[1] / (r[0] * 1e-3)), 1) for r in allv],
+            "hit_rate": round(float(allv[:, 2].sum() / max(allv[:, 3].sum(), 1)), 4),
+            "pcie_gb_per_gpu": [round(float(r[4]) / 1e9, 3) for r in allv],
+            "ms_per_token_whole_job": round(t_max / toks, 4)}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2508_18983_b200 import capi
+    from paper_2508_18983_b200 import capi, partition
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -304,12 +327,11 @@ def run_ours(args):
     if share_gpu:
         local = 0
     torch.cuda.set_device(local)
-    coll_dev = "cpu" if share_gpu else "cuda"
+    # no NCCL anywhere: the data path has no collective (north star); gloo
+    # carries the setup exchange, the barriers and the max/sum of timings
+    coll_dev = "cpu"
     if world > 1:
-        if share_gpu:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -331,7 +353,11 @@ def run_ours(args):
         return float(t.item())
 
     W, K = args.warmup, args.steps
-    T = W + K
+    # the whole 512-token stream of configs[1] is decoded; the timed tokens
+    # are its last K (so the cache is in its steady state), everything
+    # before them is untimed warm-up (>= W tokens)
+    T = max(TOKENS, W + K)
+    W = T - K
     L, E, B, d = CFG["num_layers"], CFG["experts"], CFG["batch"], MODEL["d_model"]
     seed = 7 + rank  # independent decode stream per GPU (stream partitioning, no collective)
     scores = capi.generate_trace(L, E, B, T, seed)
@@ -347,18 +373,12 @@ def run_ours(args):
     # no per-kernel CUDA events in the timed stack (they would serialise the
     # programmatic dependent launches); the per-kernel split comes from the
     # device-clock timeline (globaltimer stamps written by the kernels)
-    shared_pool = None
-    if world > 1:
-        # one pinned host pool per node, in /dev/shm, mapped by every rank
-        # (28.8 GB instead of 28.8 GB x ranks): local rank 0 fills it
-        node_local = int(os.environ.get("LOCAL_RANK", "0"))
-        shared_pool = open_shared_pool(capi, node_local, torch, dist, coll_dev)
-        stack = capi.Stack(cfg, weight_seed=7, trace_timeline=True, device=local,
-                           weights_host=(shared_pool["ptr"], shared_pool["map"]), fill_pool=(node_local == 0),
-                           pool_flags=0 if node_local == 0 else shared_pool["flags"], **MODEL)
-        shared_pool["after_create"](stack)
-    else:
-        stack = capi.Stack(cfg, weight_seed=7, trace_timeline=True, device=local, **MODEL)
+    # pinned host pools: one replica per NUMA node of GPUs (28.8 GB each),
+    # filled by the node's first rank and mapped by the others
+    pools = partition.NodePools(dist if world > 1 else None, local,
+                                os.environ.get("TORCHELASTIC_RUN_ID", "run") + "_" + os.environ.get("MASTER_PORT", "0"))
+    pool_bytes = L * E * 3 * MODEL["ffn"] * d * 2
+    stack = pools.stack(capi, cfg, "rows", pool_bytes, weight_seed=7, trace_timeline=True, device=local, **MODEL)
     create_s = time.time() - t0
     stack.set_logits_trace(logits, T)
     # a torch-owned stream for the stack's work: pinned-buffer copies recorded
@@ -493,10 +513,14 @@ def run_ours(args):
     tl_hit = timeline_summary(tl3)
     ffn_gbs = k3["ffn_bytes"] / (k3["ffn_ms"] * 1e-3) / 1e9
     per_launch_bytes = k3["ffn_bytes"] / max(k3["ffn_launches"], 1)
-    traffic = None
+    # DRAM bytes per launch of the SAME kernel from a committed ncu --set full
+    # capture of this configuration (null if the capture is of another kernel)
+    traffic, traffic_src = None, None
     try:
         with open(os.path.join(REPO, "profiles", "ncu_ffn_traffic.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        if FFN_KERNEL_B1 in tj.get("kernel", ""):
+            traffic, traffic_src = tj.get("dram_bytes_per_launch"), tj.get("source")
     except Exception:
         pass
 
@@ -522,7 +546,7 @@ def run_ours(args):
         "unit": "ms/token",
         "n_gpus": world,
         "steps": K,
-        "warmup": W,
+        "warmup": args.warmup,
         "ms_per_step": round(ms_max / K, 4),
         "higher_is_better": False,
         "scaling": "weak",
@@ -530,10 +554,11 @@ def run_ours(args):
         "dtype": "bf16 weights, fp32 accumulate; fp64 decisions",
         "data": "synthetic: reference generate_trace router logits (seed 7+rank), AR(1) hidden states, "
                 "counter-based random bf16 weights",
-        "config": {"workload": "DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode, 512-token stream, "
-                               "cache 16/64 experts per layer, CE+ER+Pre+BA alpha=0.25",
-                   "layers": L, "experts": E, "top_k": CFG["top_k"], "shared_ffn": MODEL["shared_ffn"],
-                   "d_model": d, "ffn": MODEL["ffn"], "global_batch": B * world, "tokens_per_gpu": T,
+        "config": {"workload": f"DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode of a {T}-token stream "
+                               f"(timed: its last {K} tokens), cache 16/64 experts per layer, CE+ER+Pre+BA "
+                               "alpha=0.25",
+                   "stream_tokens": T, "untimed_tokens_before_window": W, "layers": L, "experts": E, "top_k": CFG["top_k"], "shared_ffn": MODEL["shared_ffn"],
+                   "d_model": d, "ffn": MODEL["ffn"], "global_batch": B * world, "tokens_per_gpu_timed": K,
                    "slots_per_layer": CFG["slots"], "parallelism": f"stream-partitioned x{world} (no collective)",
                    "l2": "inputs > L2 (>=140 MB weights per step)"},
         "hit_rate": round(hit, 4),
@@ -546,9 +571,9 @@ def run_ours(args):
                                                           (m1["low_score_kept"] - m0["low_score_kept"])), 4)},
         "e2e": {"value": round(e2e_ms_max / K, 4), "unit": "ms/token", "h2d_bytes_per_step": B * d * 2,
                 "d2h_bytes_per_step": B * d * 2},
-        "roofline": {"bound": "hbm", "kernel": "ffn_kernel (all-resident pass, no uploads)",
+        "roofline": {"bound": "hbm", "kernel": f"{FFN_KERNEL_B1} (all-resident pass, no uploads)",
                      "achieved": round(ffn_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(ffn_gbs / hbm_peak, 4), "traffic": traffic,
+                     "frac": round(ffn_gbs / hbm_peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                      "device_clock_span_us": tl_hit["ffn_span_us"],
                      "device_clock_achieved": round(per_launch_bytes / (tl_hit["ffn_span_us"] * 1e-6) / 1e9, 1),
                      "device_clock_frac": round(per_launch_bytes / (tl_hit["ffn_span_us"] * 1e-6) / 1e9 / hbm_peak, 4),
@@ -569,8 +594,16 @@ def run_ours(args):
     }
     if abl:
         result["ablation"] = abl
-    if rank == 0 and world == 1 and not args.no_batched:
+    if not args.no_c5:
+        # C5: 64 requests stream-partitioned over the world's GPUs at the
+        # largest batch the partition allows (B <= 64 / G, <= 32)
         stack.close()
+        stack = None
+        Bc5 = min(32, 64 // world)
+        result["c5_partitioned"] = c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, Bc5)
+    if rank == 0 and world == 1 and not args.no_batched:
+        if stack is not None:
+            stack.close()
         stack = None
         result["batched_c5"] = batched_section(capi, torch, local, hbm_peak)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -691,7 +724,7 @@ def run_reference(args):
         return
     L, E, B, d = CFG["num_layers"], CFG["experts"], CFG["batch"], MODEL["d_model"]
     W, K = args.warmup, args.steps
-    T = W + K
+    T = max(TOKENS, W + K)  # the same 512-token stream as the device arm
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import pyoracle as po
     scores = po.generate_trace(L, E, B, T, 7, use_ref=po.ref() is not None)
@@ -704,8 +737,9 @@ def run_reference(args):
         "value": round(ms, 3), "unit": "ms/token", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": K, "warmup": W, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32 compute over bf16 weights; fp64 decisions", "data": "synthetic",
-        "config": {"workload": "DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode, 512-token stream, "
-                               "cache 16/64 experts per layer, CE+ER+Pre+BA alpha=0.25"},
+        "config": {"workload": f"DeepSeek-V2-Lite 26-layer MoE stack, batch-1 decode of a {T}-token stream "
+                               f"(timed: its last {K} tokens), cache 16/64 experts per layer, CE+ER+Pre+BA "
+                               "alpha=0.25", "stream_tokens": T},
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms/token", "cores": cores, "kind": kind, "sample": sample,
                          "host_weight_gbs": round(gbs, 1)},
         "e2e": {"value": round(ms, 3), "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -722,6 +756,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the batched (config C5) tensor-core FFN section")
     ap.add_argument("--cpu-sample-tokens", type=int, default=12)
+    ap.add_argument("--no-c5", action="store_true", help="skip the stream-partitioned config C5 section")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -240,6 +240,25 @@ int moeb_get_metrics(moeb_stack* s, moeb_metrics* m);
  * plus the fp32 router scores each step used (for oracle replay). */
 int moeb_get_decisions_json(moeb_stack* s, char** json);
 int moeb_get_scores(moeb_stack* s, float* out, size_t cap, size_t* n);
+/* The same per-step records as plain structs (what the C++ MoeStack wrapper,
+ * include/moesched/moe_layer.hpp, turns into RouteResult / load-list form).
+ * One moeb_step_record per (iteration, layer), batch moeb_token_records each,
+ * in step order. Bitmask resident_before = the residency snapshot the router
+ * saw (pipeline.cpp:154-155). steps/toks may be NULL to query the count. */
+typedef struct moeb_step_record {
+  uint64_t iteration;
+  uint32_t layer, batch;
+  uint64_t resident_before, completion;
+  uint8_t n_load, n_cpu, n_pref, n_evict;
+  uint8_t load[64], cpu[64], pref[64];     /* load_list, cpu_list (BA-streamed), prefetch issues */
+  uint8_t evict_layer[128], evict_expert[128];
+} moeb_step_record;
+typedef struct moeb_token_record {
+  uint8_t n_sel, n_sub, n_kept, pad;
+  uint8_t sel[16], sub_dropped[16], sub_chosen[16], kept[16];
+} moeb_token_record;
+int moeb_get_decisions(moeb_stack* s, moeb_step_record* steps, moeb_token_record* toks, size_t cap_steps,
+                       size_t* n_steps);
 /* Upload accounting: bytes and the copy stream's busy time (CUDA events). */
 typedef struct moeb_io_stats {
   uint64_t h2d_bytes, h2d_copies, d2d_copies, steps;

@@ -6,6 +6,6 @@ moesched API (include/moesched/*.hpp) and a C-ABI (include/moesched_b200.h).
 The Python package only binds the C-ABI (capi.py); the product is
 libmoeb.so (CUDA, sm_100a) and libmoesched.so (C++ drop-in).
 """
-from . import capi  # noqa: F401
+from . import capi, partition  # noqa: F401
 
-__all__ = ["capi"]
+__all__ = ["capi", "partition"]

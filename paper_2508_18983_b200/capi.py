@@ -308,6 +308,12 @@ class Stack:
         check(lib().moeb_create(C.byref(cfg), C.byref(m), wp, C.c_int(device), C.byref(h)))
         self.h, self.cfg, self.model = h, cfg, m
 
+    def pool_flags(self):
+        """Layout flags of this stack's host pool (MOEB_MODEL_DOWN_T / MOEB_MODEL_TILED)."""
+        fl = C.c_uint32(0)
+        check(lib().moeb_host_pool_flags(self.h, C.byref(fl)))
+        return fl.value
+
     def close(self):
         if getattr(self, "h", None):
             lib().moeb_destroy(self.h)

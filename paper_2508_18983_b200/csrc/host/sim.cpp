@@ -225,6 +225,34 @@ const char* to_string(TaskKind k) {
     return i < 7 ? kNames[i] : "?";
 }
 
+// SimConfig (core.hpp:94-106) -> the C-ABI's flattened moeb_config.
+moeb_config to_moeb_config(const SimConfig& cfg) {
+    moeb_config c{};
+    c.num_layers = cfg.shape.num_layers;
+    c.experts = cfg.shape.experts_per_layer;
+    c.top_k = cfg.shape.top_k;
+    c.batch = cfg.shape.batch_size;
+    c.alpha = cfg.router.alpha;
+    c.slots = cfg.cache.slots_per_layer;
+    c.window = cfg.cache.history_window;
+    c.policy = cfg.cache.policy == CachePolicy::LRU ? 1 : 0;
+    c.init_fill = cfg.cache.init_fill == InitFill::FirstSlots ? 0 : cfg.cache.init_fill == InitFill::SeededRandom ? 1 : 2;
+    c.t_attn = cfg.cost.t_attn;
+    c.t_gpu = cfg.cost.t_gpu;
+    c.t_cpu_token = cfg.cost.t_cpu_token;
+    c.t_load = cfg.cost.t_load;
+    c.t_route = cfg.cost.t_route;
+    c.p_top = cfg.predictor.p_top;
+    c.p_active = cfg.predictor.p_active;
+    c.queue_depth = cfg.predictor.queue_depth;
+    c.ce = cfg.stages.ce;
+    c.er = cfg.stages.er;
+    c.pre = cfg.stages.pre;
+    c.ba = cfg.stages.ba;
+    c.seed = cfg.seed;
+    return c;
+}
+
 SimOutput simulate(const GateTrace& trace, const SimConfig& cfg) {
     const ValidationReport rep = validate_config(cfg);
     if (!rep.ok())
@@ -253,29 +281,7 @@ SimOutput simulate(const GateTrace& trace, const SimConfig& cfg) {
                     has[row] = 1;
                 }
             }
-    moeb_config c{};
-    c.num_layers = L;
-    c.experts = E;
-    c.top_k = s.top_k;
-    c.batch = B;
-    c.alpha = cfg.router.alpha;
-    c.slots = cfg.cache.slots_per_layer;
-    c.window = cfg.cache.history_window;
-    c.policy = cfg.cache.policy == CachePolicy::LRU ? 1 : 0;
-    c.init_fill = cfg.cache.init_fill == InitFill::FirstSlots ? 0 : cfg.cache.init_fill == InitFill::SeededRandom ? 1 : 2;
-    c.t_attn = cfg.cost.t_attn;
-    c.t_gpu = cfg.cost.t_gpu;
-    c.t_cpu_token = cfg.cost.t_cpu_token;
-    c.t_load = cfg.cost.t_load;
-    c.t_route = cfg.cost.t_route;
-    c.p_top = cfg.predictor.p_top;
-    c.p_active = cfg.predictor.p_active;
-    c.queue_depth = cfg.predictor.queue_depth;
-    c.ce = cfg.stages.ce;
-    c.er = cfg.stages.er;
-    c.pre = cfg.stages.pre;
-    c.ba = cfg.stages.ba;
-    c.seed = cfg.seed;
+    const moeb_config c = to_moeb_config(cfg);
     moeb_result* r = nullptr;
     throw_status(moeb_simulate(&c, scores.data(), any_pred ? pred.data() : nullptr, any_pred ? has.data() : nullptr,
                                iters, 0, &r));

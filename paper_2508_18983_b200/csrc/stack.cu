@@ -1546,6 +1546,28 @@ int moeb_get_decisions_json(moeb_stack* s, char** json) {
   });
 }
 
+static_assert(sizeof(moeb_step_record) == sizeof(StepRec) && offsetof(moeb_step_record, load) == offsetof(StepRec, load) &&
+                  offsetof(moeb_step_record, evict_expert) == offsetof(StepRec, ev_e),
+              "moeb_step_record mirrors the device StepRec");
+static_assert(sizeof(moeb_token_record) == sizeof(TokRec) && offsetof(moeb_token_record, kept) == offsetof(TokRec, kept),
+              "moeb_token_record mirrors the device TokRec");
+
+int moeb_get_decisions(moeb_stack* s, moeb_step_record* steps, moeb_token_record* toks, size_t cap_steps,
+                       size_t* n_steps) {
+  return guarded([&] {
+    if (!s->rec_cap) throw Error(4, "stack was created without MOEB_MODEL_LOG_STEPS");
+    MOEB_CUDA(cudaDeviceSynchronize());
+    EngineState st;
+    MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
+    check_log_capacity(s, st.seq);
+    const size_t n = st.seq;
+    *n_steps = n;
+    const size_t k = std::min(n, cap_steps);
+    if (steps && k) MOEB_CUDA(cudaMemcpy(steps, s->recs.p, k * sizeof(StepRec), cudaMemcpyDeviceToHost));
+    if (toks && k) MOEB_CUDA(cudaMemcpy(toks, s->toks.p, k * s->B * sizeof(TokRec), cudaMemcpyDeviceToHost));
+  });
+}
+
 int moeb_get_scores(moeb_stack* s, float* out, size_t cap, size_t* n) {
   return guarded([&] {
     if (!s->rec_cap) throw Error(4, "stack was created without MOEB_MODEL_LOG_STEPS");
