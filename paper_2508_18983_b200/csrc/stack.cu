@@ -19,6 +19,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -1238,6 +1239,8 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // is left to it
   S->ffn_grid = S->spec ? sms - 1 : sms;
   S->serial = serial_mode_requested();
+  if (S->serial && !getenv("MOEB_SERIAL"))
+    fprintf(stderr, "moeb: profiler detected, serial pipeline mode (set MOEB_SERIAL=0 to override)\n");
   MOEB_CUDA(cudaStreamSynchronize(s));
   S->copier = std::thread([S] { S->copy_loop(); });
 }
@@ -1276,6 +1279,16 @@ static void launch_pdl(const void* fn, dim3 grid, dim3 block, size_t smem, cudaS
 // wait for this step's FFN) are only owed to later steps.
 static void serial_wait_uploads(moeb_stack* S, cudaStream_t s, uint64_t seq) {
   MOEB_CUDA(cudaStreamSynchronize(s));
+  // the copy thread must have ISSUED entry A's copies before the FFN launch:
+  // a profiler holds every API call (the copy thread's too) while it
+  // measures a kernel, and the FFN depends on those copies
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*reinterpret_cast<volatile uint64_t*>(S->ack) < 2 * seq - 1) {
+    if (S->copier_error) throw Error(5, S->copier_msg);
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+      throw Error(5, "serial mode: the copy thread did not take the step's upload commands");
+    std::this_thread::yield();
+  }
   const MailEntry* ea = &S->ring[(2 * seq - 1) % kRing];
   const MailEntry* eb = &S->ring[(2 * seq) % kRing];
   const uint64_t va = ea->seq, vb = eb->seq;
