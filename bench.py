@@ -620,28 +620,38 @@ def run_ours(args):
 
 # ----------------------------------------------------------------- CPU path
 
-def cpu_path(scores, x_host, n_tokens, nthreads):
+def cpu_path(scores, x_host, n_tokens, nthreads, cfg_d=None, model_d=None):
     """The reference CPU path: reference-library decisions + CPU fp32 layer arithmetic.
 
     Decisions: the reference's simulate() (oracle/_ref, compiled from
-    /root/reference) when present, else the oracle's C port; at batch 1 the
-    per-layer selections are the windows' selected sets. Arithmetic: oracle
-    cpu_moe.c over bf16 weights in host RAM, every host thread.
-    Returns (ms_per_token, kind, cores, sample).
+    /root/reference) when present, else the oracle's C port, over all tokens
+    (single-threaded, as the reference runs); the per-token selections for
+    the arithmetic come from the oracle's per-step records (== the reference's
+    decisions: tests/test_golden.py). Arithmetic: oracle/cpu_moe.c (fp32 over
+    bf16 weights in host RAM, persistent pool over every host thread, AVX2)
+    for the last n_tokens tokens, every token of the batch separately.
+    Returns (ms_per_token, kind, cores, sample, host_weight_gbs).
     """
     sys.path.insert(0, os.path.join(REPO, "oracle"))
     import pyoracle as po
 
-    L, E, B = CFG["num_layers"], CFG["experts"], CFG["batch"]
-    d, F, S = MODEL["d_model"], MODEL["ffn"], MODEL["shared_ffn"]
+    cfg_d = cfg_d or CFG
+    model_d = model_d or MODEL
+    L, E, B = cfg_d["num_layers"], cfg_d["experts"], cfg_d["batch"]
+    d, F, S = model_d["d_model"], model_d["ffn"], model_d["shared_ffn"]
+    sg, renorm, rscale = model_d.get("shared_gate", 0), model_d.get("renormalize", 0), model_d.get("routed_scale", 1.0)
     T = scores.shape[0]
-    cfg = po.SimCfg(**{k: v for k, v in CFG.items()})
+    cfg = po.SimCfg(**{k: v for k, v in cfg_d.items()})
     use_ref = po.ref() is not None
-    t0 = time.perf_counter()
-    out = (po.ref_simulate if use_ref else po.simulate)(cfg, scores, timeline=True)
-    dec_s = time.perf_counter() - t0
+    if use_ref:
+        dec_s = po.ref_simulate_seconds(cfg, scores)  # simulate() alone, timed inside the library
+    else:
+        t0 = time.perf_counter()
+        po.simulate(cfg, scores, timeline=False)
+        dec_s = time.perf_counter() - t0
     dec_ms_token = dec_s * 1e3 / T
-    wins = {(w[0], w[1]): w[5] for w in out["windows"]}
+    steps = po.simulate(cfg, scores, steps=True, timeline=False)["steps"]
+    sel_of = {(r["it"], r["layer"]): [t["sel"] for t in r["tok"]] for r in steps}
 
     cm = C.CDLL(os.path.join(REPO, "oracle", "libcpumoe.so"))
     cm.cpu_synth.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, C.c_void_p, C.c_int]
@@ -676,38 +686,48 @@ def cpu_path(scores, x_host, n_tokens, nthreads):
     sample = list(range(T - n_tokens, T))
     for l in range(L):
         tensor(("r", l), (l << 20) | (0xFFFF << 4), E * d, d)
-        sh = np.empty(3 * S * d, dtype=np.uint16)
-        for m in range(3):
-            cm.cpu_synth(seed, (l << 20) | (0xFFFE << 4) | m, S * d, d if m < 2 else S, sh[m * S * d:].ctypes.data,
-                         nthreads)
-        cache[("s", l)] = sh
+        if sg:
+            tensor(("g", l), (l << 20) | (0xFFFD << 4), d, d)
+        if S:
+            sh = np.empty(3 * S * d, dtype=np.uint16)
+            for m in range(3):
+                cm.cpu_synth(seed, (l << 20) | (0xFFFE << 4) | m, S * d, d if m < 2 else S,
+                             sh[m * S * d:].ctypes.data, nthreads)
+            cache[("s", l)] = sh
         for it in sample:
-            for e in wins[(it, l)]:
-                expert(l, e)
+            for sel in sel_of[(it, l)]:
+                for e in sel:
+                    expert(l, e)
     logits = np.zeros(E, dtype=np.float32)
     y = np.zeros(d, dtype=np.float32)
     cm.cpu_bytes_touched()
     t0 = time.perf_counter()
     for it in sample:
-        x = np.ascontiguousarray(x_host[it, 0]).astype(np.float32)
-        xb = (x.view(np.uint32) + np.uint32(0x7FFF) + ((x.view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
-        for l in range(L):
-            sel = wins[(it, l)]
-            ptrs = (C.c_void_p * len(sel))(*[expert(l, e).ctypes.data for e in sel])
-            wts = np.array([scores[it, l, 0, e] for e in sel], dtype=np.float32)
-            xn = np.empty(d, dtype=np.uint16)
-            cm.cpu_moe_layer(xb.ctypes.data, d, F, S, E, cache[("r", l)].ctypes.data, cache[("s", l)].ctypes.data,
-                             None, ptrs, wts.ctypes.data, len(sel), logits.ctypes.data, y.ctypes.data,
-                             xn.ctypes.data, nthreads)
-            xb = xn
+        for t in range(B):
+            x = np.ascontiguousarray(x_host[it, t]).astype(np.float32)
+            xb = (x.view(np.uint32) + np.uint32(0x7FFF) + ((x.view(np.uint32) >> 16) & 1) >> 16).astype(np.uint16)
+            for l in range(L):
+                sel = sel_of[(it, l)][t]
+                ptrs = (C.c_void_p * len(sel))(*[expert(l, e).ctypes.data for e in sel])
+                w = np.array([scores[it, l, t, e] for e in sel], dtype=np.float64)
+                if renorm:
+                    w = w / w.sum()
+                wts = (w * rscale).astype(np.float32)
+                xn = np.empty(d, dtype=np.uint16)
+                cm.cpu_moe_layer(xb.ctypes.data, d, F, S, E, cache[("r", l)].ctypes.data,
+                                 cache[("s", l)].ctypes.data if S else None,
+                                 cache[("g", l)].ctypes.data if sg else None, ptrs, wts.ctypes.data, len(sel),
+                                 logits.ctypes.data, y.ctypes.data, xn.ctypes.data, nthreads)
+                xb = xn
     arith_s = time.perf_counter() - t0
     host_gbs = cm.cpu_bytes_touched() / arith_s / 1e9
-    ms_token = arith_s * 1e3 / len(sample) + dec_ms_token
+    ms_token = arith_s * 1e3 / len(sample) + dec_ms_token  # per decode step (B tokens)
     kind = "reference" if use_ref else "port"
     sample_desc = (f"decisions: {'reference simulate() (oracle/_ref)' if use_ref else 'oracle C port'} over all "
-                   f"{T} tokens ({dec_ms_token:.3f} ms/token, 1 thread); arithmetic: oracle/cpu_moe.c fp32 over "
-                   f"bf16 host weights, last {len(sample)} tokens x {L} layers ({arith_s * 1e3 / len(sample):.1f} "
-                   f"ms/token, {nthreads} threads, {host_gbs:.1f} GB/s of host weight reads)")
+                   f"{T} steps ({dec_ms_token:.3f} ms/step, 1 thread); arithmetic: oracle/cpu_moe.c fp32 over "
+                   f"bf16 host weights, last {len(sample)} steps x {B} tokens x {L} layers "
+                   f"({arith_s * 1e3 / len(sample):.1f} ms/step, {nthreads} threads, {host_gbs:.1f} GB/s of host "
+                   f"weight reads)")
     return ms_token, kind, nthreads, sample_desc, host_gbs
 
 

@@ -278,7 +278,7 @@ typedef struct moeb_kernel_stats {
   double route_ms, ffn_ms;        /* route = fused router gate + decision launch */
   uint64_t route_launches, ffn_launches;
   uint64_t route_bytes, ffn_bytes, ffn_planned;
-  uint64_t prof_ns[16];           /* device phase timers of the decision launch */
+  uint64_t prof_ns[32];           /* device phase timers of the decision launch (make PROFILE=1) */
 } moeb_kernel_stats;
 int moeb_get_kernel_stats(moeb_stack* s, moeb_kernel_stats* out);
 int moeb_reset_kernel_stats(moeb_stack* s);

@@ -180,6 +180,18 @@ def ref_simulate(cfg: SimCfg, scores, pred=None, has_pred=None, timeline=True):
     return _take_json(lib, lib.ref_free, p)
 
 
+def ref_simulate_seconds(cfg: SimCfg, scores):
+    """Wall time of the reference simulate() alone (oracle/_ref), seconds."""
+    scores = np.ascontiguousarray(scores, dtype=np.float64)
+    c = cfg.to_c()
+    lib = ref()
+    lib.ref_simulate_ns.restype = C.c_uint64
+    ns = lib.ref_simulate_ns(C.byref(c), _dptr(scores), C.c_uint64(scores.shape[0]))
+    if not ns:
+        raise RuntimeError("reference simulate() failed")
+    return ns * 1e-9
+
+
 def ref_report_from_trace_file(cfg: SimCfg, path: str):
     """The reference's load_trace() + simulate() + build_report() on a JSONL file."""
     lib = ref()

@@ -166,6 +166,23 @@ char* ref_simulate_json(const orc_config* c, const double* scores, const double*
   }
 }
 
+// Wall time (ns) of the reference's simulate() alone on a trace — the CPU
+// decision path's cost, without verify_timeline (an O(N^2) test auditor) or
+// the JSON marshalling. Returns 0 on error.
+std::uint64_t ref_simulate_ns(const orc_config* c, const double* scores, std::uint64_t iters) {
+  try {
+    const GateTrace tr = to_trace(c, scores, nullptr, nullptr, iters);
+    const SimConfig cfg = to_cfg(c);
+    const auto t0 = std::chrono::steady_clock::now();
+    const SimOutput out = simulate(tr, cfg);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (out.metrics.iterations != iters) return 0;
+    return (std::uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count();
+  } catch (const std::exception&) {
+    return 0;
+  }
+}
+
 // route (+ optional coalesce) on one batch; JSON with per-token records.
 char* ref_route_json(const double* scores, std::uint32_t B, std::uint32_t E,
                      const std::uint8_t* mask, std::uint32_t k, double alpha, int coalesce) {

@@ -373,7 +373,7 @@ class KernelStats(C.Structure):
     _fields_ = [("route_ms", C.c_double), ("ffn_ms", C.c_double),
                 ("route_launches", C.c_uint64), ("ffn_launches", C.c_uint64),
                 ("route_bytes", C.c_uint64), ("ffn_bytes", C.c_uint64), ("ffn_planned", C.c_uint64),
-                ("prof_ns", C.c_uint64 * 16)]
+                ("prof_ns", C.c_uint64 * 32)]
 
 
 def generate_trace(L, E, B, iters, seed, hot_fraction=0.125, hot_mass=0.8, persistence=0.92, concentration=1.5):

@@ -211,6 +211,64 @@ __device__ inline void route_token(DecideSmem* sm, uint32_t t, uint64_t resident
   sm->nsub[t] = (uint8_t)ns;
 }
 
+// The same pass 2 for token t, bit-parallel on one warp: lane l handles
+// ranks l and l + 32. Every list of the reference is in rank order, so the
+// rank-space masks (bit r = the expert at rank r is in the set) give each
+// entry's output position by a popcount of the lower ranks — no serial scan.
+__device__ __forceinline__ uint32_t popc_below(uint64_t m, uint32_t r) {
+  return (uint32_t)__popcll(m & ((1ULL << r) - 1ULL));
+}
+__device__ inline void route_token_warp(DecideSmem* sm, uint32_t t, uint64_t resident, uint32_t E,
+                                        uint32_t k, uint64_t C) {
+  const uint32_t lane = (uint32_t)lane_id();
+  const uint64_t free_set = resident | C;
+  const uint8_t* order = sm->order[t];
+  const uint64_t top = sm->top[t], low = sm->low[t], alt = sm->alt[t];
+  const uint32_t r0 = lane, r1 = lane + 32;
+  const bool v0 = r0 < E, v1 = r1 < E;
+  const uint32_t x0 = v0 ? order[r0] : 0u, x1 = v1 ? order[r1] : 0u;
+  const bool a0 = v0 && r0 < k, a1 = v1 && r1 < k;  // active ranks
+  const uint64_t top_r = ballot64(a0 && has(top, x0), a1 && has(top, x1));
+  const uint64_t lowfree_r = ballot64(a0 && has(low, x0) && has(free_set, x0), a1 && has(low, x1) && has(free_set, x1));
+  const uint64_t blow_r = ballot64(a0 && has(low, x0) && !has(free_set, x0), a1 && has(low, x1) && !has(free_set, x1));
+  const uint64_t alt_r = ballot64(v0 && !a0 && has(alt, x0) && has(free_set, x0),
+                                  v1 && !a1 && has(alt, x1) && has(free_set, x1));
+  const uint32_t nt = __popcll(top_r), nf = __popcll(lowfree_r), m = __popcll(blow_r);
+  const uint32_t na = __popcll(alt_r);
+  const uint32_t covered = m < na ? m : na;
+  const uint32_t kept = m - covered;
+  auto place = [&](uint32_t r, uint32_t x) {
+    const uint64_t b = 1ULL << r;
+    if (top_r & b) {
+      sm->sel[t][popc_below(top_r, r)] = (uint8_t)x;
+    } else if (lowfree_r & b) {
+      sm->sel[t][nt + popc_below(lowfree_r, r)] = (uint8_t)x;
+    } else if (blow_r & b) {
+      const uint32_t j = popc_below(blow_r, r);
+      if (j < kept) {  // the strongest uncovered lows are kept
+        sm->sel[t][nt + nf + j] = (uint8_t)x;
+        sm->kept[t][j] = (uint8_t)x;
+      } else {         // the weakest are replaced, pairwise with the alternatives
+        sm->sub_d[t][j - kept] = (uint8_t)x;
+      }
+    } else if (alt_r & b) {
+      const uint32_t j = popc_below(alt_r, r);
+      if (j < covered) {
+        sm->sel[t][nt + nf + kept + j] = (uint8_t)x;
+        sm->sub_c[t][j] = (uint8_t)x;
+      }
+    }
+  };
+  if (v0) place(r0, x0);
+  if (v1) place(r1, x1);
+  if (lane == 0) {
+    sm->nsel[t] = (uint8_t)(nt + nf + m);
+    sm->nkept[t] = (uint8_t)kept;
+    sm->nsub[t] = (uint8_t)covered;
+  }
+  __syncwarp();
+}
+
 // router.cpp:154-248: fixed-point coalescing, warp 0. The candidate scan
 // (ascending x, replace on more others, or equal others with higher score)
 // is the lexicographic max of (others, score, -x) over candidates whose
@@ -506,14 +564,14 @@ __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, Nex
 // Called by warp 0 as soon as the demand-load / BA-stream lists are final
 // (before the GPU task clock, deferrals and prefetch), so the caller can hand
 // the uploads to the copy engine early.
-// classified(): called by every thread right after classification (before
-// routing), with the pre-route residency untouched — the stack publishes the
-// experts certain to be selected there (speculative FFN start).
+// classified(): called by warp 2 right after classification, concurrently with
+// routing on warp 0, with the pre-route residency snapshot — the stack
+// publishes the experts certain to be selected there (speculative FFN start).
 // plan_ready(): called by warp 0 once the executing layer's outcome (hits,
 // loads, BA split, deferred admissions) is final, before the prefetch phase.
 struct NoHook {
   __device__ void operator()(DecideSmem*, uint32_t, uint32_t) const {}
-  __device__ void classified(DecideSmem*) const {}
+  __device__ void classified(DecideSmem*, uint64_t) const {}
   __device__ void plan_ready(DecideSmem*) const {}
 };
 
@@ -582,42 +640,74 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   __syncthreads();
   mark(4);
-  on_loads.classified(sm);
-
+  // route pass 2 (router.cpp:114-149), one warp per token; C (the union of
+  // the batch's top-score experts, router.cpp:105-112) computed by every warp
   if (cfg.er) {
-    if (tid == 0) {
-      uint64_t C = 0;
-      for (uint32_t t = 0; t < B; ++t) C |= sm->top[t];
-      sm->C = C;
-    }
-    __syncthreads();
-    for (uint32_t t = warp; t < B; t += nw)
-      if (lane == 0) route_token(sm, t, mask, E, k);
-    __syncthreads();
-    // coalescing is a no-op for a single token: every candidate's batch count
-    // is 0, never above the occupant's (router.cpp:203-228)
-    if (warp == 0 && B > 1) coalesce_warp(sm, B, E, k, mask, sc->cnt);
-    __syncthreads();
+    uint64_t C = 0;
+    for (uint32_t t = 0; t < B; ++t) C |= sm->top[t];
+    if (tid == 0) sm->C = C;
+    for (uint32_t t = warp; t < B; t += nw) route_token_warp(sm, t, mask, E, k, C);
   } else {
     // plain_top_k (router.cpp:35-39)
     for (uint32_t t = warp; t < B; t += nw) {
+      if ((uint32_t)lane < k) sm->sel[t][lane] = sm->order[t][lane];
       if (lane == 0) {
-        for (uint32_t r = 0; r < k; ++r) sm->sel[t][r] = sm->order[t][r];
         sm->nsel[t] = (uint8_t)k;
         sm->nsub[t] = 0;
         sm->nkept[t] = 0;
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
+  mark(17);
 
-  mark(5);
-  if (warp == 1 && want_next) {
-    predict_queue_warp(cx, sm, nx);
-    asm volatile("bar.arrive 2, 64;" ::: "memory");
+  // ---- fork. warp 0 routes and runs the order-dependent rest; alongside it
+  //   warp 1: the next-layer predictor + queue ranking (barrier 2),
+  //   warp 2: the speculative plan of the certain experts (hook; barrier 3),
+  //   warp 3: mean scores -> record_scores -> window averages (barrier 4).
+  // record_scores (pipeline.cpp:191) reads only this step's scores and
+  // nothing before the first admission reads the history, so recording it
+  // beside the routing is the same computation as recording it after.
+  const bool want_pred = want_next;
+  if (warp == 1) {
+    if (want_pred) {
+      predict_queue_warp(cx, sm, nx);
+      asm volatile("bar.arrive 2, 64;" ::: "memory");
+    }
+    return;
+  }
+  if (warp == 2) {
+    on_loads.classified(sm, mask);
+    asm volatile("bar.arrive 3, 64;" ::: "memory");
+    return;
+  }
+  if (warp == 3) {
+    // mean over tokens in token order (pipeline.cpp:79-91)
+    for (uint32_t e = lane; e < E; e += 32) {
+      double m = 0.0;
+      for (uint32_t t = 0; t < B; ++t) m += sm->s[t][e];
+      sm->mean[e] = m / (double)B;
+    }
+    __syncwarp();
+    record_scores_warp(cx.ls, cx.hist_l, cfg.window, E, sm->mean);
+    if (cfg.policy == 0) {
+      // window averages of the executing layer (after recording) and of the
+      // prefetch target (unchanged by this step unless it is this layer)
+      for (uint32_t e = lane; e < E; e += 32) {
+        sm->avg[e] = window_average(cx.ls, cx.hist_l, cfg.window, E, e);
+        if (want_next && cx.tls != cx.ls) sm->tavg[e] = window_average(cx.tls, cx.thist, cfg.window, E, e);
+      }
+    }
+    asm volatile("bar.arrive 4, 64;" ::: "memory");
     return;
   }
   if (warp != 0) return;  // the rest is order-dependent: warp 0 in lock-step
+
+  // coalescing is a no-op for a single token: every candidate's batch count
+  // is 0, never above the occupant's (router.cpp:203-228)
+  if (cfg.er && B > 1) coalesce_warp(sm, B, E, k, mask, sc->cnt);
+  __syncwarp();
+  mark(5);
 
   // ---- hit accounting + batch_of (pipeline.cpp:176-189)
   // lane t <-> token t (B <= 32): selection masks, counts by ballot
@@ -637,13 +727,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     n_kept = __reduce_add_sync(0xffffffffu, nk);
     batch_counts(m, B, E, sc->cnt);
   }
-  // mean over tokens in token order (pipeline.cpp:79-91)
-  for (uint32_t e = lane; e < E; e += 32) {
-    double m = 0.0;
-    for (uint32_t t = 0; t < B; ++t) m += sm->s[t][e];
-    sm->mean[e] = m / (double)B;
-  }
-  __syncwarp();
+  mark(28);
   if (lane == 0) {
     Counters& c = st->c;
     if (cfg.er) { c.subs += n_subs; c.kept_low += n_kept; }
@@ -653,18 +737,16 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   LayerState* ls = cx.ls;
   double* hist_l = cx.hist_l;
-  record_scores_warp(ls, hist_l, cfg.window, E, sm->mean);  // pipeline.cpp:191
-  // window averages (ScoreWindow) are computed on the first admission that
-  // needs them: the history does not change again in this step
-  bool avg_ready = cfg.policy != 0;
+  // window averages: warp 3 recorded this step's mean and computed them
+  bool avg_ready = false;
   auto avg = [&]() -> const double* {
     if (!avg_ready) {
-      for (uint32_t e = lane; e < E; e += 32) sm->avg[e] = window_average(ls, hist_l, cfg.window, E, e);
-      __syncwarp();
+      asm volatile("bar.sync 4, 64;" ::: "memory");
       avg_ready = true;
     }
     return sm->avg;
   };
+  mark(29);
 
   // residents: shield + touch; misses -> demand set (pipeline.cpp:196-205)
   const uint64_t route_end = sc->route_end, attn_end = sc->attn_end;
@@ -673,25 +755,29 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   const uint64_t distinct = ballot64(c0, c1);
   const uint64_t res_sel = distinct & mask;
   const uint64_t miss = distinct & ~mask;
-  for (uint32_t e = lane; e < E; e += 32)
-    if (has(res_sel, e)) ls->last_access[e] = route_end;
+  {
+    // lists in ascending expert order: lane l places experts l and l + 32 by
+    // a popcount of the lower set bits
+    auto place = [&](uint32_t e) {
+      if (has(res_sel, e)) {
+        ls->last_access[e] = route_end;
+        const uint32_t i = (uint32_t)__popcll(res_sel & (bit(e) - 1ULL));
+        sm->out.res_slot[i] = ls->slot_of[e];
+        sm->out.res[i] = (uint8_t)e;
+      } else if (has(miss, e)) {
+        const uint32_t i = (uint32_t)__popcll(miss & (bit(e) - 1ULL));
+        sc->duid[i] = (uint8_t)e;
+        sc->dbat[i] = sc->cnt[e];
+      }
+    };
+    if ((uint32_t)lane < E) place(lane);
+    if ((uint32_t)lane + 32 < E) place(lane + 32);
+  }
   if (lane == 0) {
     ls->shield |= res_sel;
-    uint32_t n = 0;
-    for (uint64_t m = miss; m; m &= m - 1) {
-      const uint32_t e = __ffsll((long long)m) - 1;
-      sc->duid[n] = (uint8_t)e;
-      sc->dbat[n] = sc->cnt[e];
-      ++n;
-    }
-    sc->ndm = n;
-    uint32_t nr = 0;
-    for (uint64_t m = res_sel; m; m &= m - 1) {
-      const uint32_t e = __ffsll((long long)m) - 1;
-      sm->out.res_slot[nr] = ls->slot_of[e];
-      sm->out.res[nr++] = (uint8_t)e;
-    }
-    sm->out.n_res = nr;
+    sc->ndm = (uint32_t)__popcll(miss);
+    sm->out.n_res = (uint32_t)__popcll(res_sel);
+    sm->out.res_mask = res_sel;
     sm->out.mask_before = mask;
   }
   for (uint32_t e = lane; e < E; e += 32) sm->out.cnt[e] = sc->cnt[e];
@@ -710,6 +796,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     n_cpu = 0;
   }
   __syncwarp();
+  mark(18);
 
   // the per-step record's eviction arrays double as scratch for StepOut
   __shared__ uint8_t ev_layer[2 * kMaxE], ev_e[2 * kMaxE];
@@ -724,6 +811,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   if (lane == 0) { st->cpu_free = cpu_t; st->c.cpu_computed += n_cpu; }
   __syncwarp();
+  mark(19);
 
   // demand loads, serial on PCIe, admitted + shielded (pipeline.cpp:229-240)
   uint64_t ready[kMaxE];
@@ -738,7 +826,9 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   if (lane == 0) { st->pcie_free = pcie_t; st->c.demand += n_load; }
   __syncwarp();
+  mark(20);
   on_loads(sm, n_load, n_cpu);
+  mark(21);
 
   // GPU expert compute (pipeline.cpp:242-266)
   uint64_t gpu_t = st->gpu_free > route_end ? st->gpu_free : route_end;
@@ -777,7 +867,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     ls->shield = 0;  // unshield_layer (pipeline.cpp:276)
   }
   __syncwarp();
+  mark(22);
 
+  // warp 2's speculative plan is out (it read the slots of shielded hits,
+  // which a deferred admission below may now evict)
+  asm volatile("bar.sync 3, 64;" ::: "memory");
   // deferred admissions, FIFO, unshielded, at completion (pipeline.cpp:277-280)
   {
     const uint32_t nd = sm->n_def;
@@ -798,6 +892,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   if (lane == 0) sm->out.completion = completion;
   __syncwarp();
+  mark(23);
   on_loads.plan_ready(sm);
 
   mark(7);
@@ -808,9 +903,8 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     const uint64_t tit = cx.target_it;
     const uint64_t gate = completion + cfg.t_attn;
     LayerState* tls = cx.tls;
-    const double* tavg = nullptr;  // computed on the first prefetch admission
-    if (nw < 2) predict_queue_warp(cx, sm, nx);  // else warp 1 ran it concurrently
-    else asm volatile("bar.sync 2, 64;" ::: "memory");
+    const double* tavg = nullptr;  // warp 3's averages of the target layer
+    asm volatile("bar.sync 2, 64;" ::: "memory");  // warp 1's predictor + queue ranking
     const uint8_t* qorder = sm->qorder;
     const uint64_t tmask = tls->mask;
     uint32_t qn = 0;
@@ -829,15 +923,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       if (lane == 0) log_task(cx.logs, R_PCIE, K_PREFETCH, (int)tl, e, t, t + cfg.t_load, tl, tit);
       t += cfg.t_load;
       issued |= bit(i);
-      if (!tavg && cfg.policy == 0) {
-        if (tl == layer) {
-          tavg = avg();
-        } else {
-          for (uint32_t x = lane; x < E; x += 32) sm->tavg[x] = window_average(tls, cx.thist, cfg.window, E, x);
-          __syncwarp();
-          tavg = sm->tavg;
-        }
-      }
+      if (!tavg && cfg.policy == 0) tavg = (tl == layer) ? avg() : (avg(), sm->tavg);
       const int slot = admit_or_defer(cx, sm, tls, cx.thist, tl, e, t, false, ev_layer, ev_e, tavg);
       if (lane == 0) {
         sm->out.pref[n_pref] = (uint8_t)e;
@@ -861,6 +947,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     __syncwarp();
   }
   mark(8);
+  avg();  // warp 3 has recorded this step's scores (and retired)
   if (lane == 0) {
     sm->out.n_pref = n_pref;
     sm->out.completion = completion;

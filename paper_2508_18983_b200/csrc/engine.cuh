@@ -74,7 +74,7 @@ struct EngineState {
   uint64_t seq;                    // layer-step sequence number (stack mode)
   uint64_t ffn_bytes;              // algorithmic FFN bytes planned (stack mode)
   uint64_t ffn_launches;
-  uint64_t prof[16];               // phase timers of the decision launch (ns, summed)
+  uint64_t prof[32];               // phase timers of the decision launch (ns, summed)
   uint64_t ack_cache;              // last mailbox acknowledgement seen (stack mode)
 };
 
@@ -137,6 +137,7 @@ struct StepOut {
                              // deferred admission may evict a hit afterwards)
   uint32_t pref_layer;
   uint64_t mask_before, completion, resident_done;
+  uint64_t res_mask;         // the hits (set of out.res)
   uint16_t cnt[kMaxE];       // tokens per distinct selected expert
 };
 

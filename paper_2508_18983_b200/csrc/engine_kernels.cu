@@ -182,15 +182,15 @@ __global__ void __launch_bounds__(kThreads, 1) route_kernel(const double* scores
   }
   __syncthreads();
   for (uint32_t t = warp; t < B; t += kWarps) {
-    if (lane != 0) continue;
     if (mode == 2) {
+      if (lane != 0) continue;
       d->nsel[t] = io->nsel[t]; d->nsub[t] = io->nsub[t]; d->nkept[t] = io->nkept[t];
       for (int i = 0; i < kMaxK; ++i) {
         d->sel[t][i] = io->sel[t][i]; d->sub_d[t][i] = io->sub_d[t][i];
         d->sub_c[t][i] = io->sub_c[t][i]; d->kept[t][i] = io->kept[t][i];
       }
     } else {
-      route_token(d, t, resident, E, k);
+      route_token_warp(d, t, resident, E, k, d->C);
     }
   }
   __syncthreads();

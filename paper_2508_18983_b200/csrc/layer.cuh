@@ -133,10 +133,10 @@ struct GateArgs {
   uint32_t B, d, E;
 };
 
-// grid = ceil(rows / 2) with rows = E (+1 for the shared gate); 8 warps:
-// warp w -> row 2*blockIdx + (w & 1), quarter (w >> 1) of d.
+// ng = ceil(rows / 2) gate CTAs with rows = E (+1 for the shared gate), gi the
+// CTA's index among them; 8 warps: warp w -> row 2*gi + (w & 1), quarter (w >> 1) of d.
 // us: [B][d] bf16 scratch in shared memory.
-__device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
+__device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, uint32_t ng) {
   __shared__ float part[4][2][kMaxB];
   __shared__ float inv_rms[kMaxB];
   const int lane = lane_id(), warp = warp_id();
@@ -192,8 +192,8 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
     }
     const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
     reinterpret_cast<uint4*>(us + (size_t)t * d)[c] = ov;
-    if (blockIdx.x == 0) reinterpret_cast<uint4*>(a.u + (size_t)t * d)[c] = ov;
-    if (a.ut && blockIdx.x == (gridDim.x > 1 ? 1u : 0u)) {
+    if (gi == 0) reinterpret_cast<uint4*>(a.u + (size_t)t * d)[c] = ov;
+    if (a.ut && gi == (ng > 1 ? 1u : 0u)) {
       // 16 B chunk (c % 8) of K-block c / 8, row t: chunk position (c ^ t) % 8
       const uint32_t off = (c >> 3) * a.ut_rows * 128u + (t >> 3) * 1024u + (t & 7u) * 128u + (((c ^ t) & 7u) << 4);
       *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(a.ut) + off) = ov;
@@ -201,7 +201,7 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
   }
   __syncthreads();
   const uint32_t rows = a.E + (a.wsg ? 1u : 0u);
-  const uint32_t row = 2 * blockIdx.x + (warp & 1);
+  const uint32_t row = 2 * gi + (warp & 1);
   const uint32_t q = warp >> 1;
   if (row < rows) {
     const uint16_t* w = row < a.E ? a.wg + (size_t)row * d : a.wsg;
@@ -246,7 +246,7 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us) {
   __syncthreads();
   if (threadIdx.x < 2 * B) {
     const uint32_t r = threadIdx.x & 1, t = threadIdx.x >> 1;
-    const uint32_t rr = 2 * blockIdx.x + r;
+    const uint32_t rr = 2 * gi + r;
     if (rr < rows) {
       const float s = ((part[0][r][t] + part[1][r][t]) + part[2][r][t]) + part[3][r][t];
       a.logits[(size_t)t * (a.E + 1) + rr] = s;

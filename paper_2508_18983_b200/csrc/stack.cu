@@ -229,12 +229,12 @@ __device__ __forceinline__ void wait_ring_slot(const DecideArgs& a, uint64_t mse
 // Mailbox entry A of a layer-step (sequence 2*seq-1): the demand loads and
 // BA-streamed experts, published from inside the decision step the moment
 // the lists are final. Entry B (2*seq) carries the prefetches later.
-__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d);
+__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d, uint64_t mask);
 
 struct EarlyPublish {
   const DecideArgs* a;
   DecideKSmem* sm;
-  __device__ void classified(DecideSmem* d) const { publish_spec(*a, sm, d); }
+  __device__ void classified(DecideSmem* d, uint64_t mask) const { publish_spec(*a, sm, d, mask); }
   __device__ void plan_ready(DecideSmem* d) const;
   __device__ void operator()(DecideSmem* d, uint32_t n_load, uint32_t n_cpu) const {
     if (lane_id() == 0) {
@@ -303,8 +303,8 @@ struct EarlyPublish {
 // landed is final: hits are shielded (pipeline.cpp:196-201), so its slot
 // cannot change in this step. Publishing these lets the FFN kernel (already
 // resident via PDL) stream them while the rest of the decision runs.
-__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d) {
-  if (threadIdx.x != 0) return;
+__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d, uint64_t mask) {
+  if (lane_id() != 0) return;  // one lane of warp 2, beside the routing on warp 0
   sm->spec_n = 0;
   sm->spec_set = 0;
   if (!a.spec_plan) return;
@@ -314,7 +314,7 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   // stays in the final plan with no tokens: zero combine weights)
   uint64_t certain = 0;
   for (uint32_t t = 0; t < cfg.B; ++t) certain |= cfg.er ? d->top[t] : d->act[t];
-  certain &= ls->mask;
+  certain &= mask;  // the pre-route snapshot (warp 0 may be admitting meanwhile)
   Plan* sp = a.spec_plan;
   uint32_t n = 0;
   auto item = [&](const uint16_t* w, uint32_t F, uint32_t kind, uint32_t e, float wt) {
@@ -348,21 +348,56 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
 }
 
-// Thread 0 builds the FFN plan and the upload commands in shared memory.
-// The FFN items (and deferred staging->slot copies) of this step; called as
-// soon as the loads and deferred admissions are final, before the prefetch
-// phase (which only touches the prefetch target's state and the copy stream).
+// Warp 0 builds the FFN plan in shared memory as soon as the loads and
+// deferred admissions are final, before the prefetch phase (which only
+// touches the prefetch target's state and the copy stream). Item order: the
+// shared expert, the speculative plan's routed experts (ascending), the other
+// resident hits that are ready (ascending), hits whose (prefetch) upload is
+// still in flight by upload id (the copy stream is FIFO), then the demand
+// loads and the BA-streamed experts in publication order. Lane l places
+// experts l and l + 32 by popcounts over the category masks.
 __device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
   const DevCfg& cfg = sm->cfg;
   const uint32_t B = cfg.B, layer = a.layer;
+  const uint32_t lane = (uint32_t)lane_id();
   DecideSmem* d = &sm->d;
   const StepOut& out = d->out;
   Plan* p = &sm->plan;
   EngineState* st = &sm->st;
   LayerState* ls = &sm->ls;
-  uint32_t n_items = 0;
-  auto add_item = [&](const uint16_t* w, uint32_t F, uint32_t wait, uint32_t kind, uint32_t e) {
-    Item& itm = p->items[n_items++];
+  // residents: lane l takes experts l and l + 32; hit e is out.res[i] with
+  // i = its rank in the (ascending) hit set
+  const uint64_t res_sel = out.res_mask;
+  const uint32_t E = cfg.E;
+  const bool v0 = lane < E && ((res_sel >> lane) & 1), v1 = lane + 32 < E && ((res_sel >> (lane + 32)) & 1);
+  const uint32_t e0 = lane, e1 = lane + 32;
+  // their slots at route time (a deferred admission may since have evicted a hit)
+  const int s0 = v0 ? out.res_slot[__popcll(res_sel & ((1ull << e0) - 1))] : -1;
+  const int s1 = v1 ? out.res_slot[__popcll(res_sel & ((1ull << e1) - 1))] : -1;
+  // uploads already landed (the copy stream is FIFO and copies_done only
+  // grows; read during staging): their slots are plain residents again
+  const uint32_t landed = sm->landed;
+  auto wait_of = [&](int slot) -> uint32_t {
+    const uint32_t w = ls->slot_copy[slot];
+    if (w && (int32_t)(landed - w) >= 0) {
+      ls->slot_copy[slot] = 0;
+      return 0;
+    }
+    return w;
+  };
+  const uint32_t w0 = v0 ? wait_of(s0) : 0u, w1 = v1 ? wait_of(s1) : 0u;
+  const uint64_t spec_m = sm->spec_set;
+  const uint64_t wait_m = ballot64(v0 && w0 != 0, v1 && w1 != 0) & ~spec_m;
+  const uint64_t ready_m = res_sel & ~wait_m & ~spec_m;
+  const uint32_t base = a.shared_w ? 1u : 0u;
+  const uint32_t n_spec = (uint32_t)__popcll(spec_m), n_rdy = (uint32_t)__popcll(ready_m);
+  const uint32_t n_wait = (uint32_t)__popcll(wait_m);
+  __shared__ uint32_t s_wid[kMaxE];
+  if (v0) s_wid[e0] = w0;
+  if (v1) s_wid[e1] = w1;
+  __syncwarp();
+  auto item = [&](uint32_t i, const uint16_t* w, uint32_t F, uint32_t wait, uint32_t kind, uint32_t e) {
+    Item& itm = p->items[i];
     itm.w = w;
     itm.F = F;
     itm.wait = wait;
@@ -370,66 +405,55 @@ __device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
     itm.expert = e;
     itm.n_tok = 0;  // token lists are filled in parallel afterwards (fill_items)
   };
-
-  if (a.shared_w) add_item(a.shared_w, a.S, 0, 0, 0);
-  // the speculative plan's routed experts next, in its (ascending) order
-  for (uint64_t m = sm->spec_set; m; m &= m - 1) {
-    const uint32_t e = __ffsll((long long)m) - 1;
-    add_item(slot_ptr(a, layer, ls->slot_of[e]), a.F, 0, 1, e);
-  }
-  // uploads already landed (the copy stream is FIFO and copies_done only
-  // grows; read during staging): their slots are plain residents again
-  const uint32_t landed = sm->landed;
-  for (uint32_t i = 0; i < out.n_res; ++i) {
-    const int slot = out.res_slot[i];
-    const uint32_t w = ls->slot_copy[slot];
-    if (w && (int32_t)(landed - w) >= 0) ls->slot_copy[slot] = 0;
-  }
-  // residents: ready ones first, then those whose (prefetch) upload is in
-  // flight, ordered by upload id (the copy stream is FIFO)
-  for (int pass = 0; pass < 2; ++pass) {
-    for (uint32_t i = 0; i < out.n_res; ++i) {
-      const uint32_t e = out.res[i];
-      const int slot = out.res_slot[i];
-      const uint32_t wait = ls->slot_copy[slot];
-      if ((wait == 0) != (pass == 0)) continue;
-      if ((sm->spec_set >> e) & 1) continue;  // already first
-      add_item(slot_ptr(a, layer, slot), a.F, wait, 1, e);
+  auto place = [&](uint32_t e, int slot, uint32_t w) {
+    const uint64_t b = 1ull << e, below = b - 1ull;
+    uint32_t i;
+    if (spec_m & b) {
+      i = base + (uint32_t)__popcll(spec_m & below);
+      w = 0;
+    } else if (ready_m & b) {
+      i = base + n_spec + (uint32_t)__popcll(ready_m & below);
+      w = 0;
+    } else {
+      uint32_t r = 0;  // by upload id (unique)
+      for (uint64_t m = wait_m; m; m &= m - 1) r += s_wid[__ffsll((long long)m) - 1] < w;
+      i = base + n_spec + n_rdy + r;
     }
+    item(i, slot_ptr(a, layer, slot), a.F, w, 1, e);
+  };
+  if (v0) place(e0, s0, w0);
+  if (v1) place(e1, s1, w1);
+  if (lane == 0 && a.shared_w) item(0, a.shared_w, a.S, 0, 0, 0);
+  const uint32_t n0 = base + n_spec + n_rdy + n_wait;
+  for (uint32_t i = lane; i < out.n_load; i += 32) item(n0 + i, sm->load_dst[i], a.F, sm->load_id[i], 2, out.load[i]);
+  for (uint32_t i = lane; i < out.n_cpu; i += 32)
+    item(n0 + out.n_load + i, sm->cpu_dst[i], a.F, sm->cpu_id[i], 3, out.cpu[i]);
+  const uint32_t n_items = n0 + out.n_load + out.n_cpu;
+  if (lane == 0) {
+    const int8_t* stage_of = sm->stage_of;
+    uint32_t n_d2d = 0;
+    for (uint32_t i = 0; i < out.n_def; ++i) {
+      const uint32_t e = out.def_e[i];
+      const int slot = out.def_slot[i];
+      if (stage_of[e] < 0 || slot < 0) continue;
+      p->d2d[n_d2d].src = a.staging + (size_t)stage_of[e] * a.expert_elems;
+      p->d2d[n_d2d].dst = slot_ptr(a, layer, slot);
+      ls->slot_copy[slot] = 0;  // filled by this step's FFN epilogue
+      ++n_d2d;
+    }
+    // algorithmic bytes of the FFN launch: every item's weights once, plus
+    // u / x in, x out (bf16) and the fp32 layer output
+    st->ffn_bytes += 4ull * B * a.d * 2 + (uint64_t)B * a.d * 4 + 3ull * a.S * a.d * 2 +
+                     3ull * (n_items - base) * a.F * a.d * 2;
+    st->ffn_launches += 1;
+    p->n_items = n_items;
+    p->n_ready = base + n_spec + n_rdy;
+    p->n_spec = sm->spec_n;
+    p->n_d2d = n_d2d;
+    p->d2d_elems = a.expert_elems;
+    p->seq = (uint32_t)sm->seq;
   }
-  uint32_t n_ready = 0;
-  while (n_ready < n_items && p->items[n_ready].wait == 0) ++n_ready;
-  for (uint32_t i = n_ready + 1; i < n_items; ++i) {
-    Item x = p->items[i];
-    uint32_t j = i;
-    while (j > n_ready && p->items[j - 1].wait > x.wait) { p->items[j] = p->items[j - 1]; --j; }
-    p->items[j] = x;
-  }
-  for (uint32_t i = 0; i < out.n_load; ++i) add_item(sm->load_dst[i], a.F, sm->load_id[i], 2, out.load[i]);
-  for (uint32_t i = 0; i < out.n_cpu; ++i) add_item(sm->cpu_dst[i], a.F, sm->cpu_id[i], 3, out.cpu[i]);
-  const int8_t* stage_of = sm->stage_of;
-  uint32_t n_d2d = 0;
-  for (uint32_t i = 0; i < out.n_def; ++i) {
-    const uint32_t e = out.def_e[i];
-    const int slot = out.def_slot[i];
-    if (stage_of[e] < 0 || slot < 0) continue;
-    p->d2d[n_d2d].src = a.staging + (size_t)stage_of[e] * a.expert_elems;
-    p->d2d[n_d2d].dst = slot_ptr(a, layer, slot);
-    ls->slot_copy[slot] = 0;  // filled by this step's FFN epilogue
-    ++n_d2d;
-  }
-  // algorithmic bytes of the FFN launch: every item's weights once, plus
-  // u / x in, x out (bf16) and the fp32 layer output
-  uint64_t bytes = 4ull * B * a.d * 2 + (uint64_t)B * a.d * 4;
-  for (uint32_t i = 0; i < n_items; ++i) bytes += 3ull * p->items[i].F * a.d * 2;
-  st->ffn_bytes += bytes;
-  st->ffn_launches += 1;
-  p->n_items = n_items;
-  p->n_ready = n_ready;
-  p->n_spec = sm->spec_n;
-  p->n_d2d = n_d2d;
-  p->d2d_elems = a.expert_elems;
-  p->seq = (uint32_t)sm->seq;
+  __syncwarp();
 }
 
 // The prefetch upload commands (mailbox entry B), after the prefetch phase.
@@ -459,7 +483,7 @@ __device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm) {
 // Warp 0, as soon as the step's FFN items are final (before the prefetch
 // phase): build the plan, fill token lists / weights, publish it to global
 // memory and (speculative mode) release it to the running FFN kernel.
-__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm, uint32_t first, uint32_t stride);
+__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm);
 
 __device__ void EarlyPublish::plan_ready(DecideSmem* d) const {
   const DecideArgs& A = *a;
@@ -472,10 +496,17 @@ __device__ void EarlyPublish::plan_ready(DecideSmem* d) const {
     sm->denom[t] = s;
   }
   __syncwarp();
-  if (lane == 0) build_items(A, sm);
+#ifdef MOEB_PROFILE_PHASES
+  uint64_t tq = gtimer();
+  auto pmark = [&](int i) { if (lane == 0) { const uint64_t n = gtimer(); sm->st.prof[i] += n - tq; tq = n; } };
+#else
+  auto pmark = [](int) {};
+#endif
+  build_items(A, sm);
+  pmark(24);
+  fill_items(A, sm);
   __syncwarp();
-  fill_items(A, sm, lane, 32);
-  __syncwarp();
+  pmark(25);
   Plan* gp = A.plan;
   const uint32_t n_items = sm->plan.n_items;
   const uint64_t* src = reinterpret_cast<const uint64_t*>(&sm->plan);
@@ -484,6 +515,7 @@ __device__ void EarlyPublish::plan_ready(DecideSmem* d) const {
   for (uint32_t i = lane; i < words; i += 32) dst[i] = src[i];
   const size_t d0 = offsetof(Plan, d2d) / 8, d1 = d0 + sm->plan.n_d2d * sizeof(D2D) / 8;
   for (uint32_t i = d0 + lane; i < d1; i += 32) dst[i] = src[i];
+  pmark(26);
   if (A.spec_plan) {
     // the FFN kernel (already running its speculative items) takes the final
     // plan from this flag instead of waiting for this kernel to complete:
@@ -496,36 +528,42 @@ __device__ void EarlyPublish::plan_ready(DecideSmem* d) const {
     }
   }
   __syncwarp();
+  pmark(27);
 }
 
-// Token lists and combine weights of every plan item, one thread per item.
-__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm, uint32_t first, uint32_t stride) {
+// Token lists and combine weights of every plan item: lane t holds token t's
+// selection mask, one ballot per item gives its tokens (ascending) and each
+// selecting lane writes its own entry.
+__device__ void fill_items(const DecideArgs& a, DecideKSmem* sm) {
   const uint32_t B = sm->cfg.B;
+  const uint32_t lane = (uint32_t)lane_id();
   const DecideSmem* d = &sm->d;
   Plan* p = &sm->plan;
-  for (uint32_t ii = first; ii < p->n_items; ii += stride) {
+  uint64_t selm = 0;
+  if (lane < B)
+    for (uint32_t i = 0; i < d->nsel[lane]; ++i) selm |= 1ull << d->sel[lane][i];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (uint32_t ii = 0; ii < p->n_items; ++ii) {
     Item& itm = p->items[ii];
     const uint32_t kind = itm.kind, e = itm.expert;
-    uint32_t n = 0;
-    for (uint32_t t = 0; t < B; ++t) {
-      bool sel = kind == 0;
-      if (!sel)
-        for (uint32_t i = 0; i < d->nsel[t]; ++i) sel |= d->sel[t][i] == e;
-      if (!sel) continue;
+    const bool sel = lane < B && (kind == 0 || ((selm >> e) & 1));
+    const uint32_t toks = __ballot_sync(0xffffffffu, sel);
+    if (sel) {
       float wt;
       if (kind == 0) {
-        wt = a.shared_gate ? sm->sg[t] : 1.0f;
+        wt = a.shared_gate ? sm->sg[lane] : 1.0f;
       } else {
-        wt = sm->sc[t][e];
-        if (a.renormalize) wt = __fdiv_rn(wt, sm->denom[t]);
+        wt = sm->sc[lane][e];
+        if (a.renormalize) wt = __fdiv_rn(wt, sm->denom[lane]);
         wt = __fmul_rn(wt, a.routed_scale);
       }
-      itm.tok[n] = (uint8_t)t;
-      itm.wt[n] = wt;
-      ++n;
+      const uint32_t pos = __popc(toks & lt);
+      itm.tok[pos] = (uint8_t)lane;
+      itm.wt[pos] = wt;
     }
-    itm.n_tok = n;
+    if (lane == 0) itm.n_tok = __popc(toks);
   }
+  __syncwarp();
 }
 
 // Router gate (all CTAs) then, in the last CTA to finish, the decision step,
@@ -544,36 +582,34 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   MOEB_T(t_entry);
   __shared__ uint64_t t_plan_g_s;
   uint64_t& t_plan_g = t_plan_g_s;
-  // gate phase: us [B][d] bf16 aliases the decision workspace
-  gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw));
-  MOEB_T(t_gate);
-  DecideKSmem* sm = reinterpret_cast<DecideKSmem*>(smem_raw);
-  __shared__ int s_last;
-  __syncthreads();
 #ifdef MOEB_PROFILE_PHASES
   if (threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(&ga.d.st->prof[14]), (unsigned long long)t_entry);
 #endif
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t t = atomicAdd(ga.ticket, 1u);
-    s_last = (t == gridDim.x - 1);
-    if (s_last) {
-      *ga.ticket = 0;
+  // CTAs 1..G: the router gate (RMSNorm + GEMV rows); CTA 0: the decision.
+  // The decider stages the step's state while the gate runs, then waits for
+  // the gate CTAs' arrivals (they are few and co-resident) instead of the
+  // last gate CTA electing itself after the fact.
+  const uint32_t n_gate = gridDim.x - 1;
+  if (blockIdx.x != 0) {
+    // us [B][d] bf16 aliases the decision workspace
+    gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw), blockIdx.x - 1, n_gate);
+    __syncthreads();
+    if (threadIdx.x == 0) {
       __threadfence();
+      atomicAdd(ga.ticket, 1u);
     }
+    return;
   }
-  __syncthreads();
-  if (!s_last) return;
-
+  DecideKSmem* sm = reinterpret_cast<DecideKSmem*>(smem_raw);
   const DecideArgs& a = ga.d;
   if (a.tl && threadIdx.x == 0) a.tl[3] = globaltimer_ns();
   // the FFN grid counters of this step, zeroed before the FFN kernel (which
-  // may already be resident) can see the speculative plan or the final one;
-  // thread 0 alone, so its release of the spec flag / the kernel boundary
-  // publishes them
-  if (threadIdx.x == 0)
+  // may already be resident) can see the speculative plan or the final one:
+  // fenced before the barrier that precedes both releases
+  if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < (uint32_t)kFfnCtrWords; ++i) a.ffn_ctr[i] = 0;
-  MOEB_T(t_elect);
+    __threadfence();
+  }
   const int warp = warp_id(), lane = lane_id();
   const uint32_t nw = blockDim.x >> 5;
   // stage the step's state: one parallel load phase (it / seq come from the
@@ -600,8 +636,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     const uint64_t* g_h = reinterpret_cast<const uint64_t*>(a.hist + layer * hwords);
     const uint64_t* g_th = reinterpret_cast<const uint64_t*>(a.hist + tl * hwords);
     uint64_t r_st = 0, r_ls = 0, r_tls = 0, r_h[kHw], r_th[kHw];
-    uint32_t r_cd = 0;
-    if (tid == kGdThreads - 1) r_cd = *reinterpret_cast<const volatile uint32_t*>(a.copies_done);
+    const uint32_t r_cd = 0;
     if (tid < kStW) r_st = g_st[tid];
     if (tid < kLsW) r_ls = g_ls[tid];
     if (two && tid < kLsW) r_tls = g_tls[tid];
@@ -629,8 +664,20 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
       }
     }
     if (threadIdx.x == 0) sm->cfg = a.cfg;
-    if (tid == kGdThreads - 1) sm->landed = r_cd;
+    (void)r_cd;
   }
+  MOEB_T(t_staged0);
+  // the router logits and u of this layer: every gate CTA has arrived
+  if (threadIdx.x == 0) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_u32(ga.ticket) < n_gate) {
+      if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 7u); break; }
+    }
+    *ga.ticket = 0;  // reset for the next layer (ordered by this kernel's completion)
+    sm->landed = *reinterpret_cast<const volatile uint32_t*>(a.copies_done);
+  }
+  __syncthreads();
+  MOEB_T(t_gate);
   const uint32_t jobs = want_next ? 2 * B : B;
   for (uint32_t j = warp; j < jobs; j += nw) {
     if (j < B) {
@@ -698,13 +745,13 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     MOEB_T(t_plan);
     t_plan_g = t_plan;
 #ifdef MOEB_PROFILE_PHASES
-    sm->st.prof[0] += t_gate - t_entry;
-    sm->st.prof[1] += t_elect - t_gate;
-    sm->st.prof[2] += t_staged - t_elect;
+    sm->st.prof[0] += t_gate - t_staged0;   // waiting for the gate CTAs after staging
+    sm->st.prof[1] += t_staged0 - t_entry;  // staging (overlaps the gate)
+    sm->st.prof[2] += t_staged - t_gate;    // softmax + scores
     sm->st.prof[3] += t_decided - t_staged;
     sm->st.prof[9] += t_plan - t_decided;
 #endif
-    (void)t_entry; (void)t_gate; (void)t_elect; (void)t_staged; (void)t_decided; (void)t_plan;
+    (void)t_entry; (void)t_gate; (void)t_staged0; (void)t_staged; (void)t_decided; (void)t_plan;
   }
   __syncthreads();
   // publish: prefetch commands -> mapped host ring, state write-back (the
@@ -1389,7 +1436,7 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * kTlWords : nullptr;
     ga.ticket = S->ticket.p;
     if (S->timing) S->tick(s);
-    launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3((rows + 1) / 2), dim3(kGdThreads),
+    launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3(1 + (rows + 1) / 2), dim3(kGdThreads),
                S->gd_smem, s, &ga, kUsePdl && !S->serial);
     MOEB_CUDA(cudaGetLastError());
     if (S->serial) serial_wait_uploads(S, s, a.seq);
@@ -1641,7 +1688,7 @@ int moeb_get_kernel_stats(moeb_stack* s, moeb_kernel_stats* out) {
     out->ffn_launches = s->n_launch_layers;
     out->ffn_bytes = st.ffn_bytes;
     out->ffn_planned = st.ffn_launches;
-    for (int i = 0; i < 16; ++i) out->prof_ns[i] = st.prof[i];
+    for (int i = 0; i < 32; ++i) out->prof_ns[i] = st.prof[i];
     const uint64_t gb = (uint64_t)s->E * s->d * 2 + 2ull * s->B * s->d * 2 + (uint64_t)s->B * (s->E + 1) * 4 +
                         (s->model.shared_gate ? (uint64_t)s->d * 2 : 0);
     out->route_bytes = gb * s->n_launch_layers;

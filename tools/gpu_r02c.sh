@@ -1,15 +1,14 @@
-# decision-step phase split (make PROFILE=1: globaltimer phase counters in
-# the decide kernel) + device-clock timeline of the bench workload
 set -x
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
 C=paper_2508_18983_b200/csrc
-rm -f gpurun_out/phases.log
 make -C $C clean > /dev/null; make -j16 -C $C PROFILE=1 > gpurun_out/build_profile.log 2>&1
+rm -f gpurun_out/phases.log
 for args in "--tokens 24" "--tokens 24 --allhit" "--tokens 12 --batch 32 --allhit"; do
   echo "== $args" >> gpurun_out/phases.log
   timeout 300 python tools/profile_stack.py $args --time >> gpurun_out/phases.log 2>&1
 done
 make -C $C clean > /dev/null; make -j16 -C $C > gpurun_out/build.log 2>&1
-for args in "--tokens 48" "--tokens 24 --allhit" "--tokens 12 --batch 8 --allhit" "--tokens 12 --batch 32 --allhit"; do
+for args in "--tokens 48" "--tokens 24 --allhit"; do
   echo "== $args --timeline" >> gpurun_out/phases.log
   timeout 300 python tools/profile_stack.py $args --timeline >> gpurun_out/phases.log 2>&1
 done

@@ -53,7 +53,10 @@ def main():
               "ms/token wall", round(dt * 1e3 / T, 3))
         n = k["route_launches"] or 1
         names = ["gate", "elect", "stage", "decide", "d:classify", "d:route", "d:hits+record", "d:loads",
-                 "d:prefetch", "plan", "pub:fence", "span", "pub:copy", "early:fence", "-", "start_skew"]
+                 "d:prefetch", "plan", "pub:fence", "span", "pub:copy", "early:fence", "-", "start_skew",
+                 "r:spec_publish", "r:route_tokens", "l:BA", "l:cpu_clock", "l:admit_loads", "l:mailbox_A",
+                 "l:gpu_clock", "l:deferred", "p:build_items", "p:fill_items", "p:plan_copy", "p:fence_release",
+                 "h:counts+mean", "h:record", "-", "-"]
         print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names) if nm != "-"})
     if args.timeline:
         tl = st.timeline().astype(np.int64)
