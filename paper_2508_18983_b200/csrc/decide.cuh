@@ -269,34 +269,57 @@ __device__ inline void route_token_warp(DecideSmem* sm, uint32_t t, uint64_t res
   __syncwarp();
 }
 
-// router.cpp:154-248: fixed-point coalescing, warp 0. The candidate scan
-// (ascending x, replace on more others, or equal others with higher score)
-// is the lexicographic max of (others, score, -x) over candidates whose
-// count beats the occupant's, reduced across lanes.
+// Order-preserving unsigned key of a double (-0.0 folded onto +0.0, as the
+// reference's `>` treats them equal).
+__device__ __forceinline__ uint64_t dkey(double v) {
+  if (v == 0.0) v = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+
+// router.cpp:154-248: fixed-point coalescing, warp 0. The reference scans
+// candidates x ascending and replaces the best on more others, or equal
+// others and a higher score: the winner is the lexicographic max of
+// (others, score, -x) over the candidates whose count beats the occupant's.
+// Each lane evaluates experts lane and lane + 32 (the lower one wins its
+// local ties), then four warp reductions (redux.sync) find the winner:
+// max count, max score (hi then lo word of the order-preserving key), min x.
+// The band of every token (beta > 0, R <= s < L) is a bitmask computed once.
 __device__ inline void coalesce_warp(DecideSmem* sm, uint32_t B, uint32_t E, uint32_t k,
                                      uint64_t resident, uint16_t* cnt) {
-  const int lane = lane_id();
+  const uint32_t lane = (uint32_t)lane_id();
   // batch counts: a token's selection is a set, so cnt[e] = number of
   // tokens (lanes, B <= 32) whose selection mask holds e
   {
     uint64_t m = 0;
-    if ((uint32_t)lane < B)
+    if (lane < B)
       for (uint32_t i = 0; i < sm->nsel[lane]; ++i) m |= bit(sm->sel[lane][i]);
     batch_counts(m, B, E, cnt);
   }
+  __shared__ uint64_t s_band[kMaxB];
+  for (uint32_t t = 0; t < B; ++t) {
+    const double* s = sm->s[t];
+    const double beta = sm->beta[t], thR = sm->thR[t], thL = sm->thL[t];
+    const bool b0 = lane < E && beta > 0.0 && s[lane] >= thR && s[lane] < thL;
+    const bool b1 = lane + 32 < E && beta > 0.0 && s[lane + 32] >= thR && s[lane + 32] < thL;
+    const uint64_t bm = ballot64(b0, b1) & ~sm->act[t];
+    if (lane == 0) s_band[t] = bm;
+  }
   __syncwarp();
+  const uint64_t avail = resident | sm->C;
   bool changed = true;
   while (changed) {
     changed = false;
     for (uint32_t t = 0; t < B; ++t) {
+      const uint64_t low = sm->low[t];
+      if (!low) continue;
       const double* s = sm->s[t];
+      const uint64_t band = s_band[t];
       uint64_t selm = 0;
       for (uint32_t i = 0; i < sm->nsel[t]; ++i) selm |= bit(sm->sel[t][i]);
-      const uint64_t actm = sm->act[t];
-      const double beta = sm->beta[t], thR = sm->thR[t], thL = sm->thL[t];
       for (uint32_t r = 0; r < k; ++r) {
         const uint32_t orig = sm->order[t][r];
-        if (!has(sm->low[t], orig)) continue;
+        if (!has(low, orig)) continue;
         int kept_pos = -1, sub_pos = -1;
         for (uint32_t i = 0; i < sm->nkept[t]; ++i)
           if (sm->kept[t][i] == orig) { kept_pos = (int)i; break; }
@@ -310,31 +333,33 @@ __device__ inline void coalesce_warp(DecideSmem* sm, uint32_t B, uint32_t E, uin
           occupant = sm->sub_c[t][sub_pos];
         }
         const uint32_t occ_others = cnt[occupant] - 1u;
-        // lane-parallel candidate search
-        uint32_t b_oth = 0, b_x = 0xffffffffu;
-        double b_s = 0.0;
-        for (uint32_t x = lane; x < E; x += 32) {
-          const double sx = s[x];
-          if (!(beta > 0.0 && sx >= thR && sx < thL)) continue;
-          if (has(actm, x) || has(selm, x)) continue;
+        const uint64_t cand = band & ~selm;
+        // local best of the lane's two experts (x0 < x1: x0 wins ties)
+        uint32_t bc = 0, bx = 0xffffffffu;  // bc = others + 1 (0: none)
+        uint64_t bk = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t x = lane + 32u * h;
+          if (x >= E || !has(cand, x)) continue;
           const uint32_t others = cnt[x];
-          if (!(has(resident, x) || has(sm->C, x) || others > 0)) continue;
-          if (others <= occ_others) continue;
-          if (b_x == 0xffffffffu || others > b_oth || (others == b_oth && sx > b_s)) {
-            b_oth = others; b_s = sx; b_x = x;
+          if (!(has(avail, x) || others > 0) || others <= occ_others) continue;
+          const uint64_t key = dkey(s[x]);
+          if (bx == 0xffffffffu || others + 1 > bc || (others + 1 == bc && key > bk)) {
+            bc = others + 1;
+            bk = key;
+            bx = x;
           }
         }
-        for (int o = 16; o > 0; o >>= 1) {
-          const uint32_t o2 = __shfl_xor_sync(0xffffffffu, b_oth, o);
-          const double s2 = __shfl_xor_sync(0xffffffffu, b_s, o);
-          const uint32_t x2 = __shfl_xor_sync(0xffffffffu, b_x, o);
-          const bool take = x2 != 0xffffffffu &&
-                            (b_x == 0xffffffffu || o2 > b_oth ||
-                             (o2 == b_oth && (s2 > b_s || (s2 == b_s && x2 < b_x))));
-          if (take) { b_oth = o2; b_s = s2; b_x = x2; }
-        }
-        if (b_x == 0xffffffffu) continue;  // best == occupant
-        const uint32_t best = b_x;
+        const uint32_t mc = __reduce_max_sync(0xffffffffu, bc);
+        if (mc == 0) continue;  // best == occupant
+        const bool m1 = bc == mc;
+        const uint32_t hi = m1 ? (uint32_t)(bk >> 32) : 0u;
+        const uint32_t mhi = __reduce_max_sync(0xffffffffu, hi);
+        const bool m2 = m1 && hi == mhi;
+        const uint32_t lo = m2 ? (uint32_t)bk : 0u;
+        const uint32_t mlo = __reduce_max_sync(0xffffffffu, lo);
+        const bool m3 = m2 && lo == mlo;
+        const uint32_t best = __reduce_min_sync(0xffffffffu, m3 ? bx : 0xffffffffu);
         __syncwarp();
         if (lane == 0) {
           for (uint32_t i = 0; i < sm->nsel[t]; ++i)
@@ -465,87 +490,98 @@ __device__ inline int admit_or_defer(const StepCtx& cx, DecideSmem* sm, LayerSta
 __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, NextSmem* nx) {
   const DevCfg& cfg = *cx.cfg;
   EngineState* st = cx.st;
-  const int lane = lane_id();
+  const uint32_t lane = (uint32_t)lane_id();
   const uint32_t E = cfg.E, B = cfg.B, k = cfg.k;
-  for (uint32_t e = lane; e < E; e += 32) sm->merged[e] = 0.0;
+  // (1) lane t: argmax_first (prefetch.cpp:12-20: max value, lowest index)
+  // of token t's vector — the supplied prediction, or the true next scores;
+  // experts visited in a lane-rotated order (no bank conflicts), the
+  // (value desc, index asc) rule makes the order irrelevant
+  __shared__ uint8_t s_amax[kMaxB], s_head[kMaxB];
+  if (lane < B) {
+    const bool supplied = (sm->next_has_pred >> lane) & 1ULL;
+    const double* v = supplied ? sm->np[lane] : sm->ns[lane];
+    double bv = 0.0;
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t j = 0; j < E; ++j) {
+      uint32_t e = j + lane;
+      if (e >= E) e -= E;
+      const double x = v[e];
+      if (bi == 0xffffffffu || x > bv || (x == bv && e < bi)) { bv = x; bi = e; }
+    }
+    s_amax[lane] = (uint8_t)bi;
+  }
   __syncwarp();
-  uint64_t rs[4] = {st->rng[0], st->rng[1], st->rng[2], st->rng[3]};
-  for (uint32_t t = 0; t < B; ++t) {
-    const double* tn = sm->ns[t];
-    const bool supplied = (sm->next_has_pred >> t) & 1ULL;
-    // kind_of / argmax of the true vector
-    const uint64_t ntop = nx->top[t], nact = nx->act[t];
-    uint32_t head;
-    int kind;
-    // argmax_first (prefetch.cpp:12-20): max value, lowest index
-    auto argmax_first = [&](const double* v) -> uint32_t {
-      double bv = 0.0;
-      uint32_t bi = 0xffffffffu;
-      for (uint32_t e = lane; e < E; e += 32)
-        if (bi == 0xffffffffu || v[e] > bv) { bv = v[e]; bi = e; }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
-        const uint32_t i2 = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (i2 != 0xffffffffu && (bi == 0xffffffffu || v2 > bv || (v2 == bv && i2 < bi))) { bv = v2; bi = i2; }
-      }
-      return bi;
-    };
-    uint32_t tt = 0;
-    if (supplied) {
-      head = argmax_first(sm->np[t]);
-      kind = has(ntop, head) ? 0 : (has(nact, head) ? 1 : 2);
-      for (uint32_t e = lane; e < E; e += 32) {
-        const double v = sm->np[t][e];
-        if (sm->merged[e] < v) sm->merged[e] = v;
-      }
-    } else {
-      const uint32_t n_top = __popcll(ntop);
-      if (rng_double(rs) < cfg.p_top && n_top > 0) {
-        const uint32_t pick = rng_below_small(rs, n_top);
-        uint32_t c = 0;
-        head = 0;
-        for (uint32_t r = 0; r < k; ++r) {
-          const uint32_t e = nx->order[t][r];
-          if (has(ntop, e)) { if (c == pick) { head = e; break; } ++c; }
-        }
-        kind = 0;
+  // (2) lane 0: the heads, in token order from the one predictor stream
+  // (prefetch.cpp:34-83; draws only for tokens without a supplied vector)
+  if (lane == 0) {
+    uint64_t rs[4] = {st->rng[0], st->rng[1], st->rng[2], st->rng[3]};
+    Counters& c = st->c;
+    for (uint32_t t = 0; t < B; ++t) {
+      const uint64_t ntop = nx->top[t], nact = nx->act[t];
+      uint32_t head;
+      int kind;
+      if ((sm->next_has_pred >> t) & 1ULL) {
+        head = s_amax[t];
+        kind = has(ntop, head) ? 0 : (has(nact, head) ? 1 : 2);
+        c.trace_supplied++;
       } else {
-        const uint64_t lows = nact & ~ntop;
-        const uint32_t n_low = __popcll(lows);
-        if (rng_double(rs) < cfg.p_active && n_low > 0) {
-          const uint32_t pick = rng_below_small(rs, n_low);
-          uint32_t c = 0;
+        const uint32_t n_top = __popcll(ntop);
+        if (rng_double(rs) < cfg.p_top && n_top > 0) {
+          uint32_t pick = rng_below_small(rs, n_top);
           head = 0;
           for (uint32_t r = 0; r < k; ++r) {
             const uint32_t e = nx->order[t][r];
-            if (has(lows, e)) { if (c == pick) { head = e; break; } ++c; }
+            if (has(ntop, e) && pick-- == 0) { head = e; break; }
           }
-          kind = 1;
+          kind = 0;
         } else {
-          const uint64_t allm = E >= 64 ? ~0ULL : ((1ULL << E) - 1ULL);
-          const uint64_t inact = allm & ~nact;
-          uint32_t pick = rng_below_small(rs, __popcll(inact));
-          uint64_t m = inact;
-          for (uint32_t i = 0; i < pick; ++i) m &= m - 1;
-          head = __ffsll((long long)m) - 1;
-          kind = 2;
+          const uint64_t lows = nact & ~ntop;
+          const uint32_t n_low = __popcll(lows);
+          if (rng_double(rs) < cfg.p_active && n_low > 0) {
+            uint32_t pick = rng_below_small(rs, n_low);
+            head = 0;
+            for (uint32_t r = 0; r < k; ++r) {
+              const uint32_t e = nx->order[t][r];
+              if (has(lows, e) && pick-- == 0) { head = e; break; }
+            }
+            kind = 1;
+          } else {
+            const uint64_t allm = E >= 64 ? ~0ULL : ((1ULL << E) - 1ULL);
+            const uint64_t inact = allm & ~nact;
+            uint32_t pick = rng_below_small(rs, __popcll(inact));
+            uint64_t m = inact;
+            for (uint32_t i = 0; i < pick; ++i) m &= m - 1;
+            head = __ffsll((long long)m) - 1;
+            kind = 2;
+          }
         }
+        c.draws++;
       }
-      tt = argmax_first(tn);
-      for (uint32_t e = lane; e < E; e += 32) {
-        const double v = (e == head) ? tn[tt] : ((e == tt) ? tn[head] : tn[e]);
-        if (sm->merged[e] < v) sm->merged[e] = v;
-      }
-    }
-    __syncwarp();
-    if (lane == 0) {
-      Counters& c = st->c;
-      if (supplied) c.trace_supplied++; else c.draws++;
       if (kind == 0) c.head_top++; else if (kind == 1) c.head_active++; else c.head_inactive++;
+      s_head[t] = (uint8_t)head;
     }
-    __syncwarp();
+    st->rng[0] = rs[0]; st->rng[1] = rs[1]; st->rng[2] = rs[2]; st->rng[3] = rs[3];
   }
-  if (lane == 0) { st->rng[0] = rs[0]; st->rng[1] = rs[1]; st->rng[2] = rs[2]; st->rng[3] = rs[3]; }
+  __syncwarp();
+  // (3) lane-per-expert merge: elementwise max over tokens (pipeline.cpp:
+  // 412-425) of each token's predicted vector — supplied verbatim, or the
+  // true vector with the head and the true argmax swapped
+  for (uint32_t e = lane; e < E; e += 32) {
+    double m = 0.0;
+    for (uint32_t t = 0; t < B; ++t) {
+      double v;
+      if ((sm->next_has_pred >> t) & 1ULL) {
+        v = sm->np[t][e];
+      } else {
+        const double* tn = sm->ns[t];
+        const uint32_t head = s_head[t], tt = s_amax[t];
+        v = (e == head) ? tn[tt] : ((e == tt) ? tn[head] : tn[e]);
+      }
+      if (m < v) m = v;
+    }
+    sm->merged[e] = m;
+  }
+  __syncwarp();
   // build_queue (prefetch.cpp:85-115): rank merged, first `depth` non-resident
   uint8_t* qorder = sm->qorder;
   for (uint32_t e = lane; e < E; e += 32) {
@@ -557,7 +593,6 @@ __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, Nex
     }
     qorder[r] = (uint8_t)e;
   }
-  __syncwarp();
   __syncwarp();
 }
 

@@ -429,7 +429,9 @@ inline FfnLaunch ffn_splitk_config(uint32_t d, uint32_t E, uint32_t top_k, int c
   // step k -> warp k % NC: the stage count is a multiple of NC
   (void)deterministic;
   const uint32_t nc = L.threads / 32 - 1;
-  L.stages = std::max<uint32_t>(nc, kSkStages / nc * nc);
+  uint32_t want = kSkStages;
+  if (const char* v = getenv("MOEB_SK_STAGES")) want = (uint32_t)atoi(v);  // experiment knob
+  L.stages = std::min<uint32_t>(kSkMaxStages, std::max<uint32_t>(nc, want / nc * nc));
   const uint32_t max_items = 1 + std::min(E, top_k);
   L.plan_smem = (uint32_t)((offsetof(Plan, items) + (size_t)max_items * sizeof(Item) + 15) & ~(size_t)15);
   L.x_smem = 0;

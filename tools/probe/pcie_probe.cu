@@ -7,11 +7,12 @@
 #include <cstdint>
 #include <vector>
 #include <algorithm>
+#include <cmath>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
 
 template <int U>
-__global__ void zc_copy(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16) {
+__global__ void __launch_bounds__(1024) zc_copy(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16) {
   size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t base = tid; base < n16; base += stride * U) {
@@ -31,7 +32,7 @@ __global__ void zc_copy(const int4* __restrict__ src, int4* __restrict__ dst, si
 
 // contiguous per-CTA chunking (better for PCIe read combining?)
 template <int U>
-__global__ void zc_copy_chunk(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16) {
+__global__ void __launch_bounds__(1024) zc_copy_chunk(const int4* __restrict__ src, int4* __restrict__ dst, size_t n16) {
   size_t per = (n16 + gridDim.x - 1) / gridDim.x;
   size_t lo = blockIdx.x * per, hi = min(n16, lo + per);
   for (size_t base = lo + threadIdx.x; base < hi; base += (size_t)blockDim.x * U) {
@@ -62,10 +63,15 @@ int main() {
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
+  // best-of-reps duration (ms); NaN when a launch or the stream failed, so
+  // a failed configuration can never print as a bandwidth
   auto timeit = [&](auto fn, int reps) {
     float best = 1e9;
     for (int r = 0; r < reps; ++r) {
-      cudaEventRecord(a, s); fn(); cudaEventRecord(b, s); cudaEventSynchronize(b);
+      cudaEventRecord(a, s); fn();
+      if (cudaGetLastError() != cudaSuccess) return NAN;
+      cudaEventRecord(b, s);
+      if (cudaEventSynchronize(b) != cudaSuccess) return NAN;
       float ms; cudaEventElapsedTime(&ms, a, b); best = std::min(best, ms);
     }
     return best;
