@@ -88,6 +88,18 @@ typedef struct moeb_model {
  * layout; later stacks then pass it without this flag (with
  * MOEB_MODEL_DOWN_T when moeb_host_pool_flags says so). */
 #define MOEB_MODEL_FILL_POOL 32u
+/* The paper's partial-forward predictor for stage Pre in
+ * weight-driven mode (no logits trace): the FFN also emits the partial
+ * forward x + shared expert + resident hits (no uploaded or BA-streamed
+ * expert), the next layer's gate CTAs apply that layer's router to it, and
+ * the next layer's decision step first runs the previous step's
+ * schedule_prefetch with every token's prediction supplied
+ * (prefetch.cpp:43-49) — the same state transition as the reference
+ * (nothing happens between a step's prefetch and the next gate event).
+ * PredictorStats count the heads against the true scores
+ * (moeb_metrics.trace_supplied / head_top / head_active / head_inactive).
+ * Batch-1 split-K and tensor-core FFN shapes only. */
+#define MOEB_MODEL_PREDICTOR 128u
 
 typedef struct moeb_engine moeb_engine; /* decision engine only (simulate path) */
 typedef struct moeb_stack moeb_stack;   /* full MoE decode stack */
@@ -240,6 +252,10 @@ int moeb_get_metrics(moeb_stack* s, moeb_metrics* m);
  * plus the fp32 router scores each step used (for oracle replay). */
 int moeb_get_decisions_json(moeb_stack* s, char** json);
 int moeb_get_scores(moeb_stack* s, float* out, size_t cap, size_t* n);
+/* MOEB_MODEL_PREDICTOR: the predicted fp32 scores each step's prefetch used
+ * ([steps][B][E], the step that was the prefetch target; NaN rows: no
+ * prediction for that step). */
+int moeb_get_pred_scores(moeb_stack* s, float* out, size_t cap, size_t* n);
 /* The same per-step records as plain structs (what the C++ MoeStack wrapper,
  * include/moesched/moe_layer.hpp, turns into RouteResult / load-list form).
  * One moeb_step_record per (iteration, layer), batch moeb_token_records each,

@@ -274,6 +274,7 @@ def simulate(cfg: Config, scores, pred=None, has_pred=None, steps=False):
 
 
 MODEL_LOG_STEPS = 1
+MODEL_PREDICTOR = 128  # the partial-forward predictor (include/moesched_b200.h)
 
 # Model presets (dimensions of the BASELINE.json configs)
 DSV2_LITE = dict(d_model=2048, ffn=1408, shared_ffn=2816, shared_gate=0, renormalize=0, routed_scale=1.0)
@@ -286,9 +287,10 @@ class Stack:
 
     def __init__(self, cfg: Config, d_model, ffn, shared_ffn=0, shared_gate=0, renormalize=0,
                  routed_scale=1.0, weight_seed=7, log_steps=False, device=0, weights_host=None,
-                 time_kernels=False, trace_timeline=False, deterministic=False, fill_pool=False, pool_flags=0):
+                 time_kernels=False, trace_timeline=False, deterministic=False, fill_pool=False, pool_flags=0,
+                 predictor=False):
         flags = (MODEL_LOG_STEPS if log_steps else 0) | (2 if time_kernels else 0) | (4 if trace_timeline else 0) | \
-            (16 if deterministic else 0) | (32 if fill_pool else 0) | pool_flags
+            (16 if deterministic else 0) | (32 if fill_pool else 0) | pool_flags | (MODEL_PREDICTOR if predictor else 0)
         m = Model(d_model=d_model, ffn=ffn, shared_ffn=shared_ffn, shared_gate=shared_gate,
                   renormalize=renormalize, routed_scale=routed_scale, weight_seed=weight_seed,
                   max_batch=cfg.batch, flags=flags)
@@ -353,6 +355,15 @@ class Stack:
         out = np.zeros(n.value, dtype=np.float32)
         check(lib().moeb_get_scores(self.h, out.ctypes.data_as(C.POINTER(C.c_float)), C.c_size_t(n.value),
                                     C.byref(n)))
+        return out
+
+    def pred_scores(self):
+        """Predicted scores each step's prefetch used ([steps*B*E] fp32; NaN: none)."""
+        n = C.c_size_t()
+        check(lib().moeb_get_pred_scores(self.h, None, C.c_size_t(0), C.byref(n)))
+        out = np.zeros(n.value, dtype=np.float32)
+        check(lib().moeb_get_pred_scores(self.h, out.ctypes.data_as(C.POINTER(C.c_float)), C.c_size_t(n.value),
+                                         C.byref(n)))
         return out
 
     def io_stats(self):

@@ -29,6 +29,13 @@ struct StepCtx {
   uint32_t target_layer;
   uint64_t target_it;
   uint64_t* prof;        // nullable: phase timers (globaltimer deltas)
+  // predictor mode (the partial-forward predictor): the
+  // step leaves its schedule_prefetch pending (the prediction for the next
+  // layer needs this layer's FFN), and the next step runs it first
+  // (run_pending), with every token's prediction supplied in sm->np.
+  uint32_t defer_prefetch;
+  uint32_t run_pending;
+  StepRec* prev_rec;     // nullable: the previous step's record (gets the pending phase's issues)
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -503,7 +510,7 @@ __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, Nex
     double bv = 0.0;
     uint32_t bi = 0xffffffffu;
     for (uint32_t j = 0; j < E; ++j) {
-      uint32_t e = j + lane;
+      uint32_t e = j + lane % E;
       if (e >= E) e -= E;
       const double x = v[e];
       if (bi == 0xffffffffu || x > bv || (x == bv && e < bi)) { bv = x; bi = e; }
@@ -596,6 +603,108 @@ __device__ inline void predict_queue_warp(const StepCtx& cx, DecideSmem* sm, Nex
   __syncwarp();
 }
 
+// The previous step's schedule_prefetch (pipeline.cpp:293-344) into THIS
+// layer, run by warp 0 at the start of this step in predictor mode: the
+// same state transition as at the end of the previous step (nothing happens
+// in between in the reference's state machine), with every token's
+// prediction supplied (prefetch.cpp:43-49: verbatim, head = first argmax,
+// RNG untouched) and the head kinds counted against this step's true scores.
+// Issues, evictions and the queue go to the previous step's record.
+__device__ inline void deferred_prefetch(const StepCtx& cx, DecideSmem* sm, uint8_t* ev_layer, uint8_t* ev_e) {
+  const DevCfg& cfg = *cx.cfg;
+  EngineState* st = cx.st;
+  const uint32_t lane = (uint32_t)lane_id();
+  const uint32_t E = cfg.E, B = cfg.B, layer = cx.layer;
+  const uint64_t it = cx.it;
+  LayerState* ls = cx.ls;
+  // heads (lane t) and their kinds, then the per-expert max merge
+  __shared__ uint8_t s_kind[kMaxB];
+  if (lane < B) {
+    const double* v = sm->np[lane];
+    double bv = 0.0;
+    uint32_t bi = 0xffffffffu;
+    for (uint32_t j = 0; j < E; ++j) {
+      uint32_t e = j + lane % E;
+      if (e >= E) e -= E;
+      const double x = v[e];
+      if (bi == 0xffffffffu || x > bv || (x == bv && e < bi)) { bv = x; bi = e; }
+    }
+    s_kind[lane] = has(sm->top[lane], bi) ? 0 : (has(sm->act[lane], bi) ? 1 : 2);
+  }
+  for (uint32_t e = lane; e < E; e += 32) {
+    double m = 0.0;
+    for (uint32_t t = 0; t < B; ++t) m = m < sm->np[t][e] ? sm->np[t][e] : m;
+    sm->merged[e] = m;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    Counters& c = st->c;
+    for (uint32_t t = 0; t < B; ++t) {
+      c.trace_supplied++;
+      if (s_kind[t] == 0) c.head_top++; else if (s_kind[t] == 1) c.head_active++; else c.head_inactive++;
+    }
+  }
+  uint8_t* qorder = sm->qorder;
+  for (uint32_t e = lane; e < E; e += 32) {
+    const double v = sm->merged[e];
+    uint32_t r = 0;
+    for (uint32_t j = 0; j < E; ++j) {
+      const double vj = sm->merged[j];
+      r += (vj > v) || (vj == v && j < e);
+    }
+    qorder[r] = (uint8_t)e;
+  }
+  __syncwarp();
+  // build_queue + issue against the gate of this layer (completion of the
+  // previous step + t_attn), from max(pcie_free, its resident_done)
+  const uint64_t gate = st->now + cfg.t_attn;
+  uint32_t qn = 0;
+  uint8_t qe[kMaxE];
+  if (cfg.depth > 0)
+    for (uint32_t r = 0; r < E && qn < cfg.depth; ++r) {
+      const uint32_t e = qorder[r];
+      if (!has(ls->mask, e)) qe[qn++] = (uint8_t)e;
+    }
+  uint64_t t = st->pcie_free > st->pf_resident_done ? st->pcie_free : st->pf_resident_done;
+  uint64_t issued = 0;
+  uint32_t n_pref = 0;
+  bool avg_done = false;
+  for (uint32_t i = 0; i < qn; ++i) {
+    if (t + cfg.t_load > gate) break;
+    const uint32_t e = qe[i];
+    if (has(ls->mask, e)) continue;
+    t += cfg.t_load;
+    issued |= bit(i);
+    if (!avg_done && cfg.policy == 0) {  // this layer's averages before this step records
+      for (uint32_t x = lane; x < E; x += 32) sm->tavg[x] = window_average(ls, cx.hist_l, cfg.window, E, x);
+      __syncwarp();
+      avg_done = true;
+    }
+    const int slot = admit_or_defer(cx, sm, ls, cx.hist_l, layer, e, t, false, ev_layer, ev_e, sm->tavg);
+    if (lane == 0) {
+      sm->out.pref[n_pref] = (uint8_t)e;
+      sm->out.pref_slot[n_pref] = (int8_t)(slot >= 0 ? slot : -1);
+    }
+    ++n_pref;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (t > st->pcie_free) st->pcie_free = t;
+    st->q_valid = 1;
+    st->q_layer = layer;
+    st->q_it = it;
+    st->q_n = qn;
+    st->q_issued = issued;
+    for (uint32_t i = 0; i < qn; ++i) st->q_e[i] = qe[i];
+    st->c.issued += n_pref;
+    st->c.prefetch += n_pref;
+    sm->out.pref_layer = layer;
+    sm->out.n_pref = n_pref;
+    st->pf_pending = 0;
+  }
+  __syncwarp();
+}
+
 // Called by warp 0 as soon as the demand-load / BA-stream lists are final
 // (before the GPU task clock, deferrals and prefetch), so the caller can hand
 // the uploads to the copy engine early.
@@ -608,6 +717,7 @@ struct NoHook {
   __device__ void operator()(DecideSmem*, uint32_t, uint32_t) const {}
   __device__ void classified(DecideSmem*, uint64_t) const {}
   __device__ void plan_ready(DecideSmem*) const {}
+  __device__ void prefetched(DecideSmem*) const {}
 };
 
 template <class Hook = NoHook>
@@ -630,32 +740,12 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   auto mark = [](int) {};  // phase timers compiled out (build with -DMOEB_PROFILE_PHASES)
 #endif
   if (tid == 0) {
-    const uint64_t start = st->now;
-    // attention + gate (pipeline.cpp:133-145)
-    const uint64_t attn_end = start + cfg.t_attn;
-    log_task(cx.logs, R_GPU, K_ATTN, -1, 0, start, attn_end, layer, it);
-    st->gpu_free = attn_end;
-    if (st->q_valid && st->q_layer == layer && st->q_it == it) {
-      const uint64_t all = st->q_n >= 64 ? ~0ULL : ((1ULL << st->q_n) - 1ULL);
-      st->c.cancelled += __popcll(all & ~st->q_issued);
-      st->q_valid = 0;
-    }
-    // routing on CPU (pipeline.cpp:147-152)
-    const uint64_t route_start = attn_end > st->cpu_free ? attn_end : st->cpu_free;
-    const uint64_t route_end = route_start + cfg.t_route;
-    log_task(cx.logs, R_CPU, K_ROUTE, -1, 0, route_start, route_end, layer, it);
-    st->cpu_free = route_end;
-    sc->attn_end = attn_end;
-    sc->route_end = route_end;
     sm->n_def = 0;
     sm->out.n_load = sm->out.n_cpu = sm->out.n_pref = sm->out.n_def = sm->out.n_evict = 0;
     sm->out.n_res = 0;
   }
-  __syncthreads();
-  const uint64_t mask = cx.ls->mask;  // snapshot the router sees (pipeline.cpp:154-155)
-
   // classify every token (and the prefetch target's tokens) — warp per token
-  const bool want_next = cfg.pre && cx.has_target;
+  const bool want_next = cfg.pre && cx.has_target && !cx.defer_prefetch;
   const uint32_t jobs = want_next ? 2 * B : B;
   for (uint32_t j = warp; j < jobs; j += nw) {
     uint64_t a, tp, lw, al;
@@ -673,6 +763,54 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       if (lane == 0) { nx->act[t] = a; nx->top[t] = tp; }
     }
   }
+  __syncthreads();
+  // predictor mode: the previous step's prefetch into this layer first (its
+  // admissions are part of the residency this step's router sees)
+  __shared__ uint8_t pev_layer[2 * kMaxE], pev_e[2 * kMaxE];
+  if (cx.run_pending && warp == 0) {
+    StepRec* pr = cx.prev_rec;
+    uint32_t n0 = pr ? pr->n_evict : 0u;
+    if (lane == 0) sm->out.n_evict = n0;  // append to the previous step's evictions
+    __syncwarp();
+    deferred_prefetch(cx, sm, pev_layer, pev_e);
+    const uint32_t n1 = sm->out.n_evict < 2 * kMaxE ? sm->out.n_evict : 2 * kMaxE;
+    if (pr) {
+      for (uint32_t i = n0 + lane; i < n1; i += 32) {
+        pr->ev_layer[i] = pev_layer[i];
+        pr->ev_e[i] = pev_e[i];
+      }
+      for (uint32_t i = lane; i < sm->out.n_pref; i += 32) pr->pref[i] = sm->out.pref[i];
+      if (lane == 0) {
+        pr->n_evict = (uint8_t)n1;
+        pr->n_pref = (uint8_t)sm->out.n_pref;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) sm->out.n_evict = 0;
+  }
+  // predictor mode: the previous step's prefetch commands go out now (warp 0)
+  if (cx.defer_prefetch && warp == 0) on_loads.prefetched(sm);
+  if (tid == 0) {
+    const uint64_t start = st->now;
+    // attention + gate (pipeline.cpp:133-145)
+    const uint64_t attn_end = start + cfg.t_attn;
+    log_task(cx.logs, R_GPU, K_ATTN, -1, 0, start, attn_end, layer, it);
+    st->gpu_free = attn_end;
+    if (st->q_valid && st->q_layer == layer && st->q_it == it) {
+      const uint64_t all = st->q_n >= 64 ? ~0ULL : ((1ULL << st->q_n) - 1ULL);
+      st->c.cancelled += __popcll(all & ~st->q_issued);
+      st->q_valid = 0;
+    }
+    // routing on CPU (pipeline.cpp:147-152)
+    const uint64_t route_start = attn_end > st->cpu_free ? attn_end : st->cpu_free;
+    const uint64_t route_end = route_start + cfg.t_route;
+    log_task(cx.logs, R_CPU, K_ROUTE, -1, 0, route_start, route_end, layer, it);
+    st->cpu_free = route_end;
+    sc->attn_end = attn_end;
+    sc->route_end = route_end;
+  }
+  __syncthreads();
+  const uint64_t mask = cx.ls->mask;  // snapshot the router sees (pipeline.cpp:154-155)
   __syncthreads();
   mark(4);
   // route pass 2 (router.cpp:114-149), one warp per token; C (the union of
@@ -983,6 +1121,14 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   mark(8);
   avg();  // warp 3 has recorded this step's scores (and retired)
+  if (lane == 0 && cx.defer_prefetch) {
+    // predictor mode: this step's schedule_prefetch runs at the start of the
+    // next step (which has the prediction); nothing past the trace end
+    st->pf_pending = (cfg.pre && cx.has_target) ? 1u : 0u;
+    st->pf_layer = cx.target_layer;
+    st->pf_it = cx.target_it;
+    st->pf_resident_done = resident_done;
+  }
   if (lane == 0) {
     sm->out.n_pref = n_pref;
     sm->out.completion = completion;

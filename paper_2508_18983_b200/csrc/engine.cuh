@@ -76,6 +76,8 @@ struct EngineState {
   uint64_t ffn_launches;
   uint64_t prof[32];               // phase timers of the decision launch (ns, summed)
   uint64_t ack_cache;              // last mailbox acknowledgement seen (stack mode)
+  uint32_t pf_pending, pf_layer;   // predictor mode: a schedule_prefetch awaits its prediction
+  uint64_t pf_it, pf_resident_done;
 };
 
 // Log records (layouts == moeb_task / moeb_window / moeb_eviction).

@@ -82,6 +82,9 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(ReplayArgs a) {
       cx.has_target = tit < a.iters;
       cx.target_layer = tl;
       cx.target_it = tit;
+      cx.defer_prefetch = 0;
+      cx.run_pending = 0;
+      cx.prev_rec = nullptr;
       if (cfg.pre && cx.has_target) {
         const size_t row0 = ((size_t)tit * L + tl) * B;
         const double* ns = a.scores + row0 * E;

@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   __shared__ uint32_t s_hdr[kSkMaxStages][2];  // {item << 16 | 1, row} or {0, 0} = end
   __shared__ uint32_t s_pre[kMaxItems + 1];  // row prefix of a phase's items
   __shared__ uint32_t s_u[1024];             // the activation (bf16 pairs), d <= 2048
+  // partial forward for the next layer's predictor (x_pred): the consumer
+  // warps' partials at the snapshot marker, summed in warp order
+  __shared__ float s_yloc[2048];
+  __shared__ volatile uint32_t s_turn;
+  __shared__ uint32_t s_snap;
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
   const uint32_t G = gridDim.x, c = blockIdx.x;
@@ -105,6 +110,8 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   uint32_t dlo, dhi;
   share(d, c, G, dlo, dhi);
   if (threadIdx.x == 0) {
+    s_turn = 0;
+    s_snap = 0;
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -228,8 +235,25 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
     }
     const uint32_t n_items = p->n_items, n_ready = p->n_ready;
     stream(n_spec, n_ready, kFfnGuCtr, false);
+    // snapshot marker (one per consumer warp) right before the first item
+    // that is not the shared expert or a resident hit: the partial forward
+    auto snapshot = [&]() {
+      if (lane == 0) {
+        for (int w = 0; w < NC; ++w) {
+          const uint32_t st = acquire();
+          s_hdr[st][0] = 0;
+          s_hdr[st][1] = 1;
+          mbar_arrive(&full_bar[st]);
+          ++k;
+        }
+        s_snap = 1;
+      }
+      __syncwarp();
+    };
+    const uint32_t n_local = a.x_pred ? p->n_local : n_items;
     // the uploaded experts, as they land; units from the item's own counter
     for (uint32_t ii = n_ready; ii < n_items; ++ii) {
+      if (ii == n_local) snapshot();
       if (lane == 0 && p->items[ii].wait) {
         const uint64_t t0 = globaltimer_ns();
         while ((int32_t)(ld_acquire_u32(a.copies_done) - p->items[ii].wait) < 0) {
@@ -275,6 +299,25 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       mbar_wait(&full_bar[st], (k / S) & 1);
       const uint32_t h0 = s_hdr[st][0];
       if (h0 == 0) {
+        if (s_hdr[st][1] == 1) {
+          // snapshot: add this warp's partial into s_yloc, warps in order
+          while (s_turn != cw) {}
+#pragma unroll
+          for (int j = 0; j < kSkMaxYChunks; ++j)
+            if ((uint32_t)j < ych)
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                float& dst = s_yloc[j * 256 + lane * 8 + q];
+                dst = cw == 0 ? y[j][q] : dst + y[j][q];
+              }
+          __syncwarp();
+          __threadfence_block();
+          if (lane == 0) {
+            s_turn = cw + 1;
+            mbar_arrive(&empty_bar[st]);
+          }
+          continue;
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty_bar[st]);
         break;
@@ -332,6 +375,8 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   if (a.tl && threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(&a.tl[13]), (unsigned long long)globaltimer_ns());
   // this CTA's partial y (warps summed in order) -> global partials [G][d]
   float* part = a.h;
+  float* part_loc = a.h + (size_t)G * d;  // partial-forward partials (x_pred)
+  const bool snap = s_snap != 0;
   {
     const float* scratch = reinterpret_cast<const float*>(ring);
     for (uint32_t o = threadIdx.x; o < d; o += blockDim.x) {
@@ -339,6 +384,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
 #pragma unroll
       for (int w = 1; w < NC; ++w) s += scratch[(size_t)w * d + o];
       part[(size_t)c * d + o] = s;
+      if (snap) part_loc[(size_t)c * d + o] = s_yloc[o];
     }
   }
   __threadfence();
@@ -387,6 +433,30 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       for (uint32_t j = 0; j < nseg; ++j) yv += seg[threadIdx.x * nseg + j];
       a.x_out[o] = f32_to_bf16_rne(xin_pre + yv);
       a.y_out[o] = yv;
+      if (a.x_pred && !snap) a.x_pred[o] = f32_to_bf16_rne(xin_pre + yv);  // every item was local
+    }
+    if (a.x_pred && snap) {
+      // the same CTA-ordered sum over the snapshot partials
+      __syncthreads();
+      for (uint32_t t = threadIdx.x; t < no * nseg; t += blockDim.x) {
+        const uint32_t o = dlo + t / nseg, j = t % nseg;
+        float v[kSeg];
+#pragma unroll
+        for (uint32_t q = 0; q < kSeg; ++q) {
+          const uint32_t cc = j * kSeg + q;
+          v[q] = cc < G ? __ldcg(part_loc + (size_t)cc * d + o) : 0.f;
+        }
+        float sum = v[0];
+#pragma unroll
+        for (uint32_t q = 1; q < kSeg; ++q) sum += v[q];
+        seg[t] = sum;
+      }
+      __syncthreads();
+      if (threadIdx.x < no) {
+        float yv = 0.f;
+        for (uint32_t j = 0; j < nseg; ++j) yv += seg[threadIdx.x * nseg + j];
+        a.x_pred[dlo + threadIdx.x] = f32_to_bf16_rne(xin_pre + yv);
+      }
     }
   }
   // deferred admissions: staging -> slot (every CTA passed the barrier above,

@@ -91,6 +91,8 @@ struct FfnTArgs {
   const uint16_t* x_in;    // [B][d]
   uint16_t* x_out;         // [B][d]
   float* y_out;            // [B][d]
+  uint16_t* x_pred;        // [B][d] or null: bf16(x_in + the shared expert's and resident hits'
+                           // contributions) — the partial forward the next layer's predictor reads
   float* h;                // [kMaxItems][B][Fmax]
   uint32_t* ctr;           // [0,kMaxItems) item gate_up done, [kMaxItems] d2d barrier, [kMaxItems+1] exit
   const uint32_t* copies_done;

@@ -557,24 +557,31 @@ __global__ void __launch_bounds__(kUmThreads, 1) ffn_umma_kernel(const __grid_co
     uint32_t lo, hi;
     share(B * d, c, G, lo, hi);
     const uint32_t np = s_pb[s_ni];
+    // the partial forward (items [0, n_local): shared expert + resident hits)
+    // is a prefix of the partials in plan order
+    const uint32_t np_loc = a.x_pred ? s_pb[min(a.plan->n_local, s_ni)] : 0u;
     for (uint32_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       const uint32_t t = i / d, o = i % d;
       const float* pp = ua.part + (size_t)t * d + o;
       const float xin = bf2f(a.x_in[(size_t)t * d + o]);  // issued before the partials
       // partials in plan order, 32 loads in flight (branch-free: indices past
       // the end reload the last partial and are not added)
-      float y = 0.f;
+      float y = 0.f, y_loc = 0.f;
       for (uint32_t it = 0; it < np; it += 32) {
         float v[32];
 #pragma unroll
         for (uint32_t q2 = 0; q2 < 32; ++q2) v[q2] = __ldcg(pp + (size_t)min(it + q2, np - 1) * B * d);
 #pragma unroll
-        for (uint32_t q2 = 0; q2 < 32; ++q2)
+        for (uint32_t q2 = 0; q2 < 32; ++q2) {
+          if (it + q2 == np_loc) y_loc = y;
           if (it + q2 < np) y += v[q2];
+        }
       }
+      if (np_loc >= np) y_loc = y;
       const float xo = xin + y;
       a.x_out[(size_t)t * d + o] = f32_to_bf16_rne(xo);
       a.y_out[(size_t)t * d + o] = y;
+      if (a.x_pred) a.x_pred[(size_t)t * d + o] = f32_to_bf16_rne(xin + y_loc);
     }
   }
   if (a.tl && c == 0 && threadIdx.x == 0) a.tl[8] = globaltimer_ns();  // CTA 0's final sum done

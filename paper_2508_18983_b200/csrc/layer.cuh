@@ -44,7 +44,7 @@ struct Plan {
   uint32_t n_items, n_ready, n_d2d, seq;
   uint64_t d2d_elems;
   uint32_t n_spec;    // items [0, n_spec) were published early (speculative plan)
-  uint32_t pad;
+  uint32_t n_local;   // items [0, n_local) are the shared expert + resident hits (kind <= 1)
   Item items[kMaxItems];
   D2D d2d[kMaxE];
 };
@@ -130,13 +130,16 @@ struct GateArgs {
                            // tensor-core FFN (nullable; written by CTA 1, rows >= B stay 0)
   uint32_t ut_rows;
   float* logits;           // [B][E + 1]; column E = shared-gate logit
+  const uint16_t* x_pred;  // [B][d] the previous layer's partial forward (predictor) or null
+  float* plogits;          // [B][E + 1]: the same router applied to it
   uint32_t B, d, E;
 };
 
 // ng = ceil(rows / 2) gate CTAs with rows = E (+1 for the shared gate), gi the
 // CTA's index among them; 8 warps: warp w -> row 2*gi + (w & 1), quarter (w >> 1) of d.
 // us: [B][d] bf16 scratch in shared memory.
-__device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, uint32_t ng) {
+__device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, uint32_t ng, const uint16_t* xsrc,
+                                  float* logits_out, bool write_u) {
   __shared__ float part[4][2][kMaxB];
   __shared__ float inv_rms[kMaxB];
   const int lane = lane_id(), warp = warp_id();
@@ -146,7 +149,7 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, 
   // (a strided one-load-per-iteration loop is L2-latency-bound at B = 32)
   {
     const uint32_t n = B * nvec;
-    const uint4* xg = reinterpret_cast<const uint4*>(a.x);
+    const uint4* xg = reinterpret_cast<const uint4*>(xsrc);
     uint4* xs = reinterpret_cast<uint4*>(us);
     for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
       uint4 v[8];
@@ -192,8 +195,8 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, 
     }
     const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
     reinterpret_cast<uint4*>(us + (size_t)t * d)[c] = ov;
-    if (gi == 0) reinterpret_cast<uint4*>(a.u + (size_t)t * d)[c] = ov;
-    if (a.ut && gi == (ng > 1 ? 1u : 0u)) {
+    if (write_u && gi == 0) reinterpret_cast<uint4*>(a.u + (size_t)t * d)[c] = ov;
+    if (write_u && a.ut && gi == (ng > 1 ? 1u : 0u)) {
       // 16 B chunk (c % 8) of K-block c / 8, row t: chunk position (c ^ t) % 8
       const uint32_t off = (c >> 3) * a.ut_rows * 128u + (t >> 3) * 1024u + (t & 7u) * 128u + (((c ^ t) & 7u) << 4);
       *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(a.ut) + off) = ov;
@@ -249,7 +252,7 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, 
     const uint32_t rr = 2 * gi + r;
     if (rr < rows) {
       const float s = ((part[0][r][t] + part[1][r][t]) + part[2][r][t]) + part[3][r][t];
-      a.logits[(size_t)t * (a.E + 1) + rr] = s;
+      logits_out[(size_t)t * (a.E + 1) + rr] = s;
     }
   }
 }

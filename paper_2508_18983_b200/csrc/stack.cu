@@ -120,6 +120,11 @@ struct DecideArgs {
                               // 3 decider entry, 4 uploads published (entry A), 5 end of decide
   uint64_t it;                // decode iteration of this launch (host-tracked)
   uint64_t seq;               // 1-based layer-step sequence number (host-tracked)
+  // predictor mode: the prediction of this layer's scores from the previous
+  // layer's partial forward (gate CTAs: plogits), logged per step for replay
+  uint32_t predictor;
+  const float* plogits;       // [B][E + 1]
+  float* pred_log;            // [rec_cap][B][E] or null
 };
 
 struct GateDecideArgs {
@@ -236,6 +241,7 @@ struct EarlyPublish {
   DecideKSmem* sm;
   __device__ void classified(DecideSmem* d, uint64_t mask) const { publish_spec(*a, sm, d, mask); }
   __device__ void plan_ready(DecideSmem* d) const;
+  __device__ void prefetched(DecideSmem* d) const;
   __device__ void operator()(DecideSmem* d, uint32_t n_load, uint32_t n_cpu) const {
     if (lane_id() == 0) {
       const DecideArgs& A = *a;
@@ -449,6 +455,7 @@ __device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
     p->n_items = n_items;
     p->n_ready = base + n_spec + n_rdy;
     p->n_spec = sm->spec_n;
+    p->n_local = n0;
     p->n_d2d = n_d2d;
     p->d2d_elems = a.expert_elems;
     p->seq = (uint32_t)sm->seq;
@@ -457,7 +464,28 @@ __device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
 }
 
 // The prefetch upload commands (mailbox entry B), after the prefetch phase.
-__device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm) {
+__device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm, uint32_t wait_ffn);
+
+// Predictor mode: mailbox entry B of the PREVIOUS step (its schedule_prefetch
+// ran at the start of this step), before this step's entry A. Warp 0.
+__device__ void EarlyPublish::prefetched(DecideSmem*) const {
+  if (lane_id() == 0 && sm->seq >= 2) {
+    const DecideArgs& A = *a;
+    build_prefetch_cmds(A, sm, (uint32_t)(sm->seq - 1));
+    const uint64_t mseq = 2 * (sm->seq - 1);
+    wait_ring_slot(A, mseq, &sm->st.ack_cache);
+    MailEntry* me = &A.ring[mseq % kRing];
+    const uint32_t nc = sm->n_cmds;
+    for (uint32_t i = 0; i < nc; ++i) me->cmd[i] = sm->cmd[i];
+    me->n = nc;
+    if (nc) __threadfence_system();
+    me->seq = (mseq << 8) | nc;
+    sm->n_cmds = 0;
+  }
+  __syncwarp();
+}
+
+__device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm, uint32_t wait_ffn) {
   const uint32_t E = sm->cfg.E, layer = a.layer;
   const StepOut& out = sm->d.out;
   EngineState* st = &sm->st;
@@ -473,7 +501,7 @@ __device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm) {
     c.dst = (uint64_t)dst;
     c.bytes = a.expert_elems * 2;
     c.id = id;
-    c.wait_ffn = (uint32_t)sm->seq;
+    c.wait_ffn = wait_ffn;
     LayerState* tls = (tlayer == layer) ? &sm->ls : &sm->tls;
     if (slot >= 0) tls->slot_copy[slot] = id;
   }
@@ -592,7 +620,14 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   const uint32_t n_gate = gridDim.x - 1;
   if (blockIdx.x != 0) {
     // us [B][d] bf16 aliases the decision workspace
-    gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw), blockIdx.x - 1, n_gate);
+    gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw), blockIdx.x - 1, n_gate, ga.g.x, ga.g.logits, true);
+    if (ga.g.x_pred) {
+      // the predictor: this layer's router on the previous layer's partial
+      // forward (shared expert + resident hits)
+      __syncthreads();
+      gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw), blockIdx.x - 1, n_gate, ga.g.x_pred, ga.g.plogits,
+                 false);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -694,10 +729,13 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
       softmax_warp(a.trace + (((tit % a.trace_steps) * L + tl) * B + t) * E, E, sm->nsc[t]);
     }
   }
+  const bool run_pending = a.predictor && sm->st.pf_pending && sm->st.pf_layer == layer && sm->st.pf_it == it;
+  if (run_pending)  // the prediction for this layer: softmax of the router on the partial forward
+    for (uint32_t t = warp; t < B; t += nw) softmax_warp(a.plogits + (size_t)t * (E + 1), E, sm->nsc[t]);
   if (threadIdx.x == 0) {
     sm->it = it;
     sm->seq = a.seq;
-    sm->d.next_has_pred = 0;
+    sm->d.next_has_pred = run_pending ? (B >= 64 ? ~0ull : (1ull << B) - 1ull) : 0ull;
   }
   __syncthreads();
   const DevCfg& cfg = sm->cfg;
@@ -705,7 +743,9 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     const uint32_t t = i / E, e = i % E;
     sm->d.s[t][e] = (double)sm->sc[t][e];
     if (want_next) sm->d.ns[t][e] = (double)sm->nsc[t][e];
+    if (run_pending) sm->d.np[t][e] = (double)sm->nsc[t][e];
     if (a.scores_log && a.seq <= a.rec_cap) a.scores_log[((a.seq - 1) * B + t) * E + e] = sm->sc[t][e];
+    if (run_pending && a.pred_log && a.seq <= a.rec_cap) a.pred_log[((a.seq - 1) * B + t) * E + e] = sm->nsc[t][e];
   }
   __syncthreads();
   MOEB_T(t_staged);
@@ -720,10 +760,13 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   cx.logs = nullptr;
   cx.it = it;
   cx.layer = layer;
-  cx.has_target = want_next ? 1u : 0u;
+  cx.has_target = (want_next || (a.predictor && has_target)) ? 1u : 0u;
   cx.target_layer = tl;
   cx.target_it = tit;
   cx.prof = sm->st.prof;
+  cx.defer_prefetch = a.predictor;
+  cx.run_pending = run_pending;
+  cx.prev_rec = (a.recs && sm->seq >= 2 && sm->seq - 1 <= a.rec_cap) ? a.recs + (sm->seq - 2) : nullptr;
   StepRec* rec = nullptr;
   TokRec* toks = nullptr;
   if (a.recs && sm->seq <= a.rec_cap) {
@@ -735,9 +778,11 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   MOEB_T(t_decided);
 
   if (threadIdx.x == 0) {
-    build_prefetch_cmds(a, sm);
+    // predictor mode: entry B of this step is published by the next step
+    if (!a.predictor) build_prefetch_cmds(a, sm, (uint32_t)sm->seq);
+    else sm->n_cmds = 0;
     // entry B's ring slot must have been consumed by the copy thread
-    wait_ring_slot(a, 2 * sm->seq, &sm->st.ack_cache);
+    if (!a.predictor) wait_ring_slot(a, 2 * sm->seq, &sm->st.ack_cache);
     sm->st.seq = sm->seq;
     if (layer == L - 1) sm->st.it = it + 1;
   }
@@ -757,12 +802,14 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   // publish: prefetch commands -> mapped host ring, state write-back (the
   // plan went out in EarlyPublish::plan_ready)
   {
-    MailEntry* me = &a.ring[(2 * sm->seq) % kRing];
-    const uint32_t nc = sm->n_cmds;
-    const uint64_t* cs = reinterpret_cast<const uint64_t*>(sm->cmd);
-    uint64_t* cd = reinterpret_cast<uint64_t*>(me->cmd);
-    for (uint32_t i = threadIdx.x; i < nc * sizeof(MailCmd) / 8; i += blockDim.x) cd[i] = cs[i];
-    if (threadIdx.x == 0) me->n = nc;
+    if (!a.predictor) {
+      MailEntry* me = &a.ring[(2 * sm->seq) % kRing];
+      const uint32_t nc = sm->n_cmds;
+      const uint64_t* cs = reinterpret_cast<const uint64_t*>(sm->cmd);
+      uint64_t* cd = reinterpret_cast<uint64_t*>(me->cmd);
+      for (uint32_t i = threadIdx.x; i < nc * sizeof(MailCmd) / 8; i += blockDim.x) cd[i] = cs[i];
+      if (threadIdx.x == 0) me->n = nc;
+    }
     cta_copy(a.st, &sm->st);
     cta_copy(&a.layers[layer], &sm->ls);
     if (want_next && tl != layer) cta_copy(&a.layers[tl], &sm->tls);
@@ -774,7 +821,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     MOEB_T(t_pub0);
     const uint32_t nc = sm->n_cmds;
     if (nc) __threadfence_system();
-    a.ring[(2 * sm->seq) % kRing].seq = ((2 * sm->seq) << 8) | nc;
+    if (!a.predictor) a.ring[(2 * sm->seq) % kRing].seq = ((2 * sm->seq) << 8) | nc;
     if (a.tl) a.tl[5] = globaltimer_ns();
 #ifdef MOEB_PROFILE_PHASES
     const uint64_t t_pub1 = gtimer();
@@ -833,6 +880,11 @@ struct moeb_stack {
   uint64_t expert_elems = 0;
   DevBuf<uint16_t> gate_w, shared_w, sgate_w, slots, staging, hidden, u;
   DevBuf<float> logits, h, y_layers, trace, scores_log;
+  // predictor mode (MOEB_MODEL_PREDICTOR): partial forward, its router
+  // logits, the predictions used per step
+  bool predictor = false;
+  DevBuf<uint16_t> xpred;
+  DevBuf<float> plogits, pred_log;
   DevBuf<EngineState> st;
   DevBuf<LayerState> layers;
   DevBuf<double> hist;
@@ -1238,6 +1290,20 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
     S->toks.alloc(S->rec_cap * B);
     S->scores_log.alloc(S->rec_cap * B * E);
   }
+  S->predictor = (m.flags & MOEB_MODEL_PREDICTOR) != 0;
+  if (S->predictor) {
+    if (!S->splitk && !S->umma)
+      throw Error(1, "model: the predictor needs the split-K (batch 1, d_model <= 2048) or the tensor-core "
+                     "(batch 2..32, ffn and shared_ffn multiples of 128) FFN");
+    S->xpred.alloc((size_t)B * d);
+    S->xpred.zero(s);
+    S->plogits.alloc((size_t)B * (E + 1));
+    S->plogits.zero(s);
+    if (S->rec_cap) {
+      S->pred_log.alloc(S->rec_cap * B * E);
+      MOEB_CUDA(cudaMemsetAsync(S->pred_log.p, 0xff, S->rec_cap * B * E * sizeof(float), s));  // NaN: no prediction
+    }
+  }
   MOEB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->ring), sizeof(MailEntry) * kRing, cudaHostAllocMapped | cudaHostAllocPortable));
   std::memset(S->ring, 0, sizeof(MailEntry) * kRing);
   MOEB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&S->ack), 64, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1337,15 +1403,19 @@ static void serial_wait_uploads(moeb_stack* S, cudaStream_t s, uint64_t seq) {
     std::this_thread::yield();
   }
   const MailEntry* ea = &S->ring[(2 * seq - 1) % kRing];
-  const MailEntry* eb = &S->ring[(2 * seq) % kRing];
-  const uint64_t va = ea->seq, vb = eb->seq;
-  if ((va >> 8) != 2 * seq - 1 || (vb >> 8) != 2 * seq)
+  // entry B of this step, or (predictor mode) of the previous one, which this
+  // step's kernel published before entry A
+  const uint64_t bseq = S->predictor ? 2 * seq - 2 : 2 * seq;
+  const MailEntry* eb = &S->ring[bseq % kRing];
+  const uint64_t va = ea->seq, vb = bseq ? eb->seq : 0;
+  if ((va >> 8) != 2 * seq - 1 || (bseq && (vb >> 8) != bseq))
     throw Error(5, "serial mode: the decide kernel did not publish its upload commands");
+  if (S->predictor && (vb & 0xff)) S->serial_need = std::max(S->serial_need, eb->cmd[(vb & 0xff) - 1].id);
   if (va & 0xff) S->serial_need = std::max(S->serial_need, ea->cmd[(va & 0xff) - 1].id);
   if (S->serial_need &&
       p_wait32(s, (CUdeviceptr)S->copies_done.p, S->serial_need, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
     throw Error(5, "serial mode: cuStreamWaitValue32 failed");
-  if (vb & 0xff) S->serial_need = std::max(S->serial_need, eb->cmd[(vb & 0xff) - 1].id);
+  if (!S->predictor && (vb & 0xff)) S->serial_need = std::max(S->serial_need, eb->cmd[(vb & 0xff) - 1].id);
 }
 
 // The persistent FFN grids assume every CTA is co-resident (grid barriers,
@@ -1368,7 +1438,8 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
 static void step_stack(moeb_stack* S, const void* x, void* y, uint32_t B, cudaStream_t user) {
   if (B != S->B) throw Error(1, "step: batch must equal the configured batch_size");
   if (S->copier_error) throw Error(5, S->copier_msg);
-  if (S->cfg.pre && !S->trace.p) throw Error(1, "stage Pre needs a logits trace (moeb_set_logits_trace)");
+  if (S->cfg.pre && !S->trace.p && !S->predictor)
+    throw Error(1, "stage Pre needs a logits trace (moeb_set_logits_trace) or the predictor (MOEB_MODEL_PREDICTOR)");
   cudaStream_t s = user ? user : S->stream;
   MOEB_CUDA(cudaSetDevice(S->device));
   DeviceOrder& o = device_order(S->device);
@@ -1394,6 +1465,8 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     g.ut = S->umma ? S->xt.p : nullptr;
     g.ut_rows = S->um.Nx;
     g.logits = S->logits.p;
+    g.x_pred = S->predictor ? S->xpred.p : nullptr;
+    g.plogits = S->predictor ? S->plogits.p : nullptr;
     g.B = B;
     g.d = d;
     g.E = E;
@@ -1434,6 +1507,9 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     a.it = S->host_it;
     a.seq = ++S->host_seq;
     a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * kTlWords : nullptr;
+    a.predictor = S->predictor ? 1u : 0u;
+    a.plogits = S->plogits.p;
+    a.pred_log = S->pred_log.p;
     ga.ticket = S->ticket.p;
     if (S->timing) S->tick(s);
     launch_pdl(reinterpret_cast<const void*>(gate_decide_kernel), dim3(1 + (rows + 1) / 2), dim3(kGdThreads),
@@ -1448,6 +1524,7 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     f.x_in = S->hidden.p + (size_t)cur * B * d;
     f.x_out = S->hidden.p + (size_t)(cur ^ 1) * B * d;
     f.y_out = S->y_layers.p + (size_t)l * B * d;
+    f.x_pred = S->predictor ? S->xpred.p : nullptr;
     f.h = S->h.p;
     f.ctr = S->ffn_ctr.p;
     f.copies_done = S->copies_done.p;
@@ -1546,6 +1623,8 @@ int moeb_set_logits_trace(moeb_stack* s, const float* logits, uint64_t n_steps, 
   return guarded([&] {
     MOEB_CUDA(cudaSetDevice(s->device));
     MOEB_CUDA(cudaStreamSynchronize(s->stream));
+    if (logits && n_steps && s->predictor)
+      throw Error(1, "the predictor needs weight-driven routing (no logits trace)");
     if (!logits || n_steps == 0) {
       s->trace.free();
       s->trace_steps = 0;
@@ -1638,6 +1717,21 @@ int moeb_get_scores(moeb_stack* s, float* out, size_t cap, size_t* n) {
     const size_t total = std::min<uint64_t>(st.seq, s->rec_cap) * s->B * s->E;
     const size_t k = std::min(total, cap);
     if (k) MOEB_CUDA(cudaMemcpy(out, s->scores_log.p, k * sizeof(float), cudaMemcpyDeviceToHost));
+    *n = total;
+  });
+}
+
+int moeb_get_pred_scores(moeb_stack* s, float* out, size_t cap, size_t* n) {
+  return guarded([&] {
+    if (!s->predictor || !s->rec_cap)
+      throw Error(4, "stack was created without MOEB_MODEL_PREDICTOR | MOEB_MODEL_LOG_STEPS");
+    MOEB_CUDA(cudaDeviceSynchronize());
+    EngineState st;
+    MOEB_CUDA(cudaMemcpy(&st, s->st.p, sizeof st, cudaMemcpyDeviceToHost));
+    check_log_capacity(s, st.seq);
+    const size_t total = std::min<uint64_t>(st.seq, s->rec_cap) * s->B * s->E;
+    const size_t k = std::min(total, cap);
+    if (out && k) MOEB_CUDA(cudaMemcpy(out, s->pred_log.p, k * sizeof(float), cudaMemcpyDeviceToHost));
     *n = total;
   });
 }
