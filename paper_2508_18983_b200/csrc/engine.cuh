@@ -281,28 +281,13 @@ __device__ inline void classify_warp(const double* s, uint32_t E, uint32_t k, do
   const uint32_t e0 = lane, e1 = lane + 32;
   const bool v0 = e0 < E, v1 = e1 < E;
   const double s0 = v0 ? s[e0] : 0.0, s1 = v1 ? s[e1] : 0.0;
-  // rank by counting: two scores per 16-byte broadcast load, independent
-  // partial counts (E is even: the stack and the engine pad nothing, and an
-  // odd E takes the scalar tail)
-  uint32_t r0 = 0, r1 = 0, q0 = 0, q1 = 0;
-  uint32_t j = 0;
-  if ((reinterpret_cast<uintptr_t>(s) & 15u) == 0) {
-#pragma unroll 8
-    for (; j + 2 <= E; j += 2) {
-      const double2 p = *reinterpret_cast<const double2*>(s + j);
-      r0 += (p.x > s0) || (p.x == s0 && j < e0);
-      r1 += (p.x > s1) || (p.x == s1 && j < e1);
-      q0 += (p.y > s0) || (p.y == s0 && j + 1 < e0);
-      q1 += (p.y > s1) || (p.y == s1 && j + 1 < e1);
-    }
-  }
-  for (; j < E; ++j) {
+  uint32_t r0 = 0, r1 = 0;
+#pragma unroll 16
+  for (uint32_t j = 0; j < E; ++j) {
     const double sj = s[j];
     r0 += (sj > s0) || (sj == s0 && j < e0);
     r1 += (sj > s1) || (sj == s1 && j < e1);
   }
-  r0 += q0;
-  r1 += q1;
   if (v0) order[r0] = (uint8_t)e0;
   if (v1) order[r1] = (uint8_t)e1;
   __syncwarp();

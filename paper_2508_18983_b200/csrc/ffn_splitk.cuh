@@ -170,27 +170,41 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         // (an uploaded expert alone — ~10 rows per SM — goes out in 2-row
         // units: its completion is on the critical path after the upload)
         const bool det = a.deterministic != 0;
-        const uint32_t ub = a.unit_rows ? a.unit_rows : (det ? kSkStaticUnitRows : kSkUnitRows);
-        const uint32_t n1 = small_units ? 0 : det ? rows / ub : (rows * 70 / 100) / ub, e1 = n1 * ub;
-        const uint32_t n2 = small_units || det ? 0 : (rows * 95 / 100 > e1 ? rows * 95 / 100 - e1 : 0) / 8, e2 = e1 + n2 * 8;
-        const uint32_t n_units = n1 + n2 + (rows - e2 + 1) / 2;
-        uint32_t* ctr = a.ctr + ci;
-        // static mode (default): unit u belongs to CTA u % G — units of the
-        // same size, dealt round-robin, balance the SMs without counter atomics
-        // and give bitwise-reproducible partial sums
-        uint32_t u0 = det ? c : atomicAdd(ctr, 1u), u1 = det ? c + G : atomicAdd(ctr, 1u);
-        uint32_t ii = i0;
-        while (u0 < n_units) {
-          const uint32_t cur = u0;
-          u0 = u1;
-          u1 = det ? u1 + G : atomicAdd(ctr, 1u);
-          uint32_t r0, r1;
-          if (cur < n1) { r0 = cur * ub; r1 = r0 + ub; }
-          else if (cur < n1 + n2) { r0 = e1 + (cur - n1) * 8; r1 = r0 + 8; }
-          else { r0 = e2 + (cur - n1 - n2) * 2; r1 = min(rows, r0 + 2); }
+        if (det && !a.unit_rows) {
+          // static mode (default): CTA c streams the contiguous rows
+          // [rows c / G, rows (c + 1) / G) of this phase — equal shares, every
+          // CTA on one long run of DRAM pages (measured faster than dealing
+          // 4-row units round-robin: 4 / 8 / 16-row units 35.2 / 34.1 / 33.4 us
+          // per all-resident layer, finer units slower), and a fixed row ->
+          // (CTA, ring step) map: bitwise-reproducible partial sums
+          const uint32_t r0 = (uint32_t)((uint64_t)rows * c / G), r1 = (uint32_t)((uint64_t)rows * (c + 1) / G);
+          uint32_t ii = i0;
           for (uint32_t row = r0; row < r1; ++row) {
             while (s_pre[ii + 1] <= row) ++ii;
             issue_row(ii, row - s_pre[ii]);
+          }
+        } else {
+          const uint32_t ub = a.unit_rows ? a.unit_rows : (det ? kSkStaticUnitRows : kSkUnitRows);
+          const uint32_t n1 = small_units ? 0 : det ? rows / ub : (rows * 70 / 100) / ub, e1 = n1 * ub;
+          const uint32_t n2 = small_units || det ? 0 : (rows * 95 / 100 > e1 ? rows * 95 / 100 - e1 : 0) / 8, e2 = e1 + n2 * 8;
+          const uint32_t n_units = n1 + n2 + (rows - e2 + 1) / 2;
+          uint32_t* ctr = a.ctr + ci;
+          // MOEB_SK_UNIT=n (static): unit u of n rows belongs to CTA u % G;
+          // MOEB_DYNAMIC_ROWS=1: units grabbed from a grid counter
+          uint32_t u0 = det ? c : atomicAdd(ctr, 1u), u1 = det ? c + G : atomicAdd(ctr, 1u);
+          uint32_t ii = i0;
+          while (u0 < n_units) {
+            const uint32_t cur = u0;
+            u0 = u1;
+            u1 = det ? u1 + G : atomicAdd(ctr, 1u);
+            uint32_t r0, r1;
+            if (cur < n1) { r0 = cur * ub; r1 = r0 + ub; }
+            else if (cur < n1 + n2) { r0 = e1 + (cur - n1) * 8; r1 = r0 + 8; }
+            else { r0 = e2 + (cur - n1 - n2) * 2; r1 = min(rows, r0 + 2); }
+            for (uint32_t row = r0; row < r1; ++row) {
+              while (s_pre[ii + 1] <= row) ++ii;
+              issue_row(ii, row - s_pre[ii]);
+            }
           }
         }
       }
@@ -406,57 +420,51 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
     }
   }
   __syncthreads();
-  // outputs [dlo, dhi): sum of the CTA partials in CTA order, residual.
-  // Thread (o, j) sums partials [j*kSeg, (j+1)*kSeg) of output o (all loads
-  // issued together), then one thread per output adds the segments in order.
+  // outputs [dlo, dhi): sum of the CTA partials, residual. The [G][no]
+  // block this CTA needs is gathered with coalesced loads (consecutive
+  // threads read consecutive outputs of one partial, all loads in flight
+  // together) into shared memory; then each output thread sums its G values
+  // in 8 interleaved chains combined in a fixed order (deterministic).
   {
-    constexpr uint32_t kSeg = 8;
-    const uint32_t nseg = (G + kSeg - 1) / kSeg, no = dhi - dlo;
-    float* seg = reinterpret_cast<float*>(ring);  // [no][nseg]
-    for (uint32_t t = threadIdx.x; t < no * nseg; t += blockDim.x) {
-      const uint32_t o = dlo + t / nseg, j = t % nseg;
-      float v[kSeg];
+    const uint32_t no = dhi - dlo;
+    float* gath = reinterpret_cast<float*>(ring);  // [G][no]
+    auto final_sum = [&](const float* src) -> float {
+      constexpr uint32_t kIn = 8;
+      const uint32_t n = G * no;
+      for (uint32_t t0 = threadIdx.x; t0 < n; t0 += kIn * blockDim.x) {
+        float v[kIn];
 #pragma unroll
-      for (uint32_t q = 0; q < kSeg; ++q) {
-        const uint32_t cc = j * kSeg + q;
-        v[q] = cc < G ? __ldcg(part + (size_t)cc * d + o) : 0.f;
+        for (uint32_t q = 0; q < kIn; ++q) {
+          const uint32_t t = t0 + q * blockDim.x;
+          const uint32_t cc = t / no, o = t - cc * no;
+          v[q] = t < n ? __ldcg(src + (size_t)cc * d + dlo + o) : 0.f;
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < kIn; ++q) {
+          const uint32_t t = t0 + q * blockDim.x;
+          if (t < n) gath[t] = v[q];
+        }
       }
-      float sum = v[0];
-#pragma unroll
-      for (uint32_t q = 1; q < kSeg; ++q) sum += v[q];
-      seg[t] = sum;
-    }
-    __syncthreads();
+      __syncthreads();
+      float yv = 0.f;
+      if (threadIdx.x < no) {
+        float ch[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (uint32_t cc = 0; cc < G; ++cc) ch[cc & 7] += gath[cc * no + threadIdx.x];
+        yv = ((ch[0] + ch[1]) + (ch[2] + ch[3])) + ((ch[4] + ch[5]) + (ch[6] + ch[7]));
+      }
+      __syncthreads();
+      return yv;
+    };
+    const float yv = final_sum(part);
     if (threadIdx.x < no) {
       const uint32_t o = dlo + threadIdx.x;
-      float yv = 0.f;
-      for (uint32_t j = 0; j < nseg; ++j) yv += seg[threadIdx.x * nseg + j];
       a.x_out[o] = f32_to_bf16_rne(xin_pre + yv);
       a.y_out[o] = yv;
       if (a.x_pred && !snap) a.x_pred[o] = f32_to_bf16_rne(xin_pre + yv);  // every item was local
     }
-    if (a.x_pred && snap) {
-      // the same CTA-ordered sum over the snapshot partials
-      __syncthreads();
-      for (uint32_t t = threadIdx.x; t < no * nseg; t += blockDim.x) {
-        const uint32_t o = dlo + t / nseg, j = t % nseg;
-        float v[kSeg];
-#pragma unroll
-        for (uint32_t q = 0; q < kSeg; ++q) {
-          const uint32_t cc = j * kSeg + q;
-          v[q] = cc < G ? __ldcg(part_loc + (size_t)cc * d + o) : 0.f;
-        }
-        float sum = v[0];
-#pragma unroll
-        for (uint32_t q = 1; q < kSeg; ++q) sum += v[q];
-        seg[t] = sum;
-      }
-      __syncthreads();
-      if (threadIdx.x < no) {
-        float yv = 0.f;
-        for (uint32_t j = 0; j < nseg; ++j) yv += seg[threadIdx.x * nseg + j];
-        a.x_pred[dlo + threadIdx.x] = f32_to_bf16_rne(xin_pre + yv);
-      }
+    if (a.x_pred && snap) {  // the partial forward: the same sum over the snapshot partials
+      const float yl = final_sum(part_loc);
+      if (threadIdx.x < no) a.x_pred[dlo + threadIdx.x] = f32_to_bf16_rne(xin_pre + yl);
     }
   }
   // deferred admissions: staging -> slot (every CTA passed the barrier above,
