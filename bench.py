@@ -569,7 +569,7 @@ def run_ours(args):
                           "substitution_ratio": round((m1["substitutions"] - m0["substitutions"]) /
                                                       max(1, (m1["substitutions"] - m0["substitutions"]) +
                                                           (m1["low_score_kept"] - m0["low_score_kept"])), 4)},
-        "e2e": {"value": round(e2e_ms_max / K, 4), "unit": "ms/token", "h2d_bytes_per_step": B * d * 2,
+        "e2e": {"value": round(e2e_ms_max / K / world, 4), "unit": "ms/token", "h2d_bytes_per_step": B * d * 2,
                 "d2h_bytes_per_step": B * d * 2},
         "roofline": {"bound": "hbm", "kernel": f"{FFN_KERNEL_B1} (all-resident pass, no uploads)",
                      "achieved": round(ffn_gbs, 1), "peak": hbm_peak, "unit": "GB/s",

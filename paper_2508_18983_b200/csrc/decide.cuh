@@ -43,6 +43,10 @@ __device__ __forceinline__ uint64_t gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Phase timers of the decision CTA (make PROFILE=1): the SM cycle counter
+// (cycle resolution; %globaltimer ticks far more coarsely), in ns at the
+// B200's 1965 MHz boost clock the bench runs at.
+__device__ __forceinline__ uint64_t ptimer() { return (uint64_t)clock64() * 1000ull / 1965ull; }
 
 // Extra shared state for the prefetch target's classification.
 struct NextSmem {
@@ -732,9 +736,9 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
 
   const uint32_t nw = blockDim.x >> 5;
 #ifdef MOEB_PROFILE_PHASES
-  uint64_t tp = (cx.prof && tid == 0) ? gtimer() : 0;
+  uint64_t tp = (cx.prof && tid == 0) ? ptimer() : 0;
   auto mark = [&](int i) {
-    if (cx.prof && tid == 0) { const uint64_t n = gtimer(); cx.prof[i] += n - tp; tp = n; }
+    if (cx.prof && tid == 0) { const uint64_t n = ptimer(); cx.prof[i] += n - tp; tp = n; }
   };
 #else
   auto mark = [](int) {};  // phase timers compiled out (build with -DMOEB_PROFILE_PHASES)

@@ -426,18 +426,19 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   // together) into shared memory; then each output thread sums its G values
   // in 8 interleaved chains combined in a fixed order (deterministic).
   {
-    const uint32_t no = dhi - dlo;
-    float* gath = reinterpret_cast<float*>(ring);  // [G][no]
+    const uint32_t no = dhi - dlo;  // <= 16 (d <= 2048, G >= 128)
+    float* gath = reinterpret_cast<float*>(ring);  // [G][16]
     auto final_sum = [&](const float* src) -> float {
-      constexpr uint32_t kIn = 8;
-      const uint32_t n = G * no;
+      // item t = (partial t / 16, output t % 16): half-warps read one
+      // partial's outputs, every load in flight at once
+      constexpr uint32_t kIn = 9;
+      const uint32_t n = G * 16;
       for (uint32_t t0 = threadIdx.x; t0 < n; t0 += kIn * blockDim.x) {
         float v[kIn];
 #pragma unroll
         for (uint32_t q = 0; q < kIn; ++q) {
-          const uint32_t t = t0 + q * blockDim.x;
-          const uint32_t cc = t / no, o = t - cc * no;
-          v[q] = t < n ? __ldcg(src + (size_t)cc * d + dlo + o) : 0.f;
+          const uint32_t t = t0 + q * blockDim.x, cc = t >> 4, o = t & 15u;
+          v[q] = (t < n && o < no) ? __ldcg(src + (size_t)cc * d + dlo + o) : 0.f;
         }
 #pragma unroll
         for (uint32_t q = 0; q < kIn; ++q) {
@@ -448,8 +449,15 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       __syncthreads();
       float yv = 0.f;
       if (threadIdx.x < no) {
+        // 8 interleaved chains in a fixed order (deterministic)
         float ch[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (uint32_t cc = 0; cc < G; ++cc) ch[cc & 7] += gath[cc * no + threadIdx.x];
+        uint32_t cc = 0;
+        for (; cc + 8 <= G; cc += 8)
+#pragma unroll
+          for (uint32_t q = 0; q < 8; ++q) ch[q] += gath[(cc + q) * 16 + threadIdx.x];
+#pragma unroll
+        for (uint32_t q = 0; q < 8; ++q)
+          if (cc + q < G) ch[q] += gath[(cc + q) * 16 + threadIdx.x];
         yv = ((ch[0] + ch[1]) + (ch[2] + ch[3])) + ((ch[4] + ch[5]) + (ch[6] + ch[7]));
       }
       __syncthreads();

@@ -286,16 +286,17 @@ struct EarlyPublish {
       }
       me->n = n;
 #ifdef MOEB_PROFILE_PHASES
-      const uint64_t tf0 = gtimer();
+      const uint64_t tf0 = ptimer();
 #endif
-      if (n) __threadfence_system();
-      me->seq = (mseq << 8) | n;
+      // one release store at system scope orders this lane's command writes
+      // before the sequence word the copy thread polls
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&me->seq), "l"((mseq << 8) | n) : "memory");
       if (A.tl) {
         A.tl[4] = globaltimer_ns();
         A.tl[15] = n;  // uploads published by this step
       }
 #ifdef MOEB_PROFILE_PHASES
-      st->prof[13] += gtimer() - tf0;
+      st->prof[13] += ptimer() - tf0;
 #endif
     }
     __syncwarp();
@@ -525,8 +526,8 @@ __device__ void EarlyPublish::plan_ready(DecideSmem* d) const {
   }
   __syncwarp();
 #ifdef MOEB_PROFILE_PHASES
-  uint64_t tq = gtimer();
-  auto pmark = [&](int i) { if (lane == 0) { const uint64_t n = gtimer(); sm->st.prof[i] += n - tq; tq = n; } };
+  uint64_t tq = ptimer();
+  auto pmark = [&](int i) { if (lane == 0) { const uint64_t n = ptimer(); sm->st.prof[i] += n - tq; tq = n; } };
 #else
   auto pmark = [](int) {};
 #endif
@@ -1175,7 +1176,10 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   const uint32_t L = S->L, E = S->E, B = S->B, d = S->d, F = S->F, Sh = S->S;
   const uint64_t seed = m.weight_seed;
   // batch 1: split-K FFN over row-interleaved experts ([F][3][d])
-  S->splitk = B == 1 && d <= 2048 && getenv("MOEB_NO_SPLITK") == nullptr;
+  int n_sm = 0;
+  MOEB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, device));
+  // (the split-K FFN's final sum gathers <= 16 outputs per CTA: d <= 16 (SMs - 1))
+  S->splitk = B == 1 && d <= 2048 && d <= 16u * (uint32_t)(n_sm - 1) && getenv("MOEB_NO_SPLITK") == nullptr;
   if (const char* ur = getenv("MOEB_SK_UNIT")) S->unit_rows = (uint32_t)atoi(ur);
   if (const char* fd = getenv("MOEB_FFN_DBG")) S->ffn_dbg = (uint32_t)atoi(fd);  // microbenchmark knob
   // batch 2..32: tensor-core FFN over UMMA-tiled experts, when the shapes
