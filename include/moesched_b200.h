@@ -308,9 +308,10 @@ int moeb_generate_trace(uint32_t L, uint32_t E, uint32_t B, double hot_fraction,
 /* Device-clock (ns) timeline of the last <= 16384 layer-steps, 16 words each:
  * 0 FFN start, 1 FFN saw its last upload land (0: none), 2 FFN end,
  * 3 decide entry, 4 uploads published (mailbox entry A), 5 decide end,
- * 6 FFN has the speculative plan, 7 FFN CTA 0 entry,
+ * 6 FFN has the speculative plan (split-K FFN: the shared expert released
+ * right after the gate), 7 FFN CTA 0 entry,
  * 8 tcgen05 FFN: CTA 0 final sum done (other FFN kernels: unused),
- * 9 unused, 10 CUDA-core FFN: down pass starts, 11 FFN CTA 0 compute done,
+ * 9 split-K FFN: the speculative plan of the certain experts, 10 CUDA-core FFN: down pass starts, 11 FFN CTA 0 compute done,
  * 12 final plan released to the FFN, 13 last FFN CTA compute done (max over
  * CTAs), 14 split-K FFN: reduction barrier passed, 15 number of uploads the
  * step published (a count, not a time). Diagnostics only. */

@@ -235,12 +235,24 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
     uint32_t n_spec = 0;
     if (!spec) load_u();
     if (spec) {
+      const uint32_t hdr = (uint32_t)(offsetof(Plan, items) / 8), iw = (uint32_t)(sizeof(Item) / 8);
+      uint32_t n0 = 0;
+      if (a.shared_first) {
+        // the shared expert, released right after the gate
+        wait_flag(a.spec_flag + 2, 6);
+        load_u();
+        fetch(a.spec_plan, hdr, hdr + iw);
+        stream(0, 1, kFfnSpecGuCtr, false);
+        n0 = 1;
+        wait_flag(a.spec_flag, 9);
+      } else {
+        wait_flag(a.spec_flag, 6);
+        load_u();
+      }
       // the certain items while the decision runs
-      wait_flag(a.spec_flag, 6);
-      load_u();
       n_spec = ld_acquire_u32(&a.spec_plan->n_spec);
-      fetch(a.spec_plan, 0, (uint32_t)((offsetof(Plan, items) + n_spec * sizeof(Item)) / 8));
-      stream(0, n_spec, kFfnSpecGuCtr, false);
+      fetch(a.spec_plan, hdr + n0 * iw, hdr + n_spec * iw);
+      stream(n0, n_spec, kFfnSpecGuCtr, false);
       // the final plan: its first n_spec items are the speculative ones
       wait_flag(a.spec_flag + 1, 0);
       const uint32_t hdr_words = (uint32_t)(offsetof(Plan, items) / 8);

@@ -113,6 +113,7 @@ struct FfnTArgs {
   uint32_t seq;
   uint32_t unit_rows;      // split-K kernel: intermediate rows per grid-counter grab (0: default)
   uint32_t deterministic;  // split-K kernel: static row -> (CTA, warp) assignment (bitwise-reproducible sums)
+  uint32_t shared_first;   // split-K kernel: item 0 (shared expert) of spec_plan released alone by spec_flag[2]
 };
 
 // Row range of CTA c out of G over n rows.

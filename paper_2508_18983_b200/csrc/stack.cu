@@ -123,6 +123,7 @@ struct DecideArgs {
   // predictor mode: the prediction of this layer's scores from the previous
   // layer's partial forward (gate CTAs: plogits), logged per step for replay
   uint32_t predictor;
+  uint32_t shared_first;      // split-K FFN: the shared expert alone is released right after the gate
   const float* plogits;       // [B][E + 1]
   float* pred_log;            // [rec_cap][B][E] or null
 };
@@ -155,6 +156,7 @@ struct DecideKSmem {
   MailCmd cmd[kMaxCmds];
   uint32_t n_cmds;
   uint32_t landed;            // copies_done when the step's state was staged
+  volatile uint32_t mail_a;   // mailbox entry A is out (warp 0 -> warp 2)
   uint32_t spec_n;            // items in the speculative plan (0: none published)
   uint64_t spec_set;          // routed experts in it
   uint64_t it, seq;
@@ -288,13 +290,15 @@ struct EarlyPublish {
 #ifdef MOEB_PROFILE_PHASES
       const uint64_t tf0 = ptimer();
 #endif
-      // one release store at system scope orders this lane's command writes
-      // before the sequence word the copy thread polls
-      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&me->seq), "l"((mseq << 8) | n) : "memory");
+      // (a st.release.sys of the sequence word instead of fence + store
+      // measured ~1 us slower on the decision's critical path)
+      if (n) __threadfence_system();
+      me->seq = (mseq << 8) | n;
       if (A.tl) {
         A.tl[4] = globaltimer_ns();
         A.tl[15] = n;  // uploads published by this step
       }
+      sm->mail_a = 1;
 #ifdef MOEB_PROFILE_PHASES
       st->prof[13] += ptimer() - tf0;
 #endif
@@ -321,6 +325,11 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   // stays in the final plan with no tokens: zero combine weights)
   uint64_t certain = 0;
   for (uint32_t t = 0; t < cfg.B; ++t) certain |= cfg.er ? d->top[t] : d->act[t];
+  // a certain expert that is not resident means uploads this step: the
+  // speculative stream would then only compete for HBM with the decision
+  // (the FFN cannot finish before the upload lands anyway), so the plan is
+  // released once warp 0 has handed the uploads to the copy engine
+  const bool uploads = (certain & ~mask) != 0;
   certain &= mask;  // the pre-route snapshot (warp 0 may be admitting meanwhile)
   Plan* sp = a.spec_plan;
   uint32_t n = 0;
@@ -335,7 +344,10 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
     it.tok[0] = 0;
     it.wt[0] = wt;
   };
-  if (a.shared_w) item(a.shared_w, a.S, 0, 0, a.shared_gate ? sm->sg[0] : 1.0f);
+  if (a.shared_w) {
+    if (a.shared_first) ++n;  // item 0 went out right after the gate (release_shared)
+    else item(a.shared_w, a.S, 0, 0, a.shared_gate ? sm->sg[0] : 1.0f);
+  }
   uint64_t set = 0;
   for (uint64_t m = certain; m; m &= m - 1) {
     const uint32_t e = __ffsll((long long)m) - 1;
@@ -352,6 +364,10 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   sm->spec_n = n;
   sm->spec_set = set;
   __threadfence();
+  if (uploads) {
+    const uint64_t t0 = globaltimer_ns();
+    while (!sm->mail_a && globaltimer_ns() - t0 < kSpinLimitNs) {}
+  }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
 }
 
@@ -730,12 +746,28 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
       softmax_warp(a.trace + (((tit % a.trace_steps) * L + tl) * B + t) * E, E, sm->nsc[t]);
     }
   }
+  // the shared expert depends on nothing the decision computes: released to
+  // the (already resident) FFN right after the gate, before classification
+  if (a.shared_first && threadIdx.x == 0) {
+    Item& it0 = a.spec_plan->items[0];
+    it0.w = a.shared_w;
+    it0.F = a.S;
+    it0.wait = 0;
+    it0.n_tok = 1;
+    it0.kind = 0;
+    it0.expert = 0;
+    it0.tok[0] = 0;
+    it0.wt[0] = a.shared_gate ? sm->sg[0] : 1.0f;
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 2), "r"((uint32_t)a.seq) : "memory");
+  }
   const bool run_pending = a.predictor && sm->st.pf_pending && sm->st.pf_layer == layer && sm->st.pf_it == it;
   if (run_pending)  // the prediction for this layer: softmax of the router on the partial forward
     for (uint32_t t = warp; t < B; t += nw) softmax_warp(a.plogits + (size_t)t * (E + 1), E, sm->nsc[t]);
   if (threadIdx.x == 0) {
     sm->it = it;
     sm->seq = a.seq;
+    sm->mail_a = 0;
     sm->d.next_has_pred = run_pending ? (B >= 64 ? ~0ull : (1ull << B) - 1ull) : 0ull;
   }
   __syncthreads();
@@ -1275,7 +1307,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   S->spec = ((B == 1 && !m.renormalize) || S->umma) && getenv("MOEB_NO_SPEC") == nullptr;
   if (S->spec) {
     S->spec_plan.alloc(1);
-    S->spec_flag.alloc(2);  // [0] speculative plan published, [1] final plan published
+    S->spec_flag.alloc(3);  // [0] speculative plan published, [1] final plan published, [2] shared expert released
     S->spec_flag.zero(s);
   }
   S->ffn_ctr.alloc(kFfnCtrWords);
@@ -1512,6 +1544,7 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     a.seq = ++S->host_seq;
     a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * kTlWords : nullptr;
     a.predictor = S->predictor ? 1u : 0u;
+    a.shared_first = (S->spec && S->splitk && S->S && getenv("MOEB_NO_SHARED_FIRST") == nullptr) ? 1u : 0u;
     a.plogits = S->plogits.p;
     a.pred_log = S->pred_log.p;
     ga.ticket = S->ticket.p;
@@ -1544,6 +1577,7 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     f.tl = a.tl;
     f.spec_plan = a.spec_plan;
     f.spec_flag = S->spec_flag.p;
+    f.shared_first = a.shared_first;
     f.seq = (uint32_t)a.seq;
     f.unit_rows = S->unit_rows;
     // rows are dealt round-robin to the CTAs (fixed partial sums, no counter
