@@ -281,6 +281,9 @@ typedef struct moeb_io_stats {
   double copy_ms; /* sum of per-copy durations on the copy stream */
 } moeb_io_stats;
 int moeb_get_io_stats(moeb_stack* s, moeb_io_stats* st);
+/* Duration (ms, copy-stream CUDA events) of each expert upload since create or
+ * moeb_reset_kernel_stats (first 65536): per-upload PCIe rates. */
+int moeb_get_copy_times(moeb_stack* s, float* ms, size_t cap, size_t* n);
 /* Device buffers for tests: fp32 layer outputs of the last step ([L][B][d]) */
 int moeb_get_layer_outputs(moeb_stack* s, float* out, size_t cap);
 /* Reset the decision state and cache contents to the post-create state

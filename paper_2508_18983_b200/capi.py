@@ -366,6 +366,15 @@ class Stack:
                                          C.byref(n)))
         return out
 
+    def copy_times(self):
+        """Per-upload durations (ms) on the copy stream."""
+        n = C.c_size_t()
+        check(lib().moeb_get_copy_times(self.h, None, C.c_size_t(0), C.byref(n)))
+        out = np.zeros(n.value, dtype=np.float32)
+        check(lib().moeb_get_copy_times(self.h, out.ctypes.data_as(C.POINTER(C.c_float)), C.c_size_t(n.value),
+                                        C.byref(n)))
+        return out
+
     def io_stats(self):
         s = IoStats()
         check(lib().moeb_get_io_stats(self.h, C.byref(s)))

@@ -898,6 +898,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
 struct IoAcc {
   uint64_t h2d_bytes = 0, h2d_copies = 0, d2d_copies = 0, steps = 0;
   double copy_ms = 0.0;
+  std::vector<float> per_copy_ms;  // first 65536 uploads since the last reset (moeb_get_copy_times)
 };
 
 }  // namespace moeb
@@ -1008,7 +1009,10 @@ struct moeb_stack {
     if (!ev_live[i]) return;
     cudaEventSynchronize(ev_b[i]);
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, ev_a[i], ev_b[i]) == cudaSuccess) io.copy_ms += ms;
+    if (cudaEventElapsedTime(&ms, ev_a[i], ev_b[i]) == cudaSuccess) {
+      io.copy_ms += ms;
+      if (io.per_copy_ms.size() < 65536) io.per_copy_ms.push_back(ms);
+    }
     ev_live[i] = false;
   }
 
@@ -1756,6 +1760,16 @@ int moeb_get_scores(moeb_stack* s, float* out, size_t cap, size_t* n) {
     const size_t k = std::min(total, cap);
     if (k) MOEB_CUDA(cudaMemcpy(out, s->scores_log.p, k * sizeof(float), cudaMemcpyDeviceToHost));
     *n = total;
+  });
+}
+
+int moeb_get_copy_times(moeb_stack* s, float* ms, size_t cap, size_t* n) {
+  return guarded([&] {
+    MOEB_CUDA(cudaStreamSynchronize(s->copy_stream));
+    std::lock_guard<std::mutex> g(s->io_mu);
+    for (int i = 0; i < moeb_stack::kEv; ++i) s->harvest(i);
+    *n = s->io.per_copy_ms.size();
+    if (ms) std::memcpy(ms, s->io.per_copy_ms.data(), std::min(cap, *n) * sizeof(float));
   });
 }
 

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--time", action="store_true", help="print per-kernel CUDA-event times")
     ap.add_argument("--timeline", action="store_true", help="device-clock timeline summary per layer-step")
+    ap.add_argument("--uploads", action="store_true", help="per-upload PCIe rate distribution")
     args = ap.parse_args()
     import torch
     from paper_2508_18983_b200 import capi
@@ -47,17 +48,20 @@ def main():
         st.step(x[i].data_ptr(), y.data_ptr(), B)
     st.sync()
     dt = time.time() - t0
-    if args.time:
+    if args.time or args.timeline:
         k = st.kernel_stats()
         print({kk: (round(v / T, 4) if kk.endswith("_ms") else v) for kk, v in k.items() if kk != "prof_ns"},
               "ms/token wall", round(dt * 1e3 / T, 3))
         n = k["route_launches"] or 1
-        names = ["gate", "elect", "stage", "decide", "d:classify", "d:route", "d:hits+record", "d:loads",
+        if not any(k["prof_ns"][i] for i in range(14)):
+            n = 0  # phase timers compiled out (make PROFILE=1)
+        names = ["gate_wait", "staging", "softmax", "decide", "d:classify", "d:route", "d:hits+record", "d:loads",
                  "d:prefetch", "plan", "pub:fence", "span", "pub:copy", "early:fence", "-", "start_skew",
                  "r:spec_publish", "r:route_tokens", "l:BA", "l:cpu_clock", "l:admit_loads", "l:mailbox_A",
                  "l:gpu_clock", "l:deferred", "p:build_items", "p:fill_items", "p:plan_copy", "p:fence_release",
                  "h:counts+mean", "h:record", "-", "-"]
-        print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names) if nm != "-"})
+        if n:
+            print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names) if nm != "-"})
     if args.timeline:
         tl = st.timeline().astype(np.int64)
         tl = tl[len(tl) // 4:]  # skip the cold start
@@ -103,6 +107,14 @@ def main():
         if lat:
             print("single-upload steps", len(lat), "publish->landed minus 17.3MB@54.4GB/s: median us",
                   round(float(np.median(lat)) / 1e3, 2), "p10", round(float(np.percentile(lat, 10)) / 1e3, 2))
+    if args.uploads:
+        ms = st.copy_times()
+        eb = 3 * 1408 * 2048 * 2
+        gbs = eb / (ms.astype(np.float64) * 1e-3) / 1e9
+        q = np.percentile(gbs, [1, 10, 50, 90, 99]) if len(gbs) else []
+        print(f"uploads {len(gbs)} of 17.3 MB: GB/s p1/p10/p50/p90/p99", [round(float(v), 2) for v in q],
+              "mean", round(float(gbs.mean()), 2) if len(gbs) else None,
+              "vs PCIe Gen5 x16 64 GB/s nominal: p50 frac", round(float(np.median(gbs)) / 64.0, 3) if len(gbs) else None)
     st.close()
 
 
