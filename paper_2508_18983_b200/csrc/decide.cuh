@@ -36,6 +36,7 @@ struct StepCtx {
   uint32_t defer_prefetch;
   uint32_t run_pending;
   StepRec* prev_rec;     // nullable: the previous step's record (gets the pending phase's issues)
+  uint32_t f32_scores;   // every score is an fp32 value (the stack): integer-key ranking
 };
 
 __device__ __forceinline__ uint64_t gtimer() {
@@ -756,14 +757,14 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     double b, T, L, R;
     if (j < B) {
       const uint32_t t = j;
-      classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R);
+      classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R, cx.f32_scores != 0);
       if (lane == 0) {
         sm->act[t] = a; sm->top[t] = tp; sm->low[t] = lw; sm->alt[t] = al;
         sm->beta[t] = b; sm->thT[t] = T; sm->thL[t] = L; sm->thR[t] = R;
       }
     } else {
       const uint32_t t = j - B;
-      classify_warp(sm->ns[t], E, k, cfg.alpha, nx->order[t], a, tp, lw, al, b, T, L, R);
+      classify_warp(sm->ns[t], E, k, cfg.alpha, nx->order[t], a, tp, lw, al, b, T, L, R, cx.f32_scores != 0);
       if (lane == 0) { nx->act[t] = a; nx->top[t] = tp; }
     }
   }

@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(kThreads, 1) replay_kernel(ReplayArgs a) {
       cx.target_layer = tl;
       cx.target_it = tit;
       cx.defer_prefetch = 0;
+      cx.f32_scores = 0;
       cx.run_pending = 0;
       cx.prev_rec = nullptr;
       if (cfg.pre && cx.has_target) {

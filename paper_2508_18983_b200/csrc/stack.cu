@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   cx.target_it = tit;
   cx.prof = sm->st.prof;
   cx.defer_prefetch = a.predictor;
+  cx.f32_scores = 1;  // softmax in fp32, widened
   cx.run_pending = run_pending;
   cx.prev_rec = (a.recs && sm->seq >= 2 && sm->seq - 1 <= a.rec_cap) ? a.recs + (sm->seq - 2) : nullptr;
   StepRec* rec = nullptr;
