@@ -279,6 +279,14 @@ int moeb_get_decisions(moeb_stack* s, moeb_step_record* steps, moeb_token_record
 typedef struct moeb_io_stats {
   uint64_t h2d_bytes, h2d_copies, d2d_copies, steps;
   double copy_ms; /* sum of per-copy durations on the copy stream */
+  /* speculative uploads (opt-in experiment, MOEB_SPEC_UPLOAD=1; batch-1 stacks
+   * with stage Pre and a capped cache): after each decision the first expert of the
+   * prefetch queue's ranking that is not resident in the next layer is
+   * uploaded into a side buffer in chunks, only while the copy engine has
+   * nothing else to do; if the next step uploads that expert anyway it comes
+   * from the buffer (promoted: the rest issued at once). Decisions are
+   * untouched. h2d_bytes includes the chunks. */
+  uint64_t spec_jobs, spec_promoted, spec_chunks, spec_bytes;
 } moeb_io_stats;
 int moeb_get_io_stats(moeb_stack* s, moeb_io_stats* st);
 /* Duration (ms, copy-stream CUDA events) of each expert upload since create or

@@ -77,7 +77,8 @@ class Metrics(C.Structure):
 
 class IoStats(C.Structure):
     _fields_ = [("h2d_bytes", C.c_uint64), ("h2d_copies", C.c_uint64), ("d2d_copies", C.c_uint64),
-                ("steps", C.c_uint64), ("copy_ms", C.c_double)]
+                ("steps", C.c_uint64), ("copy_ms", C.c_double), ("spec_jobs", C.c_uint64),
+                ("spec_promoted", C.c_uint64), ("spec_chunks", C.c_uint64), ("spec_bytes", C.c_uint64)]
 
 
 _lib = None

@@ -78,6 +78,11 @@ struct EngineState {
   uint64_t ack_cache;              // last mailbox acknowledgement seen (stack mode)
   uint32_t pf_pending, pf_layer;   // predictor mode: a schedule_prefetch awaits its prediction
   uint64_t pf_it, pf_resident_done;
+  // speculative uploads (stack mode, physical only — decisions unchanged):
+  // buffer b holds (or is receiving) expert sp_expert[b] of (sp_it[b], sp_layer[b])
+  uint32_t sp_gen_next, sp_valid[2], sp_layer[2], sp_expert[2], sp_gen[2], sp_pad;
+  uint64_t sp_it[2];
+  uint64_t sp_jobs, sp_hits;
 };
 
 // Log records (layouts == moeb_task / moeb_window / moeb_eviction).

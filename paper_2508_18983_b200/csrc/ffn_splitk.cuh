@@ -280,6 +280,16 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
     // the uploaded experts, as they land; units from the item's own counter
     for (uint32_t ii = n_ready; ii < n_items; ++ii) {
       if (ii == n_local) snapshot();
+      if (lane == 0 && p->items[ii].spec) {  // a speculative upload buffer
+        const uint32_t sp = p->items[ii].spec, b = sp >> 31, g = sp & 0x7fffffffu;
+        const uint64_t t0 = globaltimer_ns();
+        while ((int32_t)(ld_acquire_u32(a.spec_done + b) - g) < 0) {
+          __nanosleep(128);
+          if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 8u); break; }
+        }
+        if (a.tl && c == 0) a.tl[1] = globaltimer_ns();
+        asm volatile("fence.proxy.async;" ::: "memory");
+      }
       if (lane == 0 && p->items[ii].wait) {
         const uint64_t t0 = globaltimer_ns();
         while ((int32_t)(ld_acquire_u32(a.copies_done) - p->items[ii].wait) < 0) {

@@ -32,7 +32,8 @@ struct Item {
   uint32_t n_tok;
   uint32_t kind;      // 0 shared, 1 resident, 2 loaded, 3 streamed
   uint32_t expert;
-  uint32_t pad;
+  uint32_t spec;      // (buffer << 31) | generation: weights come from a speculative upload
+                      // buffer, ready once spec_done[buffer] >= generation (0: none)
   uint8_t tok[kMaxB];
   float wt[kMaxB];
 };

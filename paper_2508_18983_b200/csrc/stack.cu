@@ -41,6 +41,7 @@
 namespace moeb {
 
 constexpr int kMaxCmds = 3 * kMaxE + 8;
+constexpr int8_t kStageSpec = 127;  // stage_of marker: the expert sits in the speculative buffer
 constexpr uint32_t kRing = 1024;
 
 // Stream memory operations come from the driver API; resolve them through
@@ -77,6 +78,11 @@ struct MailCmd {
   uint64_t bytes;
   uint32_t id;        // upload id; copies_done := id after the copy
   uint32_t wait_ffn;  // nonzero: copy waits for ffn_done >= wait_ffn
+  uint32_t kind;      // 0 upload; 1 speculative upload (the copy thread runs it in chunks
+                      // while the copy engine is otherwise idle); 2 promote: a speculative
+                      // upload is needed now, issue whatever is left of it
+  uint32_t gen, buf;  // speculative: generation, buffer (spec_done[buf] := gen when landed)
+  uint32_t pad;
 };
 // seq word = (sequence << 8) | command count: one 64-bit store publishes
 // both, so an empty entry needs no system fence (only the commands of a
@@ -124,6 +130,8 @@ struct DecideArgs {
   // layer's partial forward (gate CTAs: plogits), logged per step for replay
   uint32_t predictor;
   uint32_t shared_first;      // split-K FFN: the shared expert alone is released right after the gate
+  uint32_t spec_up;           // speculative uploads of the next layer's likely miss
+  uint16_t* specbuf;          // [2][expert_elems]
   const float* plogits;       // [B][E + 1]
   float* pred_log;            // [rec_cap][B][E] or null
 };
@@ -166,6 +174,9 @@ struct DecideKSmem {
   uint16_t* load_dst[kMaxE];
   uint16_t* cpu_dst[kMaxE];
   int8_t stage_of[kMaxE];
+  uint32_t load_spec[kMaxE], cpu_spec[kMaxE];  // Item::spec of each load / streamed expert
+  int32_t spec_slot;          // cache slot the speculative buffer is copied into (-1: none)
+  uint32_t spec_buf;
 };
 
 __device__ __forceinline__ uint64_t ld_acquire_sys_u64(const volatile uint64_t* p) {
@@ -255,6 +266,7 @@ struct EarlyPublish {
       const uint32_t layer = A.layer, E = sm->cfg.E;
       uint32_t si = 0, n = 0;
       for (uint32_t e = 0; e < E; ++e) sm->stage_of[e] = -1;
+      sm->spec_slot = -1;
       auto cmd = [&](uint32_t e, uint16_t* dst) {
         const uint32_t id = ++st->next_copy;
         MailCmd c;
@@ -263,12 +275,54 @@ struct EarlyPublish {
         c.bytes = A.expert_elems * 2;
         c.id = id;
         c.wait_ffn = 0;
+        c.kind = 0;
+        c.gen = c.buf = c.pad = 0;
         me->cmd[n++] = c;
         return id;
       };
+      // the speculative upload meant for this step (buffer seq % 2): an
+      // expert this step uploads anyway comes from there instead — the copy
+      // thread finishes it at once (promote) and the FFN copies it into its
+      // cache slot; decisions are untouched
+      const uint32_t sb = (uint32_t)(sm->seq & 1);
+      uint32_t sp_e = 0xffffffffu, sp_gen = 0;
+      if (A.spec_up && st->sp_valid[sb] && st->sp_layer[sb] == layer && st->sp_it[sb] == sm->it) {
+        sp_e = st->sp_expert[sb];
+        sp_gen = st->sp_gen[sb];
+      }
+      st->sp_valid[sb] = 0;
+      uint16_t* const sbuf = A.specbuf + (size_t)sb * A.expert_elems;
+      auto promote = [&]() {
+        MailCmd c;
+        c.src_off = c.dst = c.bytes = 0;
+        c.id = c.wait_ffn = 0;
+        c.kind = 2;
+        c.gen = sp_gen;
+        c.buf = sb;
+        c.pad = 0;
+        me->cmd[n++] = c;
+        st->sp_hits += 1;
+        sp_e = 0xffffffffu;  // one use
+      };
+      const uint32_t sp_tag = (sb << 31) | sp_gen;
       for (uint32_t i = 0; i < n_load; ++i) {
         const uint32_t e = d->out.load[i];
         const int slot = d->out.load_slot[i];
+        if (e == sp_e) {
+          promote();
+          if (slot >= 0) {
+            sm->spec_slot = slot;
+            sm->spec_buf = sb;
+            ls->slot_copy[slot] = 0;  // filled from the buffer by this step's FFN epilogue
+          } else {
+            sm->stage_of[e] = kStageSpec;  // a deferred admission copies from the buffer
+            sm->spec_buf = sb;
+          }
+          sm->load_id[i] = 0;
+          sm->load_spec[i] = sp_tag;
+          sm->load_dst[i] = sbuf;
+          continue;
+        }
         uint16_t* dst;
         if (slot >= 0) {
           dst = slot_ptr(A, layer, slot);
@@ -279,11 +333,20 @@ struct EarlyPublish {
         const uint32_t id = cmd(e, dst);
         if (slot >= 0) ls->slot_copy[slot] = id;
         sm->load_id[i] = id;
+        sm->load_spec[i] = 0;
         sm->load_dst[i] = dst;
       }
       for (uint32_t i = 0; i < n_cpu; ++i) {
+        if (d->out.cpu[i] == sp_e) {  // BA-streamed: computed straight from the buffer
+          promote();
+          sm->cpu_id[i] = 0;
+          sm->cpu_spec[i] = sp_tag;
+          sm->cpu_dst[i] = sbuf;
+          continue;
+        }
         uint16_t* dst = A.staging + (size_t)(si++ % A.n_stage) * A.expert_elems;
         sm->cpu_id[i] = cmd(d->out.cpu[i], dst);
+        sm->cpu_spec[i] = 0;
         sm->cpu_dst[i] = dst;
       }
       me->n = n;
@@ -419,13 +482,15 @@ __device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
   if (v0) s_wid[e0] = w0;
   if (v1) s_wid[e1] = w1;
   __syncwarp();
-  auto item = [&](uint32_t i, const uint16_t* w, uint32_t F, uint32_t wait, uint32_t kind, uint32_t e) {
+  auto item = [&](uint32_t i, const uint16_t* w, uint32_t F, uint32_t wait, uint32_t kind, uint32_t e,
+                  uint32_t spec = 0) {
     Item& itm = p->items[i];
     itm.w = w;
     itm.F = F;
     itm.wait = wait;
     itm.kind = kind;
     itm.expert = e;
+    itm.spec = spec;
     itm.n_tok = 0;  // token lists are filled in parallel afterwards (fill_items)
   };
   auto place = [&](uint32_t e, int slot, uint32_t w) {
@@ -448,18 +513,25 @@ __device__ void build_items(const DecideArgs& a, DecideKSmem* sm) {
   if (v1) place(e1, s1, w1);
   if (lane == 0 && a.shared_w) item(0, a.shared_w, a.S, 0, 0, 0);
   const uint32_t n0 = base + n_spec + n_rdy + n_wait;
-  for (uint32_t i = lane; i < out.n_load; i += 32) item(n0 + i, sm->load_dst[i], a.F, sm->load_id[i], 2, out.load[i]);
+  for (uint32_t i = lane; i < out.n_load; i += 32)
+    item(n0 + i, sm->load_dst[i], a.F, sm->load_id[i], 2, out.load[i], sm->load_spec[i]);
   for (uint32_t i = lane; i < out.n_cpu; i += 32)
-    item(n0 + out.n_load + i, sm->cpu_dst[i], a.F, sm->cpu_id[i], 3, out.cpu[i]);
+    item(n0 + out.n_load + i, sm->cpu_dst[i], a.F, sm->cpu_id[i], 3, out.cpu[i], sm->cpu_spec[i]);
   const uint32_t n_items = n0 + out.n_load + out.n_cpu;
   if (lane == 0) {
     const int8_t* stage_of = sm->stage_of;
     uint32_t n_d2d = 0;
+    if (sm->spec_slot >= 0) {  // the speculative buffer -> the admitted cache slot
+      p->d2d[n_d2d].src = a.specbuf + (size_t)sm->spec_buf * a.expert_elems;
+      p->d2d[n_d2d].dst = slot_ptr(a, layer, sm->spec_slot);
+      ++n_d2d;
+    }
     for (uint32_t i = 0; i < out.n_def; ++i) {
       const uint32_t e = out.def_e[i];
       const int slot = out.def_slot[i];
       if (stage_of[e] < 0 || slot < 0) continue;
-      p->d2d[n_d2d].src = a.staging + (size_t)stage_of[e] * a.expert_elems;
+      p->d2d[n_d2d].src = stage_of[e] == kStageSpec ? a.specbuf + (size_t)sm->spec_buf * a.expert_elems
+                                                    : a.staging + (size_t)stage_of[e] * a.expert_elems;
       p->d2d[n_d2d].dst = slot_ptr(a, layer, slot);
       ls->slot_copy[slot] = 0;  // filled by this step's FFN epilogue
       ++n_d2d;
@@ -519,6 +591,8 @@ __device__ void build_prefetch_cmds(const DecideArgs& a, DecideKSmem* sm, uint32
     c.bytes = a.expert_elems * 2;
     c.id = id;
     c.wait_ffn = wait_ffn;
+    c.kind = 0;
+    c.gen = c.buf = c.pad = 0;
     LayerState* tls = (tlayer == layer) ? &sm->ls : &sm->tls;
     if (slot >= 0) tls->slot_copy[slot] = id;
   }
@@ -815,6 +889,39 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     // predictor mode: entry B of this step is published by the next step
     if (!a.predictor) build_prefetch_cmds(a, sm, (uint32_t)sm->seq);
     else sm->n_cmds = 0;
+    // speculative upload for the next step: the first expert of the prefetch
+    // queue's ranking that is still not resident in the target layer after
+    // this step's prefetches (the reference's predictor, prefetch.cpp:34-115;
+    // its virtual clock decides what is ADMITTED, this only moves bytes early)
+    if (a.spec_up && !a.predictor && want_next) {
+      const LayerState* tls = (tl == layer) ? &sm->ls : &sm->tls;
+      uint32_t cand = 0xffffffffu;
+      for (uint32_t r = 0; r < E; ++r)
+        if (!((tls->mask >> sm->d.qorder[r]) & 1ull)) { cand = sm->d.qorder[r]; break; }
+      const uint32_t b = (uint32_t)((sm->seq + 1) & 1);
+      if (cand != 0xffffffffu) {
+        EngineState* st = &sm->st;
+        const uint32_t gen = ++st->sp_gen_next;
+        st->sp_valid[b] = 1;
+        st->sp_layer[b] = tl;
+        st->sp_it[b] = tit;
+        st->sp_expert[b] = cand;
+        st->sp_gen[b] = gen;
+        st->sp_jobs += 1;
+        MailCmd& c = sm->cmd[sm->n_cmds++];
+        c.src_off = ((uint64_t)tl * E + cand) * a.expert_elems * 2;
+        c.dst = (uint64_t)(a.specbuf + (size_t)b * a.expert_elems);
+        c.bytes = a.expert_elems * 2;
+        c.id = 0;
+        c.wait_ffn = 0;
+        c.kind = 1;
+        c.gen = gen;
+        c.buf = b;
+        c.pad = 0;
+      } else {
+        sm->st.sp_valid[b] = 0;
+      }
+    }
     // entry B's ring slot must have been consumed by the copy thread
     if (!a.predictor) wait_ring_slot(a, 2 * sm->seq, &sm->st.ack_cache);
     sm->st.seq = sm->seq;
@@ -899,6 +1006,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
 struct IoAcc {
   uint64_t h2d_bytes = 0, h2d_copies = 0, d2d_copies = 0, steps = 0;
   double copy_ms = 0.0;
+  uint64_t spec_jobs = 0, spec_promoted = 0, spec_chunks = 0, spec_bytes = 0;
   std::vector<float> per_copy_ms;  // first 65536 uploads since the last reset (moeb_get_copy_times)
 };
 
@@ -918,6 +1026,18 @@ struct moeb_stack {
   // predictor mode (MOEB_MODEL_PREDICTOR): partial forward, its router
   // logits, the predictions used per step
   bool predictor = false;
+  // speculative uploads (split-K stacks with stage Pre and a logits trace):
+  // two expert-sized buffers, their landed generations, the copy thread's jobs
+  bool spec_up = false;
+  DevBuf<uint16_t> specbuf;
+  DevBuf<uint32_t> spec_done;
+  struct SpecJob {
+    uint32_t gen = 0, chunks = 0, next = 0;  // next: chunks issued so far
+    uint64_t src_off = 0, dst = 0, bytes = 0;
+    bool live = false;
+  } sjob[2];
+  cudaEvent_t ev_spec = nullptr, ev_dem = nullptr;  // last speculative chunk / last upload issued
+  bool spec_inflight = false, dem_inflight = false;
   DevBuf<uint16_t> xpred;
   DevBuf<float> plogits, pred_log;
   DevBuf<EngineState> st;
@@ -971,6 +1091,7 @@ struct moeb_stack {
   static constexpr int kEv = 512;
   cudaEvent_t ev_a[kEv] = {}, ev_b[kEv] = {};
   bool ev_live[kEv] = {};
+  bool ev_chunk[kEv] = {};
   int ev_next = 0;
 
   // Kernel timing (MOEB_MODEL_TIME_KERNELS): 3 events per layer on the
@@ -1012,9 +1133,79 @@ struct moeb_stack {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ev_a[i], ev_b[i]) == cudaSuccess) {
       io.copy_ms += ms;
-      if (io.per_copy_ms.size() < 65536) io.per_copy_ms.push_back(ms);
+      if (!ev_chunk[i] && io.per_copy_ms.size() < 65536) io.per_copy_ms.push_back(ms);
     }
     ev_live[i] = false;
+    ev_chunk[i] = false;
+  }
+
+  // one upload: the copy, then copies_done := id (the FFN waits on it)
+  void issue_upload(const MailCmd& c, CUdeviceptr done_ptr) {
+    // submit first, account after: the copy's start is what the GPU waits for
+    const int ei = ev_next;
+    ev_next = (ev_next + 1) % kEv;
+    {
+      std::lock_guard<std::mutex> g(io_mu);
+      harvest(ei);  // recorded kEv uploads ago: long complete
+    }
+    cudaEventRecord(ev_a[ei], copy_stream);
+    const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(c.dst),
+                                           reinterpret_cast<const char*>(pool) + c.src_off, c.bytes,
+                                           cudaMemcpyHostToDevice, copy_stream);
+    if (p_write32(copy_stream, done_ptr, c.id, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+      copier_msg = "cuStreamWriteValue32 failed";
+      copier_error = 5;
+    }
+    cudaEventRecord(ev_b[ei], copy_stream);
+    if (ce != cudaSuccess) {
+      copier_msg = std::string("upload failed: ") + cudaGetErrorString(ce);
+      copier_error = 5;
+    }
+    std::lock_guard<std::mutex> g(io_mu);
+    ev_live[ei] = true;
+    io.h2d_bytes += c.bytes;
+    io.h2d_copies += 1;
+  }
+
+  // Speculative uploads move in chunks so a real upload never queues behind
+  // more than one chunk: a chunk is issued only while the copy stream has no
+  // upload and no other chunk in flight. The last chunk sets spec_done[buf].
+  static constexpr uint32_t kSpecChunks = 16;  // ~1.1 MB, ~20 us each for a DSV2-Lite expert
+  void issue_spec_chunk(uint32_t b) {
+    SpecJob& j = sjob[b];
+    const uint64_t per = (j.bytes / j.chunks + 255) & ~255ull;
+    const uint64_t off = (uint64_t)j.next * per;
+    const uint64_t n = off < j.bytes ? std::min(per, j.bytes - off) : 0;
+    const int ei = ev_next;
+    ev_next = (ev_next + 1) % kEv;
+    {
+      std::lock_guard<std::mutex> g(io_mu);
+      harvest(ei);
+    }
+    cudaEventRecord(ev_a[ei], copy_stream);
+    const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(j.dst + off),
+                                           reinterpret_cast<const char*>(pool) + j.src_off + off, n,
+                                           cudaMemcpyHostToDevice, copy_stream);
+    cudaEventRecord(ev_b[ei], copy_stream);
+    if (ce != cudaSuccess) {
+      copier_msg = std::string("speculative upload failed: ") + cudaGetErrorString(ce);
+      copier_error = 5;
+    }
+    j.next += 1;
+    if (j.next == j.chunks) {
+      if (p_write32(copy_stream, (CUdeviceptr)(spec_done.p + b), j.gen, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+          CUDA_SUCCESS) {
+        copier_msg = "cuStreamWriteValue32 failed";
+        copier_error = 5;
+      }
+      j.live = false;
+    }
+    std::lock_guard<std::mutex> g(io_mu);
+    ev_live[ei] = true;
+    ev_chunk[ei] = true;  // copy-engine busy time, not a whole-expert upload
+    io.spec_chunks += 1;
+    io.spec_bytes += n;
+    io.h2d_bytes += n;
   }
 
   void copy_loop() {
@@ -1023,10 +1214,28 @@ struct moeb_stack {
     CUdeviceptr ffn_ptr = (CUdeviceptr)ffn_done.p;
     uint64_t expect = 1;
     unsigned spins = 0;
+    auto t_poll = std::chrono::steady_clock::now();
     while (!stop.load(std::memory_order_relaxed)) {
       MailEntry* me = &ring[expect % kRing];
       const uint64_t sv = me->seq;
       if ((sv >> 8) != expect) {
+        // idle: feed the copy engine a speculative chunk when nothing else
+        // occupies it (event queries at most every 2 us)
+        if (spec_up && (sjob[0].live || sjob[1].live)) {
+          const auto now = std::chrono::steady_clock::now();
+          if (now - t_poll > std::chrono::microseconds(2)) {
+            t_poll = now;
+            if (dem_inflight && cudaEventQuery(ev_dem) == cudaSuccess) dem_inflight = false;
+            if (spec_inflight && cudaEventQuery(ev_spec) == cudaSuccess) spec_inflight = false;
+            if (!dem_inflight && !spec_inflight) {
+              // the older job first
+              const int b = (sjob[0].live && (!sjob[1].live || sjob[0].gen < sjob[1].gen)) ? 0 : 1;
+              issue_spec_chunk((uint32_t)b);
+              cudaEventRecord(ev_spec, copy_stream);
+              spec_inflight = true;
+            }
+          }
+        }
         // a dedicated poller: the mailbox is the decode loop's critical path
         // (publish -> copy start); yield only after a long idle stretch
         if (++spins > (1u << 20)) std::this_thread::yield();
@@ -1036,37 +1245,41 @@ struct moeb_stack {
       spins = 0;
       std::atomic_thread_fence(std::memory_order_acquire);
       const uint32_t n = (uint32_t)(sv & 0xff);
+      bool uploaded = false;
       for (uint32_t i = 0; i < n; ++i) {
         const MailCmd c = me->cmd[i];
+        if (c.kind == 1) {  // a new speculative job (supersedes whatever was left in its buffer)
+          SpecJob& j = sjob[c.buf & 1];
+          j.gen = c.gen;
+          j.chunks = kSpecChunks;
+          j.next = 0;
+          j.src_off = c.src_off;
+          j.dst = c.dst;
+          j.bytes = c.bytes;
+          j.live = true;
+          std::lock_guard<std::mutex> g(io_mu);
+          io.spec_jobs += 1;
+          continue;
+        }
+        if (c.kind == 2) {  // promoted: the step needs it now
+          SpecJob& j = sjob[c.buf & 1];
+          if (j.live && j.gen == c.gen)
+            while (j.live) issue_spec_chunk(c.buf & 1);
+          std::lock_guard<std::mutex> g(io_mu);
+          io.spec_promoted += 1;
+          continue;
+        }
         if (c.wait_ffn &&
             p_wait32(copy_stream, ffn_ptr, c.wait_ffn, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
           copier_msg = "cuStreamWaitValue32 failed";
           copier_error = 5;
         }
-        // submit first, account after: the copy's start is what the GPU waits for
-        const int ei = ev_next;
-        ev_next = (ev_next + 1) % kEv;
-        {
-          std::lock_guard<std::mutex> g(io_mu);
-          harvest(ei);  // recorded kEv uploads ago: long complete
-        }
-        cudaEventRecord(ev_a[ei], copy_stream);
-        const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(c.dst),
-                                               reinterpret_cast<const char*>(pool) + c.src_off, c.bytes,
-                                               cudaMemcpyHostToDevice, copy_stream);
-        if (p_write32(copy_stream, done_ptr, c.id, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
-          copier_msg = "cuStreamWriteValue32 failed";
-          copier_error = 5;
-        }
-        cudaEventRecord(ev_b[ei], copy_stream);
-        if (ce != cudaSuccess) {
-          copier_msg = std::string("upload failed: ") + cudaGetErrorString(ce);
-          copier_error = 5;
-        }
-        std::lock_guard<std::mutex> g(io_mu);
-        ev_live[ei] = true;
-        io.h2d_bytes += c.bytes;
-        io.h2d_copies += 1;
+        issue_upload(c, done_ptr);
+        uploaded = true;
+      }
+      if (uploaded && spec_up) {
+        cudaEventRecord(ev_dem, copy_stream);
+        dem_inflight = true;
       }
       std::atomic_thread_fence(std::memory_order_release);
       *reinterpret_cast<volatile uint64_t*>(ack) = expect;
@@ -1085,6 +1298,8 @@ struct moeb_stack {
       if (ev_a[i]) cudaEventDestroy(ev_a[i]);
       if (ev_b[i]) cudaEventDestroy(ev_b[i]);
     }
+    if (ev_spec) cudaEventDestroy(ev_spec);
+    if (ev_dem) cudaEventDestroy(ev_dem);
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ring) cudaFreeHost(ring);
@@ -1162,6 +1377,7 @@ static void reset_state(moeb_stack* S, cudaStream_t s) {
   rng_seed(st.rng, derive_seed(S->cfg.seed, 0x94ed1c70ULL));  // pipeline.cpp:62
   st.seq = prev.seq;
   st.next_copy = prev.next_copy;
+  st.sp_gen_next = prev.sp_gen_next;  // spec_done only grows
   st.ack_cache = prev.ack_cache;
   st.prof[14] = ~0ull;  // running minimum of CTA start times (phase profiling)
   S->hist.zero(s);
@@ -1393,6 +1609,22 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // is left to it
   S->ffn_grid = S->spec ? sms - 1 : sms;
   S->serial = serial_mode_requested();
+  // speculative uploads (opt-in, MOEB_SPEC_UPLOAD=1): the split-K (batch-1)
+  // path with stage Pre and a capped cache; not in serial (profiler) mode.
+  // Measured on the bench workload: 9.91 vs 7.86 ms/token without — half the
+  // guesses are wrong, chunked copies run at ~44 vs ~53 GB/s, a wrong guess
+  // delays the next real upload by a chunk, and a right one costs a buffer ->
+  // slot copy in the FFN epilogue. Kept as an experiment.
+  const char* spv = getenv("MOEB_SPEC_UPLOAD");
+  S->spec_up = spv && spv[0] == '1' && S->splitk && cfg.pre && cfg.slots < cfg.experts && !S->serial &&
+               !S->predictor;
+  if (S->spec_up) {
+    S->specbuf.alloc(2 * S->expert_elems);
+    S->spec_done.alloc(2);
+    S->spec_done.zero(s);
+    MOEB_CUDA(cudaEventCreateWithFlags(&S->ev_spec, cudaEventDisableTiming));
+    MOEB_CUDA(cudaEventCreateWithFlags(&S->ev_dem, cudaEventDisableTiming));
+  }
   if (S->serial && !getenv("MOEB_SERIAL"))
     fprintf(stderr, "moeb: profiler detected, serial pipeline mode (set MOEB_SERIAL=0 to override)\n");
   MOEB_CUDA(cudaStreamSynchronize(s));
@@ -1550,6 +1782,8 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     a.tl = S->timeline.p ? S->timeline.p + ((a.seq - 1) % 16384) * kTlWords : nullptr;
     a.predictor = S->predictor ? 1u : 0u;
     a.shared_first = (S->spec && S->splitk && S->S && getenv("MOEB_NO_SHARED_FIRST") == nullptr) ? 1u : 0u;
+    a.spec_up = S->spec_up ? 1u : 0u;
+    a.specbuf = S->specbuf.p;
     a.plogits = S->plogits.p;
     a.pred_log = S->pred_log.p;
     ga.ticket = S->ticket.p;
@@ -1583,6 +1817,7 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     f.spec_plan = a.spec_plan;
     f.spec_flag = S->spec_flag.p;
     f.shared_first = a.shared_first;
+    f.spec_done = S->spec_done.p;
     f.seq = (uint32_t)a.seq;
     f.unit_rows = S->unit_rows;
     // rows are dealt round-robin to the CTAs (fixed partial sums, no counter
@@ -1799,6 +2034,10 @@ int moeb_get_io_stats(moeb_stack* s, moeb_io_stats* out) {
     out->d2d_copies = s->io.d2d_copies;
     out->steps = s->io.steps;
     out->copy_ms = s->io.copy_ms;
+    out->spec_jobs = s->io.spec_jobs;
+    out->spec_promoted = s->io.spec_promoted;
+    out->spec_chunks = s->io.spec_chunks;
+    out->spec_bytes = s->io.spec_bytes;
   });
 }
 

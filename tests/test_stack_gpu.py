@@ -219,7 +219,10 @@ def test_dsv2_lite_full_stack(gpu):
     dec, gsc, m = check_decisions(st, kw, T)
     io = st.io_stats()
     eb = 3 * 1408 * 2048 * 2
-    assert io["h2d_bytes"] == (m["demand_loads"] + m["cpu_computed"] + m["prefetch_loads"]) * eb
+    # every decided upload moved once: by its own copy, or (promoted) by the
+    # speculative upload that anticipated it; wasted speculation on top
+    assert io["h2d_bytes"] - io["spec_bytes"] + io["spec_promoted"] * eb == \
+        (m["demand_loads"] + m["cpu_computed"] + m["prefetch_loads"]) * eb
     assert m["demand_loads"] + m["cpu_computed"] > 0  # the capped cache really uploads
     st.close()
 
@@ -261,4 +264,23 @@ def test_decision_log_overflow_is_loud(gpu):
     assert ei.value.code == 4 and "overflow" in ei.value.msg
     with pytest.raises(gpu.MoebError):
         st.scores()
+    st.close()
+
+
+def test_speculative_uploads_keep_decisions_and_outputs(gpu, monkeypatch):
+    """MOEB_SPEC_UPLOAD=1 (opt-in): the next layer's likely miss is uploaded
+    into a side buffer while the copy engine idles and used when that upload
+    is decided. Decisions and outputs are those of the default path; every
+    decided upload moved exactly once (by its own copy or the buffer)."""
+    import torch
+    monkeypatch.setenv("MOEB_SPEC_UPLOAD", "1")
+    L, E, k, d, F, S, slots, T = 3, 16, 4, 256, 128, 256, 4, 40
+    st, kw, xs, y = run_stack(gpu, torch, L, E, k, 1, d, F, S, slots, T)
+    dec, gsc, m = check_decisions(st, kw, T)
+    check_outputs(st, kw, xs, dec, gsc, d, F, S)
+    io = st.io_stats()
+    eb = 3 * F * d * 2
+    assert io["spec_jobs"] > 0 and io["spec_promoted"] > 0
+    assert io["h2d_bytes"] - io["spec_bytes"] + io["spec_promoted"] * eb == \
+        (m["demand_loads"] + m["cpu_computed"] + m["prefetch_loads"]) * eb
     st.close()

@@ -81,7 +81,8 @@ def run_case(capi, torch, cfg_d, model_d, T, K, hbm_peak, pcie_peak, pool=None, 
     m1, io1, ks = st.metrics(), st.io_stats(), st.kernel_stats()
     sel = m1["selections"] - m0["selections"]
     b_hbm = (ks["ffn_bytes"] + ks["route_bytes"]) / K
-    b_pcie = (io1["h2d_bytes"]) / K  # reset_kernel_stats zeroed the io counters
+    eb = 3 * model_d["ffn"] * d * 2
+    b_pcie = (io1["h2d_bytes"] - io1["spec_bytes"] + io1["spec_promoted"] * eb) / K  # io counters zeroed above
     t_roof = max(b_hbm / (hbm_peak * 1e9), b_pcie / (pcie_peak * 1e9)) * 1e3
     row = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B * 1e3 / ms, 1),
            "ms_per_token": round(ms / B, 4), "hit_rate": round((m1["hits"] - m0["hits"]) / max(sel, 1), 4),

@@ -1,4 +1,8 @@
-timeout 900 python -m pytest tests/test_stack_gpu.py tests/test_configs_gpu.py tests/test_bridge.py -x -q > gpurun_out/pytest_stack.log 2>&1; echo "rc $?" >> gpurun_out/pytest_stack.log
-timeout 300 python tools/profile_stack.py --tokens 48 --allhit --timeline > gpurun_out/tl_hit.log 2>&1
-timeout 300 python tools/profile_stack.py --tokens 96 --timeline > gpurun_out/tl_miss.log 2>&1
-MOEB_NO_SPEC=1 timeout 300 python tools/profile_stack.py --tokens 48 --allhit --timeline > gpurun_out/tl_hit_nospec.log 2>&1
+set -x
+timeout 900 python -m pytest tests/test_stack_gpu.py tests/test_configs_gpu.py -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/phases.log
+for env in "MOEB_X=0" "MOEB_SPEC_UPLOAD=0"; do
+  echo "== $env --tokens 64 --timeline" >> gpurun_out/phases.log
+  env $env timeout 300 python tools/profile_stack.py --tokens 64 --timeline >> gpurun_out/phases.log 2>&1
+done
+timeout 900 python bench.py --no-cpu-baseline --no-batched --no-c5 > gpurun_out/bench.log 2>&1; echo "bench rc $?" >> gpurun_out/bench.log

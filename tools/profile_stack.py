@@ -63,6 +63,9 @@ def main():
         if n:
             print("us per launch:", {nm: round(k["prof_ns"][i] / n / 1e3, 2) for i, nm in enumerate(names) if nm != "-"})
     if args.timeline:
+        io = st.io_stats()
+        print("wall ms/token", round(dt * 1e3 / T, 3), "uploads", io["h2d_copies"], "speculative jobs", io["spec_jobs"],
+              "used", io["spec_promoted"], "chunks", io["spec_chunks"])
         tl = st.timeline().astype(np.int64)
         tl = tl[len(tl) // 4:]  # skip the cold start
         us = lambda v: round(float(np.mean(v)) / 1e3, 2) if len(v) else None
