@@ -1139,14 +1139,27 @@ struct moeb_stack {
     ev_chunk[i] = false;
   }
 
+  // Harvest the oldest live copy-event pair if it has completed (idle loop;
+  // a non-blocking query, so the poller stays responsive).
+  void harvest_some() {
+    for (int n = 0; n < 4; ++n) {  // the oldest slots: the next ones to be reused
+      const int i = (ev_next + n) % kEv;
+      if (!ev_live[i]) continue;
+      if (cudaEventQuery(ev_b[i]) != cudaSuccess) return;
+      std::lock_guard<std::mutex> g(io_mu);
+      harvest(i);
+      return;
+    }
+  }
+
   // one upload: the copy, then copies_done := id (the FFN waits on it)
   void issue_upload(const MailCmd& c, CUdeviceptr done_ptr) {
     // submit first, account after: the copy's start is what the GPU waits for
     const int ei = ev_next;
     ev_next = (ev_next + 1) % kEv;
-    {
+    if (ev_live[ei]) {  // normally harvested while the thread idled (harvest_some)
       std::lock_guard<std::mutex> g(io_mu);
-      harvest(ei);  // recorded kEv uploads ago: long complete
+      harvest(ei);
     }
     cudaEventRecord(ev_a[ei], copy_stream);
     const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(c.dst),
@@ -1178,7 +1191,7 @@ struct moeb_stack {
     const uint64_t n = off < j.bytes ? std::min(per, j.bytes - off) : 0;
     const int ei = ev_next;
     ev_next = (ev_next + 1) % kEv;
-    {
+    if (ev_live[ei]) {
       std::lock_guard<std::mutex> g(io_mu);
       harvest(ei);
     }
@@ -1219,6 +1232,9 @@ struct moeb_stack {
       MailEntry* me = &ring[expect % kRing];
       const uint64_t sv = me->seq;
       if ((sv >> 8) != expect) {
+        // idle: account completed copies off the critical path (the slot
+        // about to be reused first), so issuing an upload never waits on it
+        harvest_some();
         // idle: feed the copy engine a speculative chunk when nothing else
         // occupies it (event queries at most every 2 us)
         if (spec_up && (sjob[0].live || sjob[1].live)) {

@@ -169,6 +169,53 @@ def c4(capi, torch, hbm, pcie, cpu):
     return out
 
 
+def c2_predictor(capi, torch, hbm, pcie, cpu):
+    """The headline shape in weight-driven mode: routing from the router GEMV
+    on the hidden stream, stage Pre fed by the paper's partial-forward
+    predictor (MOEB_MODEL_PREDICTOR). Reports ms/token and the prefetch
+    accuracy in the reference's PredictorStats vocabulary (prefetch.hpp:68-88):
+    the predicted head's class against the true scores of that step."""
+    cfg, model = split(DSV2)
+    L, E, B, d, T, K = 26, 64, 1, 2048, 64, 48
+    out = {"workload": "DeepSeek-V2-Lite 26 L, batch 1, cache 16/64, weight-driven routing, stage Pre with the "
+                       "partial-forward predictor (shared expert + resident hits -> next layer's router)"}
+    res = {}
+    for name, pred in (("predictor", True), ("pre_off", False)):
+        cfg_d = dict(cfg, num_layers=L, batch=B, slots=16, alpha=0.25, seed=7, pre=1 if pred else 0)
+        st = capi.Stack(capi.Config.make(**cfg_d), weight_seed=7, predictor=pred, **model)
+        x = torch.from_numpy(bench.ar1_hidden(T, B, d, 7)).to(torch.bfloat16).cuda()
+        y = torch.empty((B, d), dtype=torch.bfloat16, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for i in range(T - K):
+                st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+            st.sync()
+            m0 = st.metrics()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for i in range(T - K, T):
+                st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+            e1.record(s)
+            e1.synchronize()
+            st.sync()
+        m1 = st.metrics()
+        dm = {k: m1[k] - m0[k] for k in m1 if isinstance(m1[k], int)}
+        sel = max(dm["selections"], 1)
+        row = {"ms_per_token": round(e0.elapsed_time(e1) / K, 4), "hit_rate": round(dm["hits"] / sel, 4),
+               "demand_loads": dm["demand_loads"], "streamed_ba": dm["cpu_computed"],
+               "prefetch_loads": dm["prefetch_loads"]}
+        if pred:
+            n = max(dm["trace_supplied"], 1)
+            row["predictor_stats"] = {"predictions": dm["trace_supplied"], "head_top_frac": round(dm["head_top"] / n, 4),
+                                      "head_active_frac": round(dm["head_active"] / n, 4),
+                                      "head_inactive_frac": round(dm["head_inactive"] / n, 4),
+                                      "issued": dm["issued"], "cancelled": dm["cancelled"]}
+        res[name] = row
+        st.close()
+    out.update(res)
+    return out
+
+
 def c5(capi, torch, hbm, pcie, cpu):
     from paper_2508_18983_b200 import partition
     out = {"workload": "64 DeepSeek-V2-Lite requests x 16 tokens, stream-partitioned, cache 16/64, 1 GPU", "batch": {}}
@@ -180,7 +227,7 @@ def c5(capi, torch, hbm, pcie, cpu):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="C1,C3,C4,C5")
+    ap.add_argument("--only", default="C1,C2P,C3,C4,C5")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -192,7 +239,8 @@ def main():
     res = {"hbm_peak_gbs": hbm, "pcie_peak_gbs": round(pcie, 2), "gpu": torch.cuda.get_device_name(0)}
     for name in args.only.split(","):
         t0 = time.time()
-        res[name] = {"C1": c1, "C3": c3, "C4": c4, "C5": c5}[name](capi, torch, hbm, pcie, not args.no_cpu)
+        res[name] = {"C1": c1, "C2P": c2_predictor, "C3": c3, "C4": c4, "C5": c5}[name](capi, torch, hbm, pcie,
+                                                                                     not args.no_cpu)
         res[name]["wall_s"] = round(time.time() - t0, 1)
         print(f"{name} done in {res[name]['wall_s']} s", file=sys.stderr, flush=True)
         if args.out:

@@ -29,15 +29,17 @@ def main():
     ap.add_argument("--time", action="store_true", help="print per-kernel CUDA-event times")
     ap.add_argument("--timeline", action="store_true", help="device-clock timeline summary per layer-step")
     ap.add_argument("--uploads", action="store_true", help="per-upload PCIe rate distribution")
+    ap.add_argument("--shape", default="dsv2", choices=["dsv2", "qwen"], help="DeepSeek-V2-Lite or Qwen1.5-MoE widths")
     args = ap.parse_args()
     import torch
     from paper_2508_18983_b200 import capi
 
-    L, E, B, d = args.layers, 64, args.batch, 2048
-    cfg = capi.Config.make(num_layers=L, experts=E, top_k=6, batch=B, alpha=0.25, seed=7,
-                           slots=E if args.allhit else 16)
-    st = capi.Stack(cfg, 2048, 1408, 2816, weight_seed=7, time_kernels=args.time, trace_timeline=args.timeline,
-                    log_steps=args.timeline)
+    qwen = args.shape == "qwen"
+    L, E, B, d = args.layers, (60 if qwen else 64), args.batch, 2048
+    cfg = capi.Config.make(num_layers=L, experts=E, top_k=4 if qwen else 6, batch=B, alpha=0.25, seed=7,
+                           slots=E if args.allhit else (15 if qwen else 16))
+    st = capi.Stack(cfg, 2048, 1408, 5632 if qwen else 2816, shared_gate=1 if qwen else 0, weight_seed=7,
+                    time_kernels=args.time, trace_timeline=args.timeline, log_steps=args.timeline)
     T = args.tokens
     st.set_logits_trace(capi.trace_logits(capi.generate_trace(L, E, B, T, 7)), T)
     x = torch.randn(T, B, d).to(torch.bfloat16).cuda()
@@ -87,7 +89,7 @@ def main():
         eb = 3 * 1408 * 2048 * 2
         nexp = [len({e for t in r["tok"] for e in t["sel"]}) for r in dec]
         nexp = np.array(nexp[len(nexp) - len(tl):] if len(nexp) >= len(tl) else nexp, dtype=np.float64)
-        wbytes = nexp * eb + 2 * eb
+        wbytes = nexp * eb + (4 if qwen else 2) * eb
         ffn_ns = (tl[:, 2] - tl[:, 0]).astype(np.float64)
         if len(nexp) == len(tl) and (~miss).any():
             print("distinct experts per layer-step", round(float(nexp.mean()), 2), "weight MB", round(float(wbytes.mean()) / 1e6, 1),
