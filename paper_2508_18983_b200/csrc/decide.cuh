@@ -327,21 +327,29 @@ __device__ inline void coalesce_warp(DecideSmem* sm, uint32_t B, uint32_t E, uin
       if (!low) continue;
       const double* s = sm->s[t];
       const uint64_t band = s_band[t];
-      uint64_t selm = 0;
-      for (uint32_t i = 0; i < sm->nsel[t]; ++i) selm |= bit(sm->sel[t][i]);
+      // the token's selection as a mask: lane i holds entry i (k <= 16 < 32)
+      uint64_t selm;
+      {
+        const uint32_t e = lane < sm->nsel[t] ? sm->sel[t][lane] : 64u;
+        const uint32_t lo = __reduce_or_sync(0xffffffffu, e < 32 ? 1u << e : 0u);
+        const uint32_t hi = __reduce_or_sync(0xffffffffu, (e >= 32 && e < 64) ? 1u << (e - 32) : 0u);
+        selm = (uint64_t)lo | ((uint64_t)hi << 32);
+      }
       for (uint32_t r = 0; r < k; ++r) {
         const uint32_t orig = sm->order[t][r];
         if (!has(low, orig)) continue;
-        int kept_pos = -1, sub_pos = -1;
-        for (uint32_t i = 0; i < sm->nkept[t]; ++i)
-          if (sm->kept[t][i] == orig) { kept_pos = (int)i; break; }
+        // the slot's occupant: a kept low is its own; a substituted one, its
+        // substitute (lane i checks list entry i: first match as the scans)
+        const uint32_t km = __ballot_sync(0xffffffffu, lane < sm->nkept[t] && sm->kept[t][lane] == orig);
+        const uint32_t smk = __ballot_sync(0xffffffffu, lane < sm->nsub[t] && sm->sub_d[t][lane] == orig);
+        const int kept_pos = km ? __ffs(km) - 1 : -1;
+        int sub_pos = -1;
         uint32_t occupant;
         if (kept_pos >= 0) {
           occupant = orig;
         } else {
-          for (uint32_t i = 0; i < sm->nsub[t]; ++i)
-            if (sm->sub_d[t][i] == orig) { sub_pos = (int)i; break; }
-          if (sub_pos < 0) continue;
+          if (!smk) continue;
+          sub_pos = __ffs(smk) - 1;
           occupant = sm->sub_c[t][sub_pos];
         }
         const uint32_t occ_others = cnt[occupant] - 1u;
@@ -693,6 +701,7 @@ __device__ inline void deferred_prefetch(const StepCtx& cx, DecideSmem* sm, uint
     ++n_pref;
     __syncwarp();
   }
+  __syncwarp();  // every lane has read pcie_free
   if (lane == 0) {
     if (t > st->pcie_free) st->pcie_free = t;
     st->q_valid = 1;
@@ -751,21 +760,15 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   }
   // classify every token (and the prefetch target's tokens) — warp per token
   const bool want_next = cfg.pre && cx.has_target && !cx.defer_prefetch;
-  const uint32_t jobs = want_next ? 2 * B : B;
-  for (uint32_t j = warp; j < jobs; j += nw) {
+  // this step's tokens now; the prefetch target's tokens (only the predictor
+  // on warp 1 needs them) are classified after the fork by warps 4..
+  for (uint32_t t = warp; t < B; t += nw) {
     uint64_t a, tp, lw, al;
     double b, T, L, R;
-    if (j < B) {
-      const uint32_t t = j;
-      classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R, cx.f32_scores != 0);
-      if (lane == 0) {
-        sm->act[t] = a; sm->top[t] = tp; sm->low[t] = lw; sm->alt[t] = al;
-        sm->beta[t] = b; sm->thT[t] = T; sm->thL[t] = L; sm->thR[t] = R;
-      }
-    } else {
-      const uint32_t t = j - B;
-      classify_warp(sm->ns[t], E, k, cfg.alpha, nx->order[t], a, tp, lw, al, b, T, L, R, cx.f32_scores != 0);
-      if (lane == 0) { nx->act[t] = a; nx->top[t] = tp; }
+    classify_warp(sm->s[t], E, k, cfg.alpha, sm->order[t], a, tp, lw, al, b, T, L, R, cx.f32_scores != 0);
+    if (lane == 0) {
+      sm->act[t] = a; sm->top[t] = tp; sm->low[t] = lw; sm->alt[t] = al;
+      sm->beta[t] = b; sm->thT[t] = T; sm->thL[t] = L; sm->thR[t] = R;
     }
   }
   __syncthreads();
@@ -847,8 +850,22 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   // nothing before the first admission reads the history, so recording it
   // beside the routing is the same computation as recording it after.
   const bool want_pred = want_next;
+  const uint32_t nx_threads = (nw - 4 + 1) * 32;  // warps 4.. + warp 1 (barrier 5)
+  if (warp >= 4) {
+    if (want_pred) {
+      for (uint32_t t = warp - 4; t < B; t += nw - 4) {
+        uint64_t a, tp, lw, al;
+        double b, T, L, R;
+        classify_warp(sm->ns[t], E, k, cfg.alpha, nx->order[t], a, tp, lw, al, b, T, L, R, cx.f32_scores != 0);
+        if (lane == 0) { nx->act[t] = a; nx->top[t] = tp; }
+      }
+      asm volatile("bar.arrive 5, %0;" ::"r"(nx_threads) : "memory");
+    }
+    return;
+  }
   if (warp == 1) {
     if (want_pred) {
+      asm volatile("bar.sync 5, %0;" ::"r"(nx_threads) : "memory");  // the target's classification
       predict_queue_warp(cx, sm, nx);
       asm volatile("bar.arrive 2, 64;" ::: "memory");
     }
@@ -987,6 +1004,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     if (lane == 0) log_task(cx.logs, R_CPU, K_CPU, (int)layer, e, cpu_t, cpu_t + dur, layer, it);
     cpu_t += dur;
   }
+  __syncwarp();  // every lane has read cpu_free
   if (lane == 0) { st->cpu_free = cpu_t; st->c.cpu_computed += n_cpu; }
   __syncwarp();
   mark(19);
@@ -1002,6 +1020,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     if (lane == 0) sm->out.load_slot[i] = (int8_t)(slot >= 0 ? slot : -1);
     ready[i] = pcie_t;
   }
+  __syncwarp();  // every lane has read pcie_free
   if (lane == 0) { st->pcie_free = pcie_t; st->c.demand += n_load; }
   __syncwarp();
   mark(20);
@@ -1026,6 +1045,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   if (route_end > completion) completion = route_end;
   if (cpu_t > completion) completion = cpu_t;
   if ((nres || n_load) && gpu_t > completion) completion = gpu_t;
+  __syncwarp();  // every lane has read gpu_free
   if (lane == 0) {
     st->gpu_free = gpu_t;
     const Logs* lg = cx.logs;
@@ -1110,6 +1130,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       ++n_pref;
       __syncwarp();
     }
+    __syncwarp();  // every lane has read pcie_free
     if (lane == 0) {
       if (t > st->pcie_free) st->pcie_free = t;
       st->q_valid = 1;

@@ -92,7 +92,9 @@ template <int NC, bool XREG>
 __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kSkMaxStages], empty_bar[kSkMaxStages];
-  __shared__ uint32_t s_hdr[kSkMaxStages][2];  // {item << 16 | 1, row} or {0, 0} = end
+  // stage header written by the producer lane before the stage's copy:
+  // {item << 16 | 1, row, combine weight} or {0, 0} = end, {0, 1} = snapshot
+  __shared__ uint32_t s_hdr[kSkMaxStages][3];
   __shared__ uint32_t s_pre[kMaxItems + 1];  // row prefix of a phase's items
   __shared__ uint32_t s_u[1024];             // the activation (bf16 pairs), d <= 2048
   // partial forward for the next layer's predictor (x_pred): the consumer
@@ -147,6 +149,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       const uint32_t st = acquire();
       s_hdr[st][0] = (ii << 16) | 1u;
       s_hdr[st][1] = r;
+      s_hdr[st][2] = __float_as_uint(it.wt[0]);  // consumers never read the plan (the producer rewrites it)
       unsigned char* dst = ring + st * SB;
       (void)F;
       // row-interleaved layout: [gate r | up r | down column r] contiguous
@@ -368,13 +371,13 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         }
         have_x = true;
       }
-      const Item& it = p->items[h0 >> 16];
+      const float wt = __uint_as_float(s_hdr[st][2]);
       const uint16_t* base = reinterpret_cast<const uint16_t*>(ring + st * SB);
       if (!(a.dbg & 1)) {
         float hv;
         if constexpr (XREG) hv = sk_h(base, base + d, xb, d);
         else hv = sk_h_smem(base, base + d, s_u, d);
-        const float s = it.wt[0] * hv;
+        const float s = wt * hv;
         const uint4* wd = reinterpret_cast<const uint4*>(base + 2 * d);
 #pragma unroll
         for (int j = 0; j < kSkMaxYChunks; ++j) {

@@ -361,7 +361,7 @@ struct EarlyPublish {
         A.tl[4] = globaltimer_ns();
         A.tl[15] = n;  // uploads published by this step
       }
-      sm->mail_a = 1;
+      atomicExch(const_cast<uint32_t*>(&sm->mail_a), 1u);  // warp 2 polls it (publish_spec)
 #ifdef MOEB_PROFILE_PHASES
       st->prof[13] += ptimer() - tf0;
 #endif
@@ -429,7 +429,7 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   __threadfence();
   if (uploads) {
     const uint64_t t0 = globaltimer_ns();
-    while (!sm->mail_a && globaltimer_ns() - t0 < kSpinLimitNs) {}
+    while (!atomicAdd(const_cast<uint32_t*>(&sm->mail_a), 0u) && globaltimer_ns() - t0 < kSpinLimitNs) {}
   }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
 }
