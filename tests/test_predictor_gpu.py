@@ -33,9 +33,11 @@ def _run(gpu, torch, L, E, k, B, d, F, S, slots, T, t_load, seed=7):
     return st, kw, xs
 
 
-@pytest.mark.parametrize("B,d,F,S", [(1, 256, 128, 256), (4, 256, 128, 256)])
-def test_predictor_decisions_and_arithmetic(gpu, B, d, F, S):
+@pytest.mark.parametrize("B,d,F,S,serial", [(1, 256, 128, 256, "0"), (4, 256, 128, 256, "0"),
+                                             (1, 256, 128, 256, "1")])
+def test_predictor_decisions_and_arithmetic(gpu, B, d, F, S, serial, monkeypatch):
     import torch
+    monkeypatch.setenv("MOEB_SERIAL", serial)  # serial: entry B of a step is published by the next one
     L, E, k, slots, T = 3, 16, 4, 4, 16
     st, kw, xs = _run(gpu, torch, L, E, k, B, d, F, S, slots, T, t_load=2)
     sc = st.scores().reshape(T, L, B, E).astype(np.float64)
