@@ -407,14 +407,9 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
     it.tok[0] = 0;
     it.wt[0] = wt;
   };
-  if (a.shared_w) item(a.shared_w, a.S, 0, 0, a.shared_gate ? sm->sg[0] : 1.0f);
-  if (a.shared_first && a.shared_w) {
-    // the shared expert (item 0) depends on nothing the decision computes:
-    // released on its own right away — in a layer without uploads (in one
-    // with uploads it would only compete for HBM with the decision)
-    __threadfence();
-    if (!uploads)
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 2), "r"((uint32_t)sm->seq) : "memory");
+  if (a.shared_w) {
+    if (a.shared_first) ++n;  // item 0 went out right after the gate (release_shared)
+    else item(a.shared_w, a.S, 0, 0, a.shared_gate ? sm->sg[0] : 1.0f);
   }
   uint64_t set = 0;
   for (uint64_t m = certain; m; m &= m - 1) {
@@ -435,8 +430,6 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   if (uploads) {
     const uint64_t t0 = globaltimer_ns();
     while (!atomicAdd(const_cast<uint32_t*>(&sm->mail_a), 0u) && globaltimer_ns() - t0 < kSpinLimitNs) {}
-    if (a.shared_first && a.shared_w)
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 2), "r"((uint32_t)sm->seq) : "memory");
   }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
 }
@@ -826,6 +819,21 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
       const uint32_t t = j - B;
       softmax_warp(a.trace + (((tit % a.trace_steps) * L + tl) * B + t) * E, E, sm->nsc[t]);
     }
+  }
+  // the shared expert depends on nothing the decision computes: released to
+  // the (already resident) FFN right after the gate, before classification
+  if (a.shared_first && threadIdx.x == 0) {
+    Item& it0 = a.spec_plan->items[0];
+    it0.w = a.shared_w;
+    it0.F = a.S;
+    it0.wait = 0;
+    it0.n_tok = 1;
+    it0.kind = 0;
+    it0.expert = 0;
+    it0.tok[0] = 0;
+    it0.wt[0] = a.shared_gate ? sm->sg[0] : 1.0f;
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 2), "r"((uint32_t)a.seq) : "memory");
   }
   const bool run_pending = a.predictor && sm->st.pf_pending && sm->st.pf_layer == layer && sm->st.pf_it == it;
   if (run_pending)  // the prediction for this layer: softmax of the router on the partial forward
