@@ -294,8 +294,12 @@ def c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, B, t
     m = st.metrics()
     io = st.io_stats()
     st.close()
-    mine = torch.tensor([ms, float(T * B), float(m["hits"]), float(m["selections"]), float(io["h2d_bytes"])],
-                        dtype=torch.float64)
+    pcie = measure_pcie_gbs(torch)  # this GPU's link, for the path roofline
+    # the uploads the decisions call for (speculative chunks excluded)
+    eb = 3 * MODEL["ffn"] * d * 2
+    up = float(io["h2d_bytes"] - io["spec_bytes"] + io["spec_promoted"] * eb)
+    mine = torch.tensor([ms, float(T * B), float(m["hits"]), float(m["selections"]), up,
+                         up / (pcie * 1e9) * 1e3], dtype=torch.float64)
     if world > 1:
         allv = [torch.zeros_like(mine) for _ in range(world)]
         dist.all_gather(allv, mine)
@@ -304,8 +308,10 @@ def c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, B, t
     allv = torch.stack(allv).numpy()
     t_max = float(allv[:, 0].max())
     toks = float(allv[:, 1].sum())
+    t_roof = float(allv[:, 5].max())  # the slowest link's upload time (PCIe-bound)
     return {"batch": B, "requests": n_requests, "tokens_per_request": tokens, "gpus": world,
             "groups_per_gpu": len(groups), "whole_job_ms": round(t_max, 2),
+            "path_roofline": {"t_roof_ms": round(t_roof, 2), "frac": round(t_roof / t_max, 4), "bound": "pcie"},
             "tokens_per_s": round(toks / (t_max * 1e-3), 1),
             "per_gpu_tokens_per_s": [round(float(r[1] / (r[0] * 1e-3)), 1) for r in allv],
             "hit_rate": round(float(allv[:, 2].sum() / max(allv[:, 3].sum(), 1)), 4),
