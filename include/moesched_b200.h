@@ -234,6 +234,25 @@ int moeb_set_logits_trace(moeb_stack* s, const float* logits, uint64_t n_steps,
  * x, y: device pointers, bf16 [B][d]; stream: cudaStream_t or NULL (the
  * stack's own stream). Asynchronous; the copy thread issues expert uploads. */
 int moeb_step(moeb_stack* s, const void* x, void* y, uint32_t B, void* stream);
+/* Prefill (prompt pass): n_tokens tokens of one sequence through all L
+ * layers (x, y: device pointers, bf16 [n_tokens][d]). Plain top-k routing
+ * (plain_top_k, router.cpp:252-260: no substitution — the paper's prefill is
+ * the traditional offloading path), every selected expert
+ * computed as a grouped tcgen05 GEMM after a warp-aggregated token -> expert
+ * permutation. Experts outside the capped cache are uploaded from the pinned
+ * pool into a staging area, layer l+1's while layer l computes; the decode
+ * state (cache, score windows, counters) is not changed. Needs the
+ * UMMA-tiled layout (a stack with max_batch 2..32, ffn and shared_ffn
+ * multiples of 128). Synchronises the stream once at entry (residency);
+ * h2d_bytes (nullable) = bytes uploaded. */
+int moeb_prefill(moeb_stack* s, const void* x, void* y, uint32_t n_tokens, void* stream,
+                 uint64_t* h2d_bytes);
+/* MOEB_MODEL_LOG_STEPS: the last prefill's layer `layer`: input hidden
+ * (bf16 [N][d]), router scores (fp32 [N][E]), selections in rank order
+ * (uint8 [N][k]) and fp32 layer output before the residual ([N][d]); every
+ * pointer nullable, n_tokens = N. */
+int moeb_get_prefill_log(moeb_stack* s, uint32_t layer, uint32_t* n_tokens, uint16_t* x_in,
+                         float* scores, uint8_t* sel, float* y);
 /* Synchronise the stack's streams. A device wait that gave up (a lost
  * upload, kSpinLimitNs) is reported here once as status 5 and cleared.
  * Serial mode (MOEB_SERIAL=1, automatic under ncu / nsys / compute-sanitizer):

@@ -340,6 +340,30 @@ class Stack:
     def sync(self):
         check(lib().moeb_sync(self.h))
 
+    def prefill(self, x_ptr, y_ptr, n_tokens, stream=0):
+        """Prompt pass of n_tokens tokens (moeb_prefill): bf16 [n_tokens, d] device
+        pointers; returns the bytes uploaded from the pinned pool."""
+        b = C.c_uint64(0)
+        check(lib().moeb_prefill(self.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr), C.c_uint32(n_tokens),
+                                 C.c_void_p(stream), C.byref(b)))
+        return b.value
+
+    def prefill_log(self, layer):
+        """The last prefill's layer `layer` (MOEB_MODEL_LOG_STEPS): input hidden (bf16 bits
+        [N, d]), router scores [N, E], selections [N, k] and the fp32 layer output [N, d]."""
+        n = C.c_uint32(0)
+        check(lib().moeb_get_prefill_log(self.h, C.c_uint32(layer), C.byref(n), None, None, None, None))
+        N, d, E, k = n.value, self.model.d_model, self.cfg.experts, self.cfg.top_k
+        x = np.zeros((N, d), dtype=np.uint16)
+        sc = np.zeros((N, E), dtype=np.float32)
+        sel = np.zeros((N, k), dtype=np.uint8)
+        y = np.zeros((N, d), dtype=np.float32)
+        check(lib().moeb_get_prefill_log(self.h, C.c_uint32(layer), C.byref(n), C.c_void_p(x.ctypes.data),
+                                         C.c_void_p(sc.ctypes.data), C.c_void_p(sel.ctypes.data),
+                                         C.c_void_p(y.ctypes.data)))
+        return x, sc, sel, y
+
+
     def metrics(self):
         m = Metrics()
         check(lib().moeb_get_metrics(self.h, C.byref(m)))

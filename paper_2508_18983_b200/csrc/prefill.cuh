@@ -1,0 +1,653 @@
+// prefill.cuh — the prompt (prefill) pass of the MoE stack: N tokens per
+// layer, every token routed by plain top-k (the paper's prefill uses the
+// traditional offloading path — PAPER.md:358-362 — no substitution: expert
+// activation is dense), experts computed as a grouped GEMM
+// on the 5th-generation tensor cores.
+//
+// Per layer, five launches on the stack's stream:
+//   pf_router_kernel   RMSNorm (the decode gate's arithmetic) + router logits
+//                      on mma.sync (32 tokens x 64 experts per CTA) + softmax +
+//                      top-k by counting (score desc, index asc: plain_top_k,
+//                      router.cpp:252-260) + combine weights
+//   pf_permute_kernel  token -> expert permutation: a warp-aggregated
+//                      histogram (__match_any_sync, one shared atomic per
+//                      distinct expert per warp), the expert segments (each
+//                      padded to 16 rows), and a warp-aggregated scatter of
+//                      (token, rank) entries into slot rows; builds the item /
+//                      unit tables of the GEMM (north_star item 4)
+//   pf_gather_kernel   activations of every slot row into the SW128 K-major
+//                      operand layout the MMA reads ([d/64][R][64] bf16)
+//   pf_gemm_kernel     grouped SwiGLU: persistent, one CTA per SM; units
+//                      gate_up (item, token tile <= 128, 128 intermediate rows)
+//                      and down (item, token tile, 128 output rows), grabbed
+//                      from one grid counter; tcgen05.mma M = 128, N = token
+//                      tile, fp32 accumulators in TMEM (two buffers of 256
+//                      columns), operands staged by cp.async.bulk (weights are
+//                      UMMA-tiled, weights.cuh); h = silu(g) * up kept as bf16
+//                      hi + lo (h = hi + lo to 2^-17), both accumulated by the
+//                      down MMA; the down epilogue writes w_slot * y per slot row
+//   pf_combine_kernel  per token: shared expert row + its k slot rows in rank
+//                      order, residual, bf16 hidden for the next layer
+//
+// Token slot positions inside an expert segment come from shared-memory
+// atomics (not deterministic), but every GEMM column is an independent
+// dot product and the combine sums a token's slots in rank order, so the
+// hidden output is bitwise reproducible.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ffn_umma.cuh"
+
+namespace moeb {
+
+constexpr uint32_t kPfStageBytes = 3 * kUmBlk;  // gate_up: gate + up + x tile; down: down + hi + lo tiles
+constexpr uint32_t kPfStages = 4;
+constexpr uint32_t kPfThreads = 6 * 32;
+constexpr uint32_t kPfTmemCols = 512;           // two buffers x (gate 128 | up 128) columns
+constexpr uint32_t kPfNt = 128;                 // token rows per unit (max MMA N of one accumulator pair)
+constexpr uint32_t kPfRouterTok = 32;           // tokens per router CTA
+constexpr uint32_t kPfMaxK = 16;
+
+struct PfItem {
+  const unsigned char* w;  // expert weights, UMMA-tiled (weights.cuh)
+  uint32_t F;              // intermediate rows (multiple of 128)
+  uint32_t row0;           // first slot row (multiple of 16)
+  uint32_t n;              // tokens
+  uint32_t ntile;          // token tiles (of kPfNt)
+  uint32_t tile0;          // first token tile (global index: arrival counters)
+  uint32_t gu0, dn0;       // first gate_up / down unit
+  uint32_t expert;         // routed expert id, or 0xFFFF for the shared expert
+};
+struct PfHdr {
+  uint32_t n_items, n_gu, n_dn, rows, tiles;
+};
+
+// ------------------------------------------------------------ router
+struct PfRouterArgs {
+  const uint16_t* x;    // [N][d] bf16 layer input
+  const uint16_t* wg;   // [E][d] router weights
+  const uint16_t* wsg;  // [d] shared-expert gate row (Qwen) or null
+  uint16_t* u;          // [N][d] normalised input (bf16)
+  float* scores;        // [N][E] fp32 softmax scores
+  uint8_t* sel;         // [N][k] selected experts in rank order
+  float* wts;           // [N][k] combine weights
+  float* sgate;         // [N] sigmoid of the shared-gate logit (1 when none)
+  uint32_t N, d, E, k;
+  int32_t renormalize;
+  float routed_scale;
+};
+
+// 256 threads, dynamic smem: [32][d + 8] bf16 (u) + [32][E] fp32 (logits)
+__global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ PfRouterArgs a) {
+  extern __shared__ __align__(16) unsigned char pf_rsm[];
+  const uint32_t d = a.d, E = a.E, k = a.k, ld = d + 8;
+  uint16_t* us = reinterpret_cast<uint16_t*>(pf_rsm);
+  float* lg = reinterpret_cast<float*>(pf_rsm + (size_t)kPfRouterTok * ld * 2);
+  __shared__ float inv_rms[kPfRouterTok];
+  const int lane = lane_id(), warp = warp_id();
+  const uint32_t t0 = blockIdx.x * kPfRouterTok;
+  const uint32_t nt = min(kPfRouterTok, a.N - t0), nvec = d / 8;
+  // x -> smem (rows >= nt zero)
+  for (uint32_t i = threadIdx.x; i < kPfRouterTok * nvec; i += blockDim.x) {
+    const uint32_t t = i / nvec, c = i % nvec;
+    const uint4 v = t < nt ? reinterpret_cast<const uint4*>(a.x + (size_t)(t0 + t) * d)[c] : make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(us + (size_t)t * ld + c * 8) = v;
+  }
+  __syncthreads();
+  // RMSNorm (eps 1e-6, unit weight), the decode gate's arithmetic (layer.cuh gate_phase)
+  for (uint32_t t = warp; t < kPfRouterTok; t += 8) {
+    float ss = 0.f;
+    for (uint32_t c = lane; c < nvec; c += 32) {
+      const uint4 v = *reinterpret_cast<const uint4*>(us + (size_t)t * ld + c * 8);
+      ss += dot8(v, v);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) inv_rms[t] = __frsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), 1e-6f));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kPfRouterTok * nvec; i += blockDim.x) {
+    const uint32_t t = i / nvec, c = i % nvec;
+    uint4* p = reinterpret_cast<uint4*>(us + (size_t)t * ld + c * 8);
+    const uint4 v = *p;
+    const float r = inv_rms[t];
+    const uint32_t in[4] = {v.x, v.y, v.z, v.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float lo = __fmul_rn(__uint_as_float(in[j] << 16), r);
+      const float hi = __fmul_rn(__uint_as_float(in[j] & 0xffff0000u), r);
+      o[j] = (uint32_t)f32_to_bf16_rne(lo) | ((uint32_t)f32_to_bf16_rne(hi) << 16);
+    }
+    const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+    *p = ov;
+    if (t < nt) reinterpret_cast<uint4*>(a.u + (size_t)(t0 + t) * d)[c] = ov;
+  }
+  __syncthreads();
+  // logits = u . Wg^T on mma.sync m16n8k16: warp w -> token rows 16 (w & 1),
+  // experts 16 (w >> 1) .. +15 (two n8 tiles); fp32 accumulation
+  {
+    const uint32_t m0 = 16 * (warp & 1), e0 = 16 * (warp >> 1);
+    if (e0 < E) {
+      float acc[2][4] = {};
+      const uint32_t a_addr = smem_u32(us + (size_t)(m0 + (lane & 15)) * ld + (lane >> 4) * 8);
+      const uint32_t* w0 = nullptr;
+      const uint32_t* w1 = nullptr;
+      const uint32_t ea = e0 + (lane >> 2), eb = e0 + 8 + (lane >> 2);
+      if (ea < E) w0 = reinterpret_cast<const uint32_t*>(a.wg + (size_t)ea * d) + (lane & 3);
+      if (eb < E) w1 = reinterpret_cast<const uint32_t*>(a.wg + (size_t)eb * d) + (lane & 3);
+      for (uint32_t k0 = 0; k0 < d; k0 += 64) {
+        uint32_t b[4][2][2];
+#pragma unroll
+        for (uint32_t s = 0; s < 4; ++s) {
+          const uint32_t kw = (k0 + s * 16) / 2;
+          b[s][0][0] = w0 ? __ldg(w0 + kw) : 0u;
+          b[s][0][1] = w0 ? __ldg(w0 + kw + 4) : 0u;
+          b[s][1][0] = w1 ? __ldg(w1 + kw) : 0u;
+          b[s][1][1] = w1 ? __ldg(w1 + kw + 4) : 0u;
+        }
+#pragma unroll
+        for (uint32_t s = 0; s < 4; ++s) {
+          uint32_t af[4];
+          ldsm_x4(a_addr + (k0 + s * 16) * 2, af);
+          mma16816(acc[0], af, b[s][0][0], b[s][0][1]);
+          mma16816(acc[1], af, b[s][1][0], b[s][1][1]);
+        }
+      }
+#pragma unroll
+      for (uint32_t j = 0; j < 2; ++j) {
+        const uint32_t r = m0 + (lane >> 2), e = e0 + 8 * j + 2 * (lane & 3);
+        if (e < E) {
+          lg[r * E + e] = acc[j][0];
+          lg[(r + 8) * E + e] = acc[j][2];
+        }
+        if (e + 1 < E) {
+          lg[r * E + e + 1] = acc[j][1];
+          lg[(r + 8) * E + e + 1] = acc[j][3];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // per token (warp): softmax, top-k by counting, combine weights, shared gate
+  for (uint32_t t = warp; t < nt; t += 8) {
+    float sc[2];
+    {
+      const float l0 = (uint32_t)lane < E ? lg[t * E + lane] : -INFINITY;
+      const float l1 = (uint32_t)lane + 32 < E ? lg[t * E + lane + 32] : -INFINITY;
+      float m = fmaxf(l0, l1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      const float x0 = (uint32_t)lane < E ? expf(l0 - m) : 0.f;
+      const float x1 = (uint32_t)lane + 32 < E ? expf(l1 - m) : 0.f;
+      float s = x0 + x1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      sc[0] = __fdiv_rn(x0, s);
+      sc[1] = __fdiv_rn(x1, s);
+    }
+    const size_t tg = t0 + t;
+    if ((uint32_t)lane < E) a.scores[tg * E + lane] = sc[0];
+    if ((uint32_t)lane + 32 < E) a.scores[tg * E + lane + 32] = sc[1];
+    // rank of expert e: #{j : s_j > s_e or (s_j == s_e and j < e)}
+    uint32_t rk[2] = {0u, 0u};
+    for (uint32_t j = 0; j < E; ++j) {
+      const float sj = __shfl_sync(0xffffffffu, sc[j >> 5], j & 31);
+#pragma unroll
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t e = lane + 32 * h;
+        rk[h] += (sj > sc[h] || (sj == sc[h] && j < e)) ? 1u : 0u;
+      }
+    }
+    // denominator (renormalisation): selected scores summed in rank order
+    float den = 1.f;
+    if (a.renormalize) {
+      den = 0.f;
+      for (uint32_t r = 0; r < k; ++r) {
+        const uint32_t hit = __ballot_sync(0xffffffffu, (lane < (int)E && rk[0] == r) || (lane + 32 < (int)E && rk[1] == r));
+        const int src = __ffs(hit) - 1;
+        const float v = __shfl_sync(0xffffffffu, rk[0] == r && lane < (int)E ? sc[0] : sc[1], src);
+        den += v;
+      }
+    }
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+      const uint32_t e = lane + 32 * h;
+      if (e < E && rk[h] < k) {
+        a.sel[tg * k + rk[h]] = (uint8_t)e;
+        float w = sc[h];
+        if (a.renormalize) w = __fdiv_rn(w, den);
+        a.wts[tg * k + rk[h]] = __fmul_rn(w, a.routed_scale);
+      }
+    }
+    if (a.sgate) {
+      float z = 1.f;
+      if (a.wsg) {
+        float s = 0.f;
+        const uint4* wv = reinterpret_cast<const uint4*>(a.wsg);
+        for (uint32_t c = lane; c < nvec; c += 32)
+          s += dot8(__ldg(wv + c), *reinterpret_cast<const uint4*>(us + (size_t)t * ld + c * 8));
+        s = warp_sum(s);
+        z = 1.f / (1.f + expf(-s));
+      }
+      if (lane == 0) a.sgate[tg] = z;
+    }
+  }
+}
+
+// ------------------------------------------------------------ permutation
+struct PfPermuteArgs {
+  const uint8_t* sel;    // [N][k]
+  const float* wts;      // [N][k]
+  const float* sgate;    // [N] (shared expert weight)
+  const LayerState* ls;  // this layer's cache state (residency, slots)
+  const unsigned char* slot_base;   // this layer's cache slots
+  const unsigned char* stage_base;  // staging of the non-resident experts (by expert id)
+  const unsigned char* shared_w;    // shared expert (null: none)
+  uint64_t expert_bytes;
+  uint32_t N, k, E, d, F, S;
+  PfItem* items;
+  PfHdr* hdr;
+  int32_t* slot_tok;     // [R] token of each slot row (-1: padding)
+  float* slot_w;         // [R] combine weight of each slot row
+  int32_t* entry_slot;   // [N][k] slot row of each (token, rank)
+  uint32_t R;            // slot rows allocated
+};
+
+__global__ void __launch_bounds__(1024) pf_permute_kernel(const __grid_constant__ PfPermuteArgs a) {
+  __shared__ uint32_t cnt[kMaxE], base[kMaxE];
+  __shared__ uint32_t s_rows;
+  const int lane = lane_id();
+  const uint32_t n = a.N * a.k;
+  for (uint32_t e = threadIdx.x; e < kMaxE; e += blockDim.x) cnt[e] = 0;
+  __syncthreads();
+  // histogram: one shared atomic per distinct expert per warp
+  for (uint32_t i0 = threadIdx.x - lane; i0 < n; i0 += blockDim.x) {
+    const uint32_t i = i0 + lane;
+    const bool live = i < n;
+    const uint32_t e = live ? a.sel[i] : 0xFFu;
+    const uint32_t act = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const uint32_t peers = __match_any_sync(act, e);
+      if (lane == __ffs(peers) - 1) atomicAdd(&cnt[e], __popc(peers));
+    }
+  }
+  __syncthreads();
+  // segments and the item / unit tables (warp 0, lane-parallel scan)
+  if (threadIdx.x < 32) {
+    const uint32_t nmt = a.d / 128;
+    uint32_t rows = 0, tiles = 0, gu = 0, n_items = 0;
+    if (a.S) {
+      PfItem it{};
+      it.w = a.shared_w;
+      it.F = a.S;
+      it.row0 = 0;
+      it.n = a.N;
+      it.ntile = (a.N + kPfNt - 1) / kPfNt;
+      it.tile0 = 0;
+      it.gu0 = 0;
+      it.expert = 0xFFFFu;
+      if (lane == 0) a.items[0] = it;
+      rows = (a.N + 15) & ~15u;
+      tiles = it.ntile;
+      gu = it.ntile * (a.S / 128);
+      n_items = 1;
+    }
+    const uint64_t mask = a.ls->mask;
+    for (uint32_t e0 = 0; e0 < a.E; e0 += 32) {
+      const uint32_t e = e0 + lane;
+      const uint32_t c = e < a.E ? cnt[e] : 0u;
+      const uint32_t pr = (c + 15) & ~15u, nt = (c + kPfNt - 1) / kPfNt;
+      // exclusive prefix sums over the lanes (experts in ascending order)
+      uint32_t sr = pr, st = nt, sg = nt * (a.F / 128), si = c ? 1u : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t vr = __shfl_up_sync(0xffffffffu, sr, o), vt = __shfl_up_sync(0xffffffffu, st, o);
+        const uint32_t vg = __shfl_up_sync(0xffffffffu, sg, o), vi = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) { sr += vr; st += vt; sg += vg; si += vi; }
+      }
+      if (c) {
+        PfItem it{};
+        const bool res = (mask >> e) & 1ull;
+        it.w = res ? a.slot_base + (uint64_t)a.ls->slot_of[e] * a.expert_bytes : a.stage_base + (uint64_t)e * a.expert_bytes;
+        it.F = a.F;
+        it.row0 = rows + sr - pr;
+        it.n = c;
+        it.ntile = nt;
+        it.tile0 = tiles + st - nt;
+        it.gu0 = gu + sg - nt * (a.F / 128);
+        it.expert = e;
+        a.items[n_items + si - 1] = it;
+      }
+      if (e < a.E) base[e] = rows + sr - pr;
+      rows += __shfl_sync(0xffffffffu, sr, 31);
+      tiles += __shfl_sync(0xffffffffu, st, 31);
+      gu += __shfl_sync(0xffffffffu, sg, 31);
+      n_items += __shfl_sync(0xffffffffu, si, 31);
+    }
+    __syncwarp();
+    // down units after every gate_up unit, in item order
+    uint32_t dn = gu;
+    for (uint32_t i0 = 0; i0 < n_items; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t v = i < n_items ? a.items[i].ntile * nmt : 0u;
+      uint32_t s = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+      }
+      if (i < n_items) a.items[i].dn0 = dn + s - v;
+      dn += __shfl_sync(0xffffffffu, s, 31);
+    }
+    if (lane == 0) {
+      *a.hdr = PfHdr{n_items, gu, dn - gu, rows, tiles};
+      s_rows = rows;
+    }
+  }
+  __syncthreads();
+  const uint32_t rows = s_rows;
+  // padding rows -1, shared rows = the tokens in order
+  for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
+    const bool sh = a.S && r < a.N;
+    a.slot_tok[r] = sh ? (int32_t)r : -1;
+    a.slot_w[r] = sh ? a.sgate[r] : 0.f;
+  }
+  __syncthreads();
+  // scatter: a warp's entries of one expert take consecutive slots (one atomic)
+  for (uint32_t i0 = threadIdx.x - lane; i0 < n; i0 += blockDim.x) {
+    const uint32_t i = i0 + lane;
+    const bool live = i < n;
+    const uint32_t e = live ? a.sel[i] : 0xFFu;
+    const uint32_t act = __ballot_sync(0xffffffffu, live);
+    if (live) {
+      const uint32_t peers = __match_any_sync(act, e);
+      const int leader = __ffs(peers) - 1;
+      uint32_t b = 0;
+      if (lane == leader) b = atomicAdd(&base[e], __popc(peers));
+      b = __shfl_sync(peers, b, leader);
+      const uint32_t slot = b + __popc(peers & ((1u << lane) - 1u));
+      a.slot_tok[slot] = (int32_t)(i / a.k);
+      a.slot_w[slot] = a.wts[i];
+      a.entry_slot[i] = (int32_t)slot;
+    }
+  }
+}
+
+// ------------------------------------------------------------ gather
+// slot row r <- u[slot_tok[r]] (zero for padding), SW128: 16 B chunk c of
+// row r in K-block c / 8 at chunk position (c ^ r) % 8. One warp per row.
+__global__ void __launch_bounds__(256) pf_gather_kernel(const uint16_t* __restrict__ u, const int32_t* __restrict__ slot_tok,
+                                                        const PfHdr* __restrict__ hdr, unsigned char* __restrict__ xg,
+                                                        uint32_t d, uint32_t R) {
+  const uint32_t rows = hdr->rows, nvec = d / 8;
+  const int lane = lane_id();
+  for (uint32_t r = blockIdx.x * 8 + warp_id(); r < rows; r += gridDim.x * 8) {
+    const int32_t t = slot_tok[r];
+    const uint4* src = reinterpret_cast<const uint4*>(u + (size_t)(t < 0 ? 0 : t) * d);
+    for (uint32_t c = lane; c < nvec; c += 32) {
+      const uint4 v = t >= 0 ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
+      const size_t off = (size_t)(c >> 3) * R * 128u + (r >> 3) * 1024u + (r & 7u) * 128u + (((c ^ r) & 7u) << 4);
+      *reinterpret_cast<uint4*>(xg + off) = v;
+    }
+  }
+}
+
+// ------------------------------------------------------------ grouped GEMM
+struct PfGemmArgs {
+  const PfItem* items;
+  const PfHdr* hdr;
+  const unsigned char* xg;  // [d/64][R][128 B] activations (SW128)
+  unsigned char* hg;        // [Fmax/64][2][R][128 B] h hi / lo (SW128)
+  float* out;               // [R][d] w_slot * expert output
+  const float* slot_w;      // [R]
+  uint32_t* ctr;            // [0] unit grab, [1] CTAs done, [2 + tile] gate_up arrivals
+  uint32_t d, R;
+};
+
+struct PfRec {
+  uint32_t kind;  // 0 gate_up, 1 down, 2 end
+  uint32_t item, tile, idx, nt, nrows;
+};
+
+__global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_constant__ PfGemmArgs a) {
+  extern __shared__ unsigned char pf_smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kPfStages], empty_bar[kPfStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t rfull_bar[kUmRec], rempty_bar[kUmRec];
+  __shared__ PfRec recs[kUmRec];
+  __shared__ PfItem s_items[kMaxItems];
+  __shared__ uint32_t s_tmem;
+  const int warp = warp_id(), lane = lane_id();
+  const uint32_t d = a.d, R = a.R, nkb = d / 64, nmt = d / 128;
+  const uint32_t raw_addr = smem_u32(pf_smem_raw);
+  unsigned char* ring = pf_smem_raw + (((raw_addr + 1023u) & ~1023u) - raw_addr);
+  const uint32_t ring_addr = smem_u32(ring);
+  const PfHdr hdr = *a.hdr;
+  for (uint32_t i = threadIdx.x; i < hdr.n_items; i += blockDim.x) s_items[i] = a.items[i];
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < kPfStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    for (uint32_t j = 0; j < kUmRec; ++j) {
+      mbar_init(&rfull_bar[j], 1);
+      mbar_init(&rempty_bar[j], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "n"(kPfTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    um_fence_before();
+  }
+  __syncthreads();
+  um_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ producer
+      const uint64_t pol_w = l2_evict_first_policy(), pol_x = l2_evict_last_policy();
+      const uint32_t total = hdr.n_gu + hdr.n_dn;
+      uint32_t k = 0, u = 0;
+      for (uint32_t unit = atomicAdd(&a.ctr[0], 1u); unit < total; unit = atomicAdd(&a.ctr[0], 1u)) {
+        PfRec r{};
+        const bool gu = unit < hdr.n_gu;
+        uint32_t i = 0;
+        // the item holding the unit (items are in unit order)
+        for (uint32_t j = 1; j < hdr.n_items; ++j)
+          if ((gu ? s_items[j].gu0 : s_items[j].dn0) <= unit) i = j;
+        const PfItem& it = s_items[i];
+        const uint32_t q = unit - (gu ? it.gu0 : it.dn0), per = gu ? it.F / 128 : nmt;
+        r.kind = gu ? 0u : 1u;
+        r.item = i;
+        r.tile = q / per;
+        r.idx = q % per;
+        r.nrows = min(kPfNt, it.n - r.tile * kPfNt);
+        r.nt = (r.nrows + 15) & ~15u;
+        {
+          const uint32_t j = u % kUmRec;
+          mbar_wait(&rempty_bar[j], ((u / kUmRec) & 1) ^ 1);
+          recs[j] = r;
+          mbar_arrive(&rfull_bar[j]);
+          ++u;
+        }
+        const size_t row = (size_t)it.row0 + r.tile * kPfNt;
+        const uint32_t xb = r.nt * 128;
+        if (gu) {
+          const unsigned char* wsrc = it.w + ((size_t)r.idx * nkb) * kUmA;
+          for (uint32_t kb = 0; kb < nkb; ++kb, ++k) {
+            const uint32_t st = k % kPfStages;
+            mbar_wait(&empty_bar[st], ((k / kPfStages) & 1) ^ 1);
+            mbar_expect_tx(&full_bar[st], kUmA + xb);
+            bulk_g2s(ring + st * kPfStageBytes, wsrc + (size_t)kb * kUmA, kUmA, &full_bar[st], pol_w);
+            bulk_g2s(ring + st * kPfStageBytes + kUmA, a.xg + ((size_t)kb * R + row) * 128, xb, &full_bar[st], pol_x);
+          }
+        } else {
+          // h of this (item, token tile): every gate_up unit must have landed
+          wait_ctr_ge(&a.ctr[2 + it.tile0 + r.tile], it.F / 128, 10u);
+          fence_proxy_async_global();
+          const uint32_t nfb = it.F / 64;
+          const unsigned char* wsrc = it.w + (size_t)2 * it.F * d * 2 + (size_t)r.idx * nfb * kUmBlk;
+          for (uint32_t kb = 0; kb < nfb; ++kb, ++k) {
+            const uint32_t st = k % kPfStages;
+            mbar_wait(&empty_bar[st], ((k / kPfStages) & 1) ^ 1);
+            mbar_expect_tx(&full_bar[st], kUmBlk + 2 * xb);
+            unsigned char* dst = ring + st * kPfStageBytes;
+            bulk_g2s(dst, wsrc + (size_t)kb * kUmBlk, kUmBlk, &full_bar[st], pol_w);
+            bulk_g2s(dst + kUmBlk, a.hg + ((size_t)(2 * kb) * R + row) * 128, xb, &full_bar[st], pol_x);
+            bulk_g2s(dst + kUmBlk + xb, a.hg + ((size_t)(2 * kb + 1) * R + row) * 128, xb, &full_bar[st], pol_x);
+          }
+        }
+      }
+      const uint32_t j = u % kUmRec;
+      mbar_wait(&rempty_bar[j], ((u / kUmRec) & 1) ^ 1);
+      recs[j] = PfRec{2u, 0u, 0u, 0u, 0u, 0u};
+      mbar_arrive(&rfull_bar[j]);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- MMA issuer
+      uint32_t k = 0;
+      for (uint32_t u = 0;; ++u) {
+        const uint32_t j = u % kUmRec;
+        mbar_wait(&rfull_bar[j], (u / kUmRec) & 1);
+        const PfRec r = recs[j];
+        if (r.kind == 2) break;
+        const uint32_t b = u & 1;
+        mbar_wait(&tempty_bar[b], ((u >> 1) & 1) ^ 1);
+        um_fence_after();
+        const uint32_t acc = tmem + b * 256, idesc = um_idesc(r.nt), xb = r.nt * 128;
+        const uint32_t n_st = r.kind == 0 ? nkb : s_items[r.item].F / 64;
+        for (uint32_t s = 0; s < n_st; ++s, ++k) {
+          const uint32_t st = k % kPfStages;
+          mbar_wait(&full_bar[st], (k / kPfStages) & 1);
+          um_fence_after();
+          const uint32_t sa = ring_addr + st * kPfStageBytes;
+          if (r.kind == 0) {
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk) {
+              const uint64_t bx = um_desc(sa + kUmA + kk * 32);
+              um_mma(acc, um_desc(sa + kk * 32), bx, idesc, (s | kk) != 0);
+              um_mma(acc + 128, um_desc(sa + kUmBlk + kk * 32), bx, idesc, (s | kk) != 0);
+            }
+          } else {
+#pragma unroll
+            for (uint32_t kk = 0; kk < 4; ++kk) {
+              const uint64_t aw = um_desc(sa + kk * 32);
+              um_mma(acc, aw, um_desc(sa + kUmBlk + kk * 32), idesc, (s | kk) != 0);
+              um_mma(acc, aw, um_desc(sa + kUmBlk + xb + kk * 32), idesc, 1u);
+            }
+          }
+          um_commit(&empty_bar[st]);
+        }
+        um_commit(&tfull_bar[b]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------- epilogue
+    const uint32_t q = warp & 3, et = (warp - 2) * 32 + lane;
+    for (uint32_t u = 0;; ++u) {
+      const uint32_t j = u % kUmRec;
+      mbar_wait(&rfull_bar[j], (u / kUmRec) & 1);
+      const PfRec r = recs[j];
+      if (r.kind == 2) break;
+      const PfItem& it = s_items[r.item];
+      const uint32_t b = u & 1;
+      mbar_wait(&tfull_bar[b], (u >> 1) & 1);
+      um_fence_after();
+      const uint32_t ta = tmem + ((q * 32) << 16) + b * 256;
+      const uint32_t row0 = it.row0 + r.tile * kPfNt;
+      if (r.kind == 0) {
+        // intermediate row f of the item -> h K-block f / 64, column f % 64
+        const uint32_t f = r.idx * 128 + q * 32 + lane;
+        unsigned char* hhi = a.hg + (size_t)(2 * (f >> 6)) * R * 128;
+        unsigned char* hlo = hhi + (size_t)R * 128;
+        const uint32_t col = f & 63;
+        for (uint32_t c0 = 0; c0 < r.nt; c0 += 16) {
+          float g[16], up[16];
+          um_ld16(ta + c0, g);
+          um_ld16(ta + 128 + c0, up);
+          um_ld_wait();
+#pragma unroll
+          for (uint32_t i = 0; i < 16; ++i) {
+            const uint32_t c = c0 + i, rr = row0 + c;
+            const float h = c < r.nrows ? (g[i] / (1.f + __expf(-g[i]))) * up[i] : 0.f;
+            const uint16_t hi = f32_to_bf16_rne(h);
+            const uint16_t lo = f32_to_bf16_rne(h - bf2f(hi));
+            *reinterpret_cast<uint16_t*>(hhi + sw128_off(rr, col)) = hi;
+            *reinterpret_cast<uint16_t*>(hlo + sw128_off(rr, col)) = lo;
+          }
+        }
+        um_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[b]);
+        fence_proxy_async_global();  // h is read by the down units' bulk copies
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (et == 0) {
+          __threadfence();
+          atomicAdd(&a.ctr[2 + it.tile0 + r.tile], 1u);
+          mbar_arrive(&rempty_bar[j]);
+        }
+      } else {
+        const uint32_t m = r.idx * 128 + q * 32 + lane;
+        for (uint32_t c0 = 0; c0 < r.nt; c0 += 16) {
+          float v[16];
+          um_ld16(ta + c0, v);
+          um_ld_wait();
+#pragma unroll
+          for (uint32_t i = 0; i < 16; ++i) {
+            const uint32_t c = c0 + i;
+            if (c < r.nrows) __stcg(a.out + (size_t)(row0 + c) * d + m, v[i] * __ldg(a.slot_w + row0 + c));
+          }
+        }
+        um_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[b]);
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (et == 0) mbar_arrive(&rempty_bar[j]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kPfTmemCols));
+}
+
+// ------------------------------------------------------------ combine
+// hidden[t] = bf16(x[t] + shared row t + the token's k slot rows in rank order);
+// y (nullable) keeps the fp32 layer output. One thread per 4 outputs.
+__global__ void __launch_bounds__(256) pf_combine_kernel(const uint16_t* __restrict__ x, const float* __restrict__ out,
+                                                         const int32_t* __restrict__ entry_slot, uint16_t* __restrict__ xo,
+                                                         float* __restrict__ y, uint32_t N, uint32_t d, uint32_t k,
+                                                         uint32_t shared) {
+  const uint32_t per = d / 4;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N * per; i += gridDim.x * blockDim.x) {
+    const uint32_t t = i / per, c = (i % per) * 4;
+    float4 s = shared ? __ldcg(reinterpret_cast<const float4*>(out + (size_t)t * d + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t j = 0; j < k; ++j) {
+      const int32_t sl = __ldg(entry_slot + (size_t)t * k + j);
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(out + (size_t)sl * d + c));
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+    const uint2 xv = *reinterpret_cast<const uint2*>(x + (size_t)t * d + c);
+    const float o0 = __uint_as_float(xv.x << 16) + s.x, o1 = __uint_as_float(xv.x & 0xffff0000u) + s.y;
+    const float o2 = __uint_as_float(xv.y << 16) + s.z, o3 = __uint_as_float(xv.y & 0xffff0000u) + s.w;
+    uint2 ov;
+    ov.x = (uint32_t)f32_to_bf16_rne(o0) | ((uint32_t)f32_to_bf16_rne(o1) << 16);
+    ov.y = (uint32_t)f32_to_bf16_rne(o2) | ((uint32_t)f32_to_bf16_rne(o3) << 16);
+    *reinterpret_cast<uint2*>(xo + (size_t)t * d + c) = ov;
+    if (y) *reinterpret_cast<float4*>(y + (size_t)t * d + c) = s;
+  }
+}
+
+}  // namespace moeb

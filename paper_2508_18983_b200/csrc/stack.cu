@@ -36,6 +36,7 @@
 #include "ffn_tma.cuh"
 #include "ffn_splitk.cuh"
 #include "ffn_umma.cuh"
+#include "prefill.cuh"
 #include "weights.cuh"
 
 namespace moeb {
@@ -1083,6 +1084,26 @@ struct moeb_stack {
   // with MOEB_SERIAL=1 or automatically under ncu / nsys / compute-sanitizer,
   // which serialise kernels (and the copy thread's API calls) behind the one
   // being measured, so an FFN spinning on copies_done could never see them.
+  // Prefill (moeb_prefill): buffers sized for pf_cap tokens; staging for the
+  // non-resident experts of two layers (the layer being computed and the next
+  // one, uploading); a copy stream and its events.
+  uint32_t pf_cap = 0, pf_R = 0, pf_tiles = 0;
+  DevBuf<uint16_t> pf_u, pf_hid, pf_stage;
+  DevBuf<float> pf_scores, pf_wts, pf_sgate, pf_slot_w, pf_out;
+  DevBuf<uint8_t> pf_sel;
+  DevBuf<int32_t> pf_slot_tok, pf_entry;
+  DevBuf<PfItem> pf_items;
+  DevBuf<PfHdr> pf_hdr;
+  DevBuf<uint32_t> pf_ctr;
+  DevBuf<unsigned char> pf_xg, pf_hg;
+  cudaStream_t pf_copy = nullptr;
+  cudaEvent_t pf_up[2] = {}, pf_free[2] = {};
+  // MOEB_MODEL_LOG_STEPS: the last prefill's per-layer inputs, scores,
+  // selections and fp32 outputs (moeb_get_prefill_log)
+  uint32_t pf_log_n = 0, pf_last_n = 0;
+  DevBuf<uint16_t> pf_log_x;
+  DevBuf<float> pf_log_scores, pf_log_y;
+  DevBuf<uint8_t> pf_log_sel;
   bool serial = false;
   uint32_t serial_need = 0;  // highest upload id the next FFN may depend on
   uint64_t n_launch_layers = 0;        // (gate+decide, FFN) launch pairs
@@ -1314,6 +1335,12 @@ struct moeb_stack {
       if (ev_a[i]) cudaEventDestroy(ev_a[i]);
       if (ev_b[i]) cudaEventDestroy(ev_b[i]);
     }
+    if (pf_copy) cudaStreamSynchronize(pf_copy);
+    for (int i = 0; i < 2; ++i) {
+      if (pf_up[i]) cudaEventDestroy(pf_up[i]);
+      if (pf_free[i]) cudaEventDestroy(pf_free[i]);
+    }
+    if (pf_copy) cudaStreamDestroy(pf_copy);
     if (ev_spec) cudaEventDestroy(ev_spec);
     if (ev_dem) cudaEventDestroy(ev_dem);
     if (stream) cudaStreamDestroy(stream);
@@ -1872,6 +1899,184 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
   S->io.steps += 1;
 }
 
+// ---------------------------------------------------------------- prefill
+// N prompt tokens through all L layers (prefill.cuh). Plain top-k routing
+// (no substitution, no cache admission: the decode state is untouched —
+// PAPER.md:358-362), every selected expert computed on the tensor cores.
+// Experts not resident in the capped cache are uploaded into a per-layer
+// staging area from the pinned pool, layer l+1's while layer l computes (the
+// paper's prefill pipeline); all of them, since prefill activation is dense
+// (PAPER.md:770-774).
+static void prefill_alloc(moeb_stack* S, uint32_t N) {
+  const uint32_t E = S->E, k = S->cfg.top_k, d = S->d, Fmax = std::max(S->F, S->S);
+  const cudaStream_t s = S->stream;
+  if (N > S->pf_cap) {
+    const uint32_t R = ((N + 15) & ~15u) + N * k + 16 * E;
+    const uint32_t tiles = (N + kPfNt - 1) / kPfNt + (N * k + kPfNt - 1) / kPfNt + E;
+    S->pf_u.alloc((size_t)N * d);
+    S->pf_hid.alloc((size_t)2 * N * d);
+    S->pf_scores.alloc((size_t)N * E);
+    S->pf_wts.alloc((size_t)N * k);
+    S->pf_sel.alloc((size_t)N * k);
+    S->pf_sgate.alloc(N);
+    S->pf_entry.alloc((size_t)N * k);
+    S->pf_slot_tok.alloc(R);
+    S->pf_slot_w.alloc(R);
+    S->pf_out.alloc((size_t)R * d);
+    S->pf_xg.alloc((size_t)R * d * 2);
+    S->pf_hg.alloc((size_t)R * Fmax * 4);
+    S->pf_hg.zero(s);
+    S->pf_ctr.alloc(2 + tiles);
+    S->pf_items.alloc(kMaxItems);
+    S->pf_hdr.alloc(1);
+    S->pf_cap = N;
+    S->pf_R = R;
+    S->pf_tiles = tiles;
+  }
+  if (!S->pf_copy) {
+    MOEB_CUDA(cudaStreamCreateWithFlags(&S->pf_copy, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      MOEB_CUDA(cudaEventCreateWithFlags(&S->pf_up[i], cudaEventDisableTiming));
+      MOEB_CUDA(cudaEventCreateWithFlags(&S->pf_free[i], cudaEventDisableTiming));
+    }
+    MOEB_CUDA(cudaFuncSetAttribute(pf_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kPfStages * kPfStageBytes + 1024)));
+    MOEB_CUDA(cudaFuncSetAttribute(pf_router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(kPfRouterTok * (d + 8) * 2 + kPfRouterTok * E * 4)));
+  }
+  if (S->rec_cap && N > S->pf_log_n) {
+    const uint32_t L = S->L;
+    S->pf_log_x.alloc((size_t)L * N * d);
+    S->pf_log_scores.alloc((size_t)L * N * E);
+    S->pf_log_y.alloc((size_t)L * N * d);
+    S->pf_log_sel.alloc((size_t)L * N * k);
+    S->pf_log_n = N;
+  }
+}
+
+static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N, cudaStream_t s) {
+  const uint32_t L = S->L, E = S->E, k = S->cfg.top_k, d = S->d, F = S->F, Sh = S->S;
+  if (!S->umma)
+    throw Error(1, "prefill needs the UMMA-tiled expert layout (a stack with max_batch 2..32, ffn and "
+                   "shared_ffn multiples of 128)");
+  if (N == 0) throw Error(1, "prefill: no tokens");
+  if (k > kPfMaxK) throw Error(1, "prefill: top_k > 16");
+  prefill_alloc(S, N);
+  // the cache residency each layer's items read (the decode state is not changed)
+  MOEB_CUDA(cudaStreamSynchronize(s));
+  std::vector<LayerState> ls(L);
+  MOEB_CUDA(cudaMemcpy(ls.data(), S->layers.p, sizeof(LayerState) * L, cudaMemcpyDeviceToHost));
+  const uint64_t eb = S->expert_elems * 2;
+  bool any_up = false;
+  for (uint32_t l = 0; l < L; ++l)
+    if (ls[l].mask != (E == 64 ? ~0ull : ((1ull << E) - 1))) any_up = true;
+  if (any_up && !S->pf_stage.p) S->pf_stage.alloc(2 * (size_t)E * S->expert_elems);
+  uint64_t h2d = 0;
+  std::vector<char> up(L, 0);
+  auto upload = [&](uint32_t l) {
+    unsigned char* dst = reinterpret_cast<unsigned char*>(S->pf_stage.p) + (size_t)(l % 2) * E * eb;
+    const unsigned char* src = reinterpret_cast<const unsigned char*>(S->pool) + (size_t)l * E * eb;
+    for (uint32_t e = 0; e < E;) {
+      if ((ls[l].mask >> e) & 1ull) {
+        ++e;
+        continue;
+      }
+      uint32_t e1 = e;
+      while (e1 < E && !((ls[l].mask >> e1) & 1ull)) ++e1;  // a run of non-resident experts: one copy
+      MOEB_CUDA(cudaMemcpyAsync(dst + (size_t)e * eb, src + (size_t)e * eb, (size_t)(e1 - e) * eb,
+                                cudaMemcpyHostToDevice, S->pf_copy));
+      h2d += (uint64_t)(e1 - e) * eb;
+      up[l] = 1;
+      e = e1;
+    }
+    MOEB_CUDA(cudaEventRecord(S->pf_up[l % 2], S->pf_copy));
+  };
+  int n_sm = 0;
+  MOEB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, S->device));
+  const size_t r_smem = (size_t)kPfRouterTok * (d + 8) * 2 + (size_t)kPfRouterTok * E * 4;
+  const bool log = S->rec_cap != 0;
+  if (any_up) upload(0);
+  for (uint32_t l = 0; l < L; ++l) {
+    if (any_up && l + 1 < L) {
+      if (l >= 1) MOEB_CUDA(cudaStreamWaitEvent(S->pf_copy, S->pf_free[(l + 1) % 2], 0));
+      upload(l + 1);
+    }
+    if (up[l]) MOEB_CUDA(cudaStreamWaitEvent(s, S->pf_up[l % 2], 0));
+    const uint16_t* xin = l == 0 ? static_cast<const uint16_t*>(x) : S->pf_hid.p + (size_t)((l - 1) % 2) * N * d;
+    uint16_t* xout = l + 1 == L ? static_cast<uint16_t*>(y) : S->pf_hid.p + (size_t)(l % 2) * N * d;
+    PfRouterArgs ra{};
+    ra.x = xin;
+    ra.wg = S->gate_w.p + (size_t)l * E * d;
+    ra.wsg = S->model.shared_gate ? S->sgate_w.p + (size_t)l * d : nullptr;
+    ra.u = S->pf_u.p;
+    ra.scores = S->pf_scores.p;
+    ra.sel = S->pf_sel.p;
+    ra.wts = S->pf_wts.p;
+    ra.sgate = S->pf_sgate.p;
+    ra.N = N;
+    ra.d = d;
+    ra.E = E;
+    ra.k = k;
+    ra.renormalize = S->model.renormalize;
+    ra.routed_scale = S->model.routed_scale;
+    pf_router_kernel<<<(N + kPfRouterTok - 1) / kPfRouterTok, 256, r_smem, s>>>(ra);
+    MOEB_CUDA(cudaGetLastError());
+    PfPermuteArgs pa{};
+    pa.sel = S->pf_sel.p;
+    pa.wts = S->pf_wts.p;
+    pa.sgate = S->pf_sgate.p;
+    pa.ls = S->layers.p + l;
+    pa.slot_base = reinterpret_cast<const unsigned char*>(S->slots.p + (size_t)l * S->slots_alloc * S->expert_elems);
+    pa.stage_base = S->pf_stage.p ? reinterpret_cast<const unsigned char*>(S->pf_stage.p) + (size_t)(l % 2) * E * eb
+                                  : nullptr;
+    pa.shared_w = Sh ? reinterpret_cast<const unsigned char*>(S->shared_w.p + (size_t)l * 3 * Sh * d) : nullptr;
+    pa.expert_bytes = eb;
+    pa.N = N;
+    pa.k = k;
+    pa.E = E;
+    pa.d = d;
+    pa.F = F;
+    pa.S = Sh;
+    pa.items = S->pf_items.p;
+    pa.hdr = S->pf_hdr.p;
+    pa.slot_tok = S->pf_slot_tok.p;
+    pa.slot_w = S->pf_slot_w.p;
+    pa.entry_slot = S->pf_entry.p;
+    pa.R = S->pf_R;
+    pf_permute_kernel<<<1, 1024, 0, s>>>(pa);
+    MOEB_CUDA(cudaGetLastError());
+    MOEB_CUDA(cudaMemsetAsync(S->pf_ctr.p, 0, S->pf_ctr.n * sizeof(uint32_t), s));
+    pf_gather_kernel<<<(unsigned)std::min<uint64_t>((S->pf_R + 7) / 8, (uint64_t)n_sm * 16), 256, 0, s>>>(
+        S->pf_u.p, S->pf_slot_tok.p, S->pf_hdr.p, S->pf_xg.p, d, S->pf_R);
+    MOEB_CUDA(cudaGetLastError());
+    PfGemmArgs ga{};
+    ga.items = S->pf_items.p;
+    ga.hdr = S->pf_hdr.p;
+    ga.xg = S->pf_xg.p;
+    ga.hg = S->pf_hg.p;
+    ga.out = S->pf_out.p;
+    ga.slot_w = S->pf_slot_w.p;
+    ga.ctr = S->pf_ctr.p;
+    ga.d = d;
+    ga.R = S->pf_R;
+    pf_gemm_kernel<<<n_sm, kPfThreads, kPfStages * kPfStageBytes + 1024, s>>>(ga);
+    MOEB_CUDA(cudaGetLastError());
+    if (any_up) MOEB_CUDA(cudaEventRecord(S->pf_free[l % 2], s));
+    float* ylog = log && N <= S->pf_log_n ? S->pf_log_y.p + (size_t)l * N * d : nullptr;
+    pf_combine_kernel<<<(unsigned)std::min<uint64_t>(((uint64_t)N * d / 4 + 255) / 256, (uint64_t)n_sm * 16), 256, 0,
+                        s>>>(xin, S->pf_out.p, S->pf_entry.p, xout, ylog, N, d, k, Sh ? 1u : 0u);
+    MOEB_CUDA(cudaGetLastError());
+    if (ylog) {
+      MOEB_CUDA(cudaMemcpyAsync(S->pf_log_x.p + (size_t)l * N * d, xin, (size_t)N * d * 2, cudaMemcpyDeviceToDevice, s));
+      MOEB_CUDA(cudaMemcpyAsync(S->pf_log_scores.p + (size_t)l * N * E, S->pf_scores.p, (size_t)N * E * 4,
+                                cudaMemcpyDeviceToDevice, s));
+      MOEB_CUDA(cudaMemcpyAsync(S->pf_log_sel.p + (size_t)l * N * k, S->pf_sel.p, (size_t)N * k, cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  if (log) S->pf_last_n = N;
+  return h2d;
+}
+
 // The device raises g_spin_timeout when a bounded wait gives up. It is read
 // and cleared together: the failure is reported once (by the moeb_sync that
 // observes it) and does not poison later syncs of this or other stacks.
@@ -1935,6 +2140,39 @@ int moeb_set_logits_trace(moeb_stack* s, const float* logits, uint64_t n_steps, 
 
 int moeb_step(moeb_stack* s, const void* x, void* y, uint32_t B, void* stream) {
   return guarded([&] { step_stack(s, x, y, B, static_cast<cudaStream_t>(stream)); });
+}
+
+int moeb_prefill(moeb_stack* s, const void* x, void* y, uint32_t n_tokens, void* stream, uint64_t* h2d_bytes) {
+  return guarded([&] {
+    if (s->copier_error) throw Error(5, s->copier_msg);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s->stream;
+    MOEB_CUDA(cudaSetDevice(s->device));
+    DeviceOrder& o = device_order(s->device);
+    std::lock_guard<std::mutex> lk(o.mu);
+    if (!o.ev) MOEB_CUDA(cudaEventCreateWithFlags(&o.ev, cudaEventDisableTiming));
+    if (o.owner && o.owner != s) MOEB_CUDA(cudaStreamWaitEvent(st, o.ev, 0));
+    const uint64_t b = prefill_stack(s, x, y, n_tokens, st);
+    MOEB_CUDA(cudaEventRecord(o.ev, st));
+    o.owner = s;
+    if (h2d_bytes) *h2d_bytes = b;
+  });
+}
+
+int moeb_get_prefill_log(moeb_stack* s, uint32_t layer, uint32_t* n_tokens, uint16_t* x_in, float* scores,
+                         uint8_t* sel, float* y) {
+  return guarded([&] {
+    if (!s->rec_cap) throw Error(1, "prefill log needs MOEB_MODEL_LOG_STEPS");
+    if (!s->pf_last_n) throw Error(1, "no prefill has run");
+    if (layer >= s->L) throw Error(1, "layer out of range");
+    MOEB_CUDA(cudaSetDevice(s->device));
+    MOEB_CUDA(cudaDeviceSynchronize());
+    const size_t N = s->pf_last_n, d = s->d, E = s->E, k = s->cfg.top_k;
+    if (n_tokens) *n_tokens = (uint32_t)N;
+    if (x_in) MOEB_CUDA(cudaMemcpy(x_in, s->pf_log_x.p + layer * N * d, N * d * 2, cudaMemcpyDeviceToHost));
+    if (scores) MOEB_CUDA(cudaMemcpy(scores, s->pf_log_scores.p + layer * N * E, N * E * 4, cudaMemcpyDeviceToHost));
+    if (sel) MOEB_CUDA(cudaMemcpy(sel, s->pf_log_sel.p + layer * N * k, N * k, cudaMemcpyDeviceToHost));
+    if (y) MOEB_CUDA(cudaMemcpy(y, s->pf_log_y.p + layer * N * d, N * d * 4, cudaMemcpyDeviceToHost));
+  });
 }
 
 int moeb_sync(moeb_stack* s) {
