@@ -291,3 +291,199 @@ void cpu_moe_layer(const uint16_t* x, uint32_t d, uint32_t F, uint32_t S, uint32
 
 /* Weight bytes read by cpu_moe_layer since the last call (then reset). */
 uint64_t cpu_bytes_touched(void) { return atomic_exchange(&g_bytes, 0); }
+
+/* ------------------------------------------------------------ prefill */
+/* The prefill layer (csrc/prefill.cuh restated on the CPU): N tokens, plain
+ * top-k routing (score desc, index asc: router.cpp:252-260), the shared
+ * expert + the selected experts batched per expert: every weight row is read
+ * once per layer and reused across all of that expert's tokens (phase 1 by
+ * (item, intermediate row), phase 2 by output row). */
+#define PF_MAX_ITEMS 80
+typedef struct {
+  const uint16_t* w;
+  uint32_t F, n;        /* intermediate rows, tokens */
+  const uint32_t* tok;  /* [n] */
+  const float* wt;      /* [n] */
+  float* h;             /* [n][F] */
+  uint64_t row0;        /* first phase-1 row */
+} pf_item;
+
+typedef struct {
+  uint32_t N, d, E, k, n_items;
+  const uint16_t* router;
+  const uint16_t* shared_gate;
+  float* u;             /* [N][d] */
+  float* logits;        /* [N][E] */
+  float* sg;            /* [N] */
+  pf_item it[PF_MAX_ITEMS];
+  uint64_t rows1;
+  float* y;             /* [N][d] */
+} pf_ctx;
+
+static void pf_route(void* p, int tid, int nt) {
+  pf_ctx* c = (pf_ctx*)p;
+  uint64_t lo, hi;
+  split(c->N, tid, nt, &lo, &hi);
+  for (uint64_t t = lo; t < hi; ++t) {
+    const float* u = c->u + t * c->d;
+    for (uint32_t e = 0; e < c->E; ++e) c->logits[t * c->E + e] = dot_bf16(c->router + (size_t)e * c->d, u, c->d);
+    c->sg[t] = c->shared_gate ? 1.0f / (1.0f + expf(-dot_bf16(c->shared_gate, u, c->d))) : 1.0f;
+  }
+}
+
+static void pf_phase1(void* p, int tid, int nt) {
+  pf_ctx* c = (pf_ctx*)p;
+  uint64_t lo, hi;
+  split(c->rows1, tid, nt, &lo, &hi);
+  const uint32_t d = c->d;
+  for (uint64_t r = lo; r < hi;) {
+    uint32_t k = 0;
+    while (k + 1 < c->n_items && c->it[k + 1].row0 <= r) ++k;
+    pf_item* t = &c->it[k];
+    const uint64_t end = t->row0 + t->F < hi ? t->row0 + t->F : hi;
+    for (; r < end; ++r) {
+      const uint64_t j = r - t->row0;
+      const uint16_t* g = t->w + j * d;
+      const uint16_t* up = t->w + (size_t)t->F * d + j * d;
+      for (uint32_t i = 0; i < t->n; ++i) {
+        const float* u = c->u + (size_t)t->tok[i] * d;
+        const float gv = dot_bf16(g, u, d), uv = dot_bf16(up, u, d);
+        t->h[(size_t)i * t->F + j] = gv / (1.0f + expf(-gv)) * uv;
+      }
+    }
+  }
+}
+
+static void pf_phase2(void* p, int tid, int nt) {
+  pf_ctx* c = (pf_ctx*)p;
+  uint64_t lo, hi;
+  split(c->d, tid, nt, &lo, &hi);
+  const uint32_t d = c->d;
+  for (uint64_t o = lo; o < hi; ++o)
+    for (uint32_t k = 0; k < c->n_items; ++k) {
+      const pf_item* t = &c->it[k];
+      const uint16_t* dn = t->w + 2 * (size_t)t->F * d + o * t->F;
+      for (uint32_t i = 0; i < t->n; ++i)
+        c->y[(size_t)t->tok[i] * d + o] += t->wt[i] * dot_bf16(dn, t->h + (size_t)i * t->F, t->F);
+    }
+}
+
+/* x, x_next: [N][d] bf16; experts: [E] weight pointers ([gate][up][down]);
+ * y_out (nullable): the fp32 layer output [N][d]. */
+void cpu_moe_prefill_layer(const uint16_t* x, uint32_t N, uint32_t d, uint32_t F, uint32_t S, uint32_t E,
+                           uint32_t k, const uint16_t* router, const uint16_t* shared,
+                           const uint16_t* shared_gate, const uint16_t* const* experts, int renormalize,
+                           float routed_scale, uint16_t* x_next, float* y_out, int nthreads) {
+  pthread_mutex_lock(&g_pool.mu);
+  pool_ensure(nthreads);
+  static pf_ctx c;  /* under g_pool.mu */
+  c.N = N;
+  c.d = d;
+  c.E = E;
+  c.k = k;
+  c.router = router;
+  c.shared_gate = S ? shared_gate : NULL;
+  c.u = (float*)aligned_alloc(64, sizeof(float) * (size_t)N * d);
+  c.logits = (float*)malloc(sizeof(float) * (size_t)N * E);
+  c.sg = (float*)malloc(sizeof(float) * N);
+  c.y = (float*)calloc((size_t)N * d, sizeof(float));
+  for (uint32_t t = 0; t < N; ++t) {
+    const uint16_t* xt = x + (size_t)t * d;
+    double ss = 0.0;
+    for (uint32_t i = 0; i < d; ++i) ss += (double)bf(xt[i]) * bf(xt[i]);
+    const float inv = (float)(1.0 / sqrt(ss / d + 1e-6));
+    for (uint32_t i = 0; i < d; ++i) c.u[(size_t)t * d + i] = bf(to_bf(bf(xt[i]) * inv));
+  }
+  pool_run(pf_route, &c);
+  /* softmax, plain top-k, combine weights; per-expert token lists */
+  uint32_t* cnt = (uint32_t*)calloc(E, sizeof(uint32_t));
+  uint32_t* sel = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)N * k);
+  float* wsel = (float*)malloc(sizeof(float) * (size_t)N * k);
+  float* sc = (float*)malloc(sizeof(float) * E);
+  for (uint32_t t = 0; t < N; ++t) {
+    const float* lg = c.logits + (size_t)t * E;
+    float m = lg[0];
+    for (uint32_t e = 1; e < E; ++e) m = lg[e] > m ? lg[e] : m;
+    float s = 0.f;
+    for (uint32_t e = 0; e < E; ++e) s += (sc[e] = expf(lg[e] - m));
+    for (uint32_t e = 0; e < E; ++e) sc[e] /= s;
+    float den = 0.f;
+    for (uint32_t e = 0; e < E; ++e) {
+      uint32_t rk = 0;
+      for (uint32_t j = 0; j < E; ++j) rk += (sc[j] > sc[e] || (sc[j] == sc[e] && j < e));
+      if (rk < k) {
+        sel[(size_t)t * k + rk] = e;
+        wsel[(size_t)t * k + rk] = sc[e];
+      }
+    }
+    for (uint32_t r = 0; r < k; ++r) den += wsel[(size_t)t * k + r];
+    for (uint32_t r = 0; r < k; ++r) {
+      float w = wsel[(size_t)t * k + r];
+      if (renormalize) w /= den;
+      wsel[(size_t)t * k + r] = w * routed_scale;
+      ++cnt[sel[(size_t)t * k + r]];
+    }
+  }
+  uint32_t* toks = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)N * k + N));
+  float* tw = (float*)malloc(sizeof(float) * ((size_t)N * k + N));
+  uint64_t hsz = (uint64_t)N * S;
+  for (uint32_t e = 0; e < E; ++e) hsz += (uint64_t)cnt[e] * F;
+  float* hbuf = (float*)malloc(sizeof(float) * (hsz + 8));
+  uint32_t n_items = 0, off = 0;
+  uint64_t row = 0, hoff = 0;
+  if (S) {
+    pf_item* it = &c.it[n_items++];
+    it->w = shared;
+    it->F = S;
+    it->n = N;
+    for (uint32_t t = 0; t < N; ++t) {
+      toks[t] = t;
+      tw[t] = c.sg[t];
+    }
+    it->tok = toks;
+    it->wt = tw;
+    off = N;
+  }
+  for (uint32_t e = 0; e < E; ++e) {
+    if (!cnt[e]) continue;
+    pf_item* it = &c.it[n_items++];
+    it->w = experts[e];
+    it->F = F;
+    it->n = 0;
+    it->tok = toks + off;
+    it->wt = tw + off;
+    for (uint32_t t = 0; t < N; ++t)
+      for (uint32_t r = 0; r < k; ++r)
+        if (sel[(size_t)t * k + r] == e) {
+          toks[off + it->n] = t;
+          tw[off + it->n] = wsel[(size_t)t * k + r];
+          ++it->n;
+        }
+    off += it->n;
+  }
+  for (uint32_t i = 0; i < n_items; ++i) {
+    c.it[i].row0 = row;
+    c.it[i].h = hbuf + hoff;
+    row += c.it[i].F;
+    hoff += (uint64_t)c.it[i].n * c.it[i].F;
+    atomic_fetch_add(&g_bytes, 3ull * c.it[i].F * d * 2);
+  }
+  c.n_items = n_items;
+  c.rows1 = row;
+  pool_run(pf_phase1, &c);
+  pool_run(pf_phase2, &c);
+  for (size_t i = 0; i < (size_t)N * d; ++i) x_next[i] = to_bf(bf(x[i]) + c.y[i]);
+  if (y_out) memcpy(y_out, c.y, sizeof(float) * (size_t)N * d);
+  pthread_mutex_unlock(&g_pool.mu);
+  free(c.u);
+  free(c.logits);
+  free(c.sg);
+  free(c.y);
+  free(cnt);
+  free(sel);
+  free(wsel);
+  free(sc);
+  free(toks);
+  free(tw);
+  free(hbuf);
+}

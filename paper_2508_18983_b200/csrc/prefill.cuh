@@ -6,33 +6,37 @@
 //
 // Per layer, five launches on the stack's stream:
 //   pf_router_kernel   RMSNorm (the decode gate's arithmetic) + router logits
-//                      on mma.sync (32 tokens x 64 experts per CTA) + softmax +
-//                      top-k by counting (score desc, index asc: plain_top_k,
-//                      router.cpp:252-260) + combine weights
-//   pf_permute_kernel  token -> expert permutation: a warp-aggregated
-//                      histogram (__match_any_sync, one shared atomic per
-//                      distinct expert per warp), the expert segments (each
-//                      padded to 16 rows), and a warp-aggregated scatter of
-//                      (token, rank) entries into slot rows; builds the item /
-//                      unit tables of the GEMM (north_star item 4)
-//   pf_gather_kernel   activations of every slot row into the SW128 K-major
-//                      operand layout the MMA reads ([d/64][R][64] bf16)
+//                      on mma.sync (16 tokens x 16 experts per CTA, K split
+//                      over warps); writes the shared expert's operand rows
+//   pf_topk_kernel     softmax + top-k by counting (score desc, index asc:
+//                      plain_top_k, router.cpp:252-260) + combine weights +
+//                      the expert histogram (shared-memory, then one global
+//                      atomic per expert per CTA); its last CTA builds the
+//                      plan with one warp: expert segments (each padded to 16
+//                      rows), the item table and the GEMM's unit numbering
+//   pf_scatter_kernel  token -> expert permutation (north_star item 4): a
+//                      warp's entries of one expert (__match_any_sync) take
+//                      consecutive slot rows with one atomic, then the warp
+//                      copies each entry's activation row into its slot in the
+//                      SW128 K-major operand layout the MMA reads
 //   pf_gemm_kernel     grouped SwiGLU: persistent, one CTA per SM; units
-//                      gate_up (item, token tile <= 128, 128 intermediate rows)
-//                      and down (item, token tile, 128 output rows), grabbed
-//                      from one grid counter; tcgen05.mma M = 128, N = token
-//                      tile, fp32 accumulators in TMEM (two buffers of 256
-//                      columns), operands staged by cp.async.bulk (weights are
-//                      UMMA-tiled, weights.cuh); h = silu(g) * up kept as bf16
-//                      hi + lo (h = hi + lo to 2^-17), both accumulated by the
-//                      down MMA; the down epilogue writes w_slot * y per slot row
+//                      gate_up (item, 128 intermediate rows, token tile <= 128)
+//                      and down (item, 128 output rows, token tile), token
+//                      tiles innermost so a weight tile's re-reads hit L2,
+//                      grabbed from one grid counter; tcgen05.mma M = 128,
+//                      N = token tile, fp32 accumulators in TMEM (two buffers
+//                      of 256 columns), operands staged by cp.async.bulk
+//                      (weights are UMMA-tiled, weights.cuh); h = silu(g) * up
+//                      kept as bf16 hi + lo (h = hi + lo to 2^-17), both
+//                      accumulated by the down MMA; the down epilogue writes
+//                      w_slot * y per slot row
 //   pf_combine_kernel  per token: shared expert row + its k slot rows in rank
 //                      order, residual, bf16 hidden for the next layer
 //
-// Token slot positions inside an expert segment come from shared-memory
-// atomics (not deterministic), but every GEMM column is an independent
-// dot product and the combine sums a token's slots in rank order, so the
-// hidden output is bitwise reproducible.
+// Token slot positions inside an expert segment come from atomics (not
+// deterministic), but every GEMM column is an independent dot product and
+// the combine sums a token's slots in rank order, so the hidden output is
+// bitwise reproducible.
 #pragma once
 
 #include <cstdint>
@@ -47,7 +51,7 @@ constexpr uint32_t kPfStages = 4;
 constexpr uint32_t kPfThreads = 6 * 32;
 constexpr uint32_t kPfTmemCols = 512;           // two buffers x (gate 128 | up 128) columns
 constexpr uint32_t kPfNt = 128;                 // token rows per unit (max MMA N of one accumulator pair)
-constexpr uint32_t kPfRouterTok = 32;           // tokens per router CTA
+constexpr uint32_t kPfRouterTok = 16;           // tokens per router CTA (one m16 tile)
 constexpr uint32_t kPfMaxK = 16;
 
 struct PfItem {
@@ -70,33 +74,41 @@ struct PfRouterArgs {
   const uint16_t* wg;   // [E][d] router weights
   const uint16_t* wsg;  // [d] shared-expert gate row (Qwen) or null
   uint16_t* u;          // [N][d] normalised input (bf16)
-  float* scores;        // [N][E] fp32 softmax scores
-  uint8_t* sel;         // [N][k] selected experts in rank order
-  float* wts;           // [N][k] combine weights
-  float* sgate;         // [N] sigmoid of the shared-gate logit (1 when none)
-  uint32_t N, d, E, k;
-  int32_t renormalize;
-  float routed_scale;
+  unsigned char* xg;    // SW128 activations: rows [0, N) = the shared expert's (null: no shared expert)
+  float* logits;        // [N][E + 1]; column E = shared-gate logit
+  uint32_t N, d, E, R;
 };
 
-// 256 threads, dynamic smem: [32][d + 8] bf16 (u) + [32][E] fp32 (logits)
+// grid (ceil(N / 16), ceil(E / 16)), 256 threads; dynamic smem [16][d + 8]
+// bf16. Each CTA: RMSNorm of its 16 tokens (the decode gate's arithmetic,
+// layer.cuh gate_phase), then logits of 16 experts on mma.sync m16n8k16:
+// warp w takes the K eighth w; the eighths are summed in a fixed order
+// (fp32 accumulation).
 __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ PfRouterArgs a) {
   extern __shared__ __align__(16) unsigned char pf_rsm[];
-  const uint32_t d = a.d, E = a.E, k = a.k, ld = d + 8;
+  const uint32_t d = a.d, E = a.E, ld = d + 8;
   uint16_t* us = reinterpret_cast<uint16_t*>(pf_rsm);
-  float* lg = reinterpret_cast<float*>(pf_rsm + (size_t)kPfRouterTok * ld * 2);
   __shared__ float inv_rms[kPfRouterTok];
+  __shared__ float part[8][kPfRouterTok][16];
   const int lane = lane_id(), warp = warp_id();
-  const uint32_t t0 = blockIdx.x * kPfRouterTok;
+  const uint32_t t0 = blockIdx.x * kPfRouterTok, e0 = blockIdx.y * 16;
   const uint32_t nt = min(kPfRouterTok, a.N - t0), nvec = d / 8;
-  // x -> smem (rows >= nt zero)
-  for (uint32_t i = threadIdx.x; i < kPfRouterTok * nvec; i += blockDim.x) {
-    const uint32_t t = i / nvec, c = i % nvec;
-    const uint4 v = t < nt ? reinterpret_cast<const uint4*>(a.x + (size_t)(t0 + t) * d)[c] : make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(us + (size_t)t * ld + c * 8) = v;
+  const bool first = blockIdx.y == 0;
+  for (uint32_t i0 = threadIdx.x; i0 < kPfRouterTok * nvec; i0 += 8 * blockDim.x) {
+    uint4 v[8];  // 8 independent 16 B loads in flight per thread
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+      const uint32_t i = i0 + j * blockDim.x, t = i / nvec, c = i % nvec;
+      v[j] = i < kPfRouterTok * nvec && t < nt ? __ldg(reinterpret_cast<const uint4*>(a.x + (size_t)(t0 + t) * d) + c)
+                                               : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+      const uint32_t i = i0 + j * blockDim.x, t = i / nvec, c = i % nvec;
+      if (i < kPfRouterTok * nvec) *reinterpret_cast<uint4*>(us + (size_t)t * ld + c * 8) = v[j];
+    }
   }
   __syncthreads();
-  // RMSNorm (eps 1e-6, unit weight), the decode gate's arithmetic (layer.cuh gate_phase)
   for (uint32_t t = warp; t < kPfRouterTok; t += 8) {
     float ss = 0.f;
     for (uint32_t c = lane; c < nvec; c += 32) {
@@ -122,60 +134,180 @@ __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ 
     }
     const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
     *p = ov;
-    if (t < nt) reinterpret_cast<uint4*>(a.u + (size_t)(t0 + t) * d)[c] = ov;
-  }
-  __syncthreads();
-  // logits = u . Wg^T on mma.sync m16n8k16: warp w -> token rows 16 (w & 1),
-  // experts 16 (w >> 1) .. +15 (two n8 tiles); fp32 accumulation
-  {
-    const uint32_t m0 = 16 * (warp & 1), e0 = 16 * (warp >> 1);
-    if (e0 < E) {
-      float acc[2][4] = {};
-      const uint32_t a_addr = smem_u32(us + (size_t)(m0 + (lane & 15)) * ld + (lane >> 4) * 8);
-      const uint32_t* w0 = nullptr;
-      const uint32_t* w1 = nullptr;
-      const uint32_t ea = e0 + (lane >> 2), eb = e0 + 8 + (lane >> 2);
-      if (ea < E) w0 = reinterpret_cast<const uint32_t*>(a.wg + (size_t)ea * d) + (lane & 3);
-      if (eb < E) w1 = reinterpret_cast<const uint32_t*>(a.wg + (size_t)eb * d) + (lane & 3);
-      for (uint32_t k0 = 0; k0 < d; k0 += 64) {
-        uint32_t b[4][2][2];
-#pragma unroll
-        for (uint32_t s = 0; s < 4; ++s) {
-          const uint32_t kw = (k0 + s * 16) / 2;
-          b[s][0][0] = w0 ? __ldg(w0 + kw) : 0u;
-          b[s][0][1] = w0 ? __ldg(w0 + kw + 4) : 0u;
-          b[s][1][0] = w1 ? __ldg(w1 + kw) : 0u;
-          b[s][1][1] = w1 ? __ldg(w1 + kw + 4) : 0u;
-        }
-#pragma unroll
-        for (uint32_t s = 0; s < 4; ++s) {
-          uint32_t af[4];
-          ldsm_x4(a_addr + (k0 + s * 16) * 2, af);
-          mma16816(acc[0], af, b[s][0][0], b[s][0][1]);
-          mma16816(acc[1], af, b[s][1][0], b[s][1][1]);
-        }
-      }
-#pragma unroll
-      for (uint32_t j = 0; j < 2; ++j) {
-        const uint32_t r = m0 + (lane >> 2), e = e0 + 8 * j + 2 * (lane & 3);
-        if (e < E) {
-          lg[r * E + e] = acc[j][0];
-          lg[(r + 8) * E + e] = acc[j][2];
-        }
-        if (e + 1 < E) {
-          lg[r * E + e + 1] = acc[j][1];
-          lg[(r + 8) * E + e + 1] = acc[j][3];
-        }
+    if (first && t < nt) {
+      reinterpret_cast<uint4*>(a.u + (size_t)(t0 + t) * d)[c] = ov;
+      if (a.xg) {  // the shared expert's operand rows = the tokens in order
+        const uint32_t r = t0 + t;
+        const size_t off = (size_t)(c >> 3) * a.R * 128u + (r >> 3) * 1024u + (r & 7u) * 128u + (((c ^ r) & 7u) << 4);
+        *reinterpret_cast<uint4*>(a.xg + off) = ov;
       }
     }
   }
   __syncthreads();
-  // per token (warp): softmax, top-k by counting, combine weights, shared gate
-  for (uint32_t t = warp; t < nt; t += 8) {
+  {
+    const uint32_t kq = warp, kspan = d / 8;
+    float acc[2][4] = {};
+    const uint32_t a_addr = smem_u32(us + (size_t)(lane & 15) * ld + (lane >> 4) * 8);
+    const uint32_t ea = e0 + (lane >> 2), eb = e0 + 8 + (lane >> 2);
+    const uint32_t* w0 = ea < E ? reinterpret_cast<const uint32_t*>(a.wg + (size_t)ea * d) + (lane & 3) : nullptr;
+    const uint32_t* w1 = eb < E ? reinterpret_cast<const uint32_t*>(a.wg + (size_t)eb * d) + (lane & 3) : nullptr;
+#pragma unroll 4
+    for (uint32_t k0 = kq * kspan; k0 < (kq + 1) * kspan; k0 += 16) {
+      const uint32_t kw = k0 / 2;
+      const uint32_t b00 = w0 ? __ldg(w0 + kw) : 0u, b01 = w0 ? __ldg(w0 + kw + 4) : 0u;
+      const uint32_t b10 = w1 ? __ldg(w1 + kw) : 0u, b11 = w1 ? __ldg(w1 + kw + 4) : 0u;
+      uint32_t af[4];
+      ldsm_x4(a_addr + k0 * 2, af);
+      mma16816(acc[0], af, b00, b01);
+      mma16816(acc[1], af, b10, b11);
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < 2; ++j) {
+      const uint32_t r = lane >> 2, e = 8 * j + 2 * (lane & 3);
+      part[kq][r][e] = acc[j][0];
+      part[kq][r][e + 1] = acc[j][1];
+      part[kq][r + 8][e] = acc[j][2];
+      part[kq][r + 8][e + 1] = acc[j][3];
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kPfRouterTok * 16; i += blockDim.x) {
+    const uint32_t t = i / 16, e = i % 16;
+    if (t < nt && e0 + e < E) {
+      float v = 0.f;
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) v += part[q][t][e];  // fixed order
+      a.logits[(size_t)(t0 + t) * (E + 1) + e0 + e] = v;
+    }
+  }
+  if (first && a.wsg)  // Qwen shared-expert gate logit
+    for (uint32_t t = warp; t < nt; t += 8) {
+      float s = 0.f;
+      const uint4* wv = reinterpret_cast<const uint4*>(a.wsg);
+      for (uint32_t c = lane; c < nvec; c += 32)
+        s += dot8(__ldg(wv + c), *reinterpret_cast<const uint4*>(us + (size_t)t * ld + c * 8));
+      s = warp_sum(s);
+      if (lane == 0) a.logits[(size_t)(t0 + t) * (E + 1) + E] = s;
+    }
+}
+
+// ------------------------------------------------------------ plan
+struct PfPlanArgs {
+  uint32_t* cnt;         // [E] tokens per expert (re-zeroed here for the next layer)
+  uint32_t* cursor;      // [E] next free slot row of each expert segment
+  const LayerState* ls;  // this layer's cache state (residency, slots)
+  const unsigned char* slot_base;   // this layer's cache slots
+  const unsigned char* stage_base;  // staging of the non-resident experts (by expert id)
+  const unsigned char* shared_w;    // shared expert (null: none)
+  uint64_t expert_bytes;
+  uint32_t N, E, d, F, S;
+  PfItem* items;
+  PfHdr* hdr;
+};
+
+// One warp: the expert segments (each padded to 16 rows, experts in
+// ascending order after the shared expert's N rows), the item table and the
+// GEMM's unit numbering (lane-parallel prefix sums).
+__device__ void pf_plan_warp(const PfPlanArgs& a) {
+  const int lane = lane_id();
+  const uint32_t nmt = a.d / 128, ftl = a.F / 128;
+  uint32_t rows = 0, tiles = 0, gu = 0, n_items = 0;
+  if (a.S) {
+    PfItem it{};
+    it.w = a.shared_w;
+    it.F = a.S;
+    it.n = a.N;
+    it.ntile = (a.N + kPfNt - 1) / kPfNt;
+    it.expert = 0xFFFFu;
+    if (lane == 0) a.items[0] = it;
+    rows = (a.N + 15) & ~15u;
+    tiles = it.ntile;
+    gu = it.ntile * (a.S / 128);
+    n_items = 1;
+  }
+  const uint64_t mask = a.ls->mask;
+  for (uint32_t e0 = 0; e0 < a.E; e0 += 32) {
+    const uint32_t e = e0 + lane;
+    const uint32_t c = e < a.E ? __ldcg(&a.cnt[e]) : 0u;
+    const uint32_t pr = (c + 15) & ~15u, nt = (c + kPfNt - 1) / kPfNt;
+    uint32_t sr = pr, st = nt, sg = nt * ftl, si = c ? 1u : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t vr = __shfl_up_sync(0xffffffffu, sr, o), vt = __shfl_up_sync(0xffffffffu, st, o);
+      const uint32_t vg = __shfl_up_sync(0xffffffffu, sg, o), vi = __shfl_up_sync(0xffffffffu, si, o);
+      if (lane >= o) { sr += vr; st += vt; sg += vg; si += vi; }
+    }
+    if (c) {
+      PfItem it{};
+      const bool res = (mask >> e) & 1ull;
+      it.w = res ? a.slot_base + (uint64_t)a.ls->slot_of[e] * a.expert_bytes : a.stage_base + (uint64_t)e * a.expert_bytes;
+      it.F = a.F;
+      it.row0 = rows + sr - pr;
+      it.n = c;
+      it.ntile = nt;
+      it.tile0 = tiles + st - nt;
+      it.gu0 = gu + sg - nt * ftl;
+      it.expert = e;
+      a.items[n_items + si - 1] = it;
+    }
+    if (e < a.E) {
+      a.cursor[e] = rows + sr - pr;
+      a.cnt[e] = 0;
+    }
+    rows += __shfl_sync(0xffffffffu, sr, 31);
+    tiles += __shfl_sync(0xffffffffu, st, 31);
+    gu += __shfl_sync(0xffffffffu, sg, 31);
+    n_items += __shfl_sync(0xffffffffu, si, 31);
+  }
+  __syncwarp();
+  uint32_t dn = gu;  // down units after every gate_up unit, in item order
+  for (uint32_t i0 = 0; i0 < n_items; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < n_items ? __ldcg(&a.items[i].ntile) * nmt : 0u;
+    uint32_t s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += t;
+    }
+    if (i < n_items) a.items[i].dn0 = dn + s - v;
+    dn += __shfl_sync(0xffffffffu, s, 31);
+  }
+  if (lane == 0) *a.hdr = PfHdr{n_items, gu, dn - gu, rows, tiles};
+}
+
+// ------------------------------------------------------------ top-k
+struct PfTopkArgs {
+  const float* logits;   // [N][E + 1]
+  float* scores;         // [N][E] fp32 softmax scores
+  uint8_t* sel;          // [N][k] selected experts in rank order
+  float* wts;            // [N][k] combine weights
+  float* slot_w;         // [R]: rows [0, N) = the shared expert's weight per token (null: no shared expert)
+  uint32_t* cnt;         // [E] tokens per expert (histogram; zero on entry)
+  uint32_t* ticket;      // CTAs done (the last one builds the plan; reset to 0)
+  PfPlanArgs plan;
+  uint32_t N, E, k;
+  int32_t renormalize, shared_gate;
+  float routed_scale;
+};
+
+// One warp per token: softmax, rank by counting (score desc, index asc:
+// plain_top_k, router.cpp:252-260), combine weights; the expert histogram is
+// aggregated per CTA in shared memory, one global atomic per expert per CTA;
+// the last CTA to finish builds the plan (pf_plan_warp).
+__global__ void __launch_bounds__(256) pf_topk_kernel(const __grid_constant__ PfTopkArgs a) {
+  __shared__ uint32_t hist[kMaxE];
+  const int lane = lane_id();
+  const uint32_t E = a.E, k = a.k;
+  for (uint32_t e = threadIdx.x; e < kMaxE; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const uint32_t t = blockIdx.x * 8 + warp_id();
+  if (t < a.N) {
+    const float* lg = a.logits + (size_t)t * (E + 1);
     float sc[2];
     {
-      const float l0 = (uint32_t)lane < E ? lg[t * E + lane] : -INFINITY;
-      const float l1 = (uint32_t)lane + 32 < E ? lg[t * E + lane + 32] : -INFINITY;
+      const float l0 = (uint32_t)lane < E ? lg[lane] : -INFINITY;
+      const float l1 = (uint32_t)lane + 32 < E ? lg[lane + 32] : -INFINITY;
       float m = fmaxf(l0, l1);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -187,10 +319,8 @@ __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ 
       sc[0] = __fdiv_rn(x0, s);
       sc[1] = __fdiv_rn(x1, s);
     }
-    const size_t tg = t0 + t;
-    if ((uint32_t)lane < E) a.scores[tg * E + lane] = sc[0];
-    if ((uint32_t)lane + 32 < E) a.scores[tg * E + lane + 32] = sc[1];
-    // rank of expert e: #{j : s_j > s_e or (s_j == s_e and j < e)}
+    if ((uint32_t)lane < E) a.scores[(size_t)t * E + lane] = sc[0];
+    if ((uint32_t)lane + 32 < E) a.scores[(size_t)t * E + lane + 32] = sc[1];
     uint32_t rk[2] = {0u, 0u};
     for (uint32_t j = 0; j < E; ++j) {
       const float sj = __shfl_sync(0xffffffffu, sc[j >> 5], j & 31);
@@ -200,163 +330,66 @@ __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ 
         rk[h] += (sj > sc[h] || (sj == sc[h] && j < e)) ? 1u : 0u;
       }
     }
-    // denominator (renormalisation): selected scores summed in rank order
+    const bool s0 = (uint32_t)lane < E && rk[0] < k, s1 = (uint32_t)lane + 32 < E && rk[1] < k;
     float den = 1.f;
-    if (a.renormalize) {
+    if (a.renormalize) {  // selected scores summed in rank order
       den = 0.f;
       for (uint32_t r = 0; r < k; ++r) {
-        const uint32_t hit = __ballot_sync(0xffffffffu, (lane < (int)E && rk[0] == r) || (lane + 32 < (int)E && rk[1] == r));
-        const int src = __ffs(hit) - 1;
-        const float v = __shfl_sync(0xffffffffu, rk[0] == r && lane < (int)E ? sc[0] : sc[1], src);
-        den += v;
+        const uint32_t hit = __ballot_sync(0xffffffffu, (s0 && rk[0] == r) || (s1 && rk[1] == r));
+        den += __shfl_sync(0xffffffffu, (s0 && rk[0] == r) ? sc[0] : sc[1], __ffs(hit) - 1);
       }
     }
 #pragma unroll
     for (uint32_t h = 0; h < 2; ++h) {
-      const uint32_t e = lane + 32 * h;
-      if (e < E && rk[h] < k) {
-        a.sel[tg * k + rk[h]] = (uint8_t)e;
+      if (h ? s1 : s0) {
+        const uint32_t e = lane + 32 * h;
+        a.sel[(size_t)t * k + rk[h]] = (uint8_t)e;
         float w = sc[h];
         if (a.renormalize) w = __fdiv_rn(w, den);
-        a.wts[tg * k + rk[h]] = __fmul_rn(w, a.routed_scale);
+        a.wts[(size_t)t * k + rk[h]] = __fmul_rn(w, a.routed_scale);
+        atomicAdd(&hist[e], 1u);
       }
     }
-    if (a.sgate) {
-      float z = 1.f;
-      if (a.wsg) {
-        float s = 0.f;
-        const uint4* wv = reinterpret_cast<const uint4*>(a.wsg);
-        for (uint32_t c = lane; c < nvec; c += 32)
-          s += dot8(__ldg(wv + c), *reinterpret_cast<const uint4*>(us + (size_t)t * ld + c * 8));
-        s = warp_sum(s);
-        z = 1.f / (1.f + expf(-s));
-      }
-      if (lane == 0) a.sgate[tg] = z;
-    }
+    if (a.slot_w && lane == 0) a.slot_w[t] = a.shared_gate ? 1.f / (1.f + expf(-lg[E])) : 1.f;
+  }
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < E; e += blockDim.x)
+    if (hist[e]) atomicAdd(&a.cnt[e], hist[e]);
+  __shared__ uint32_t s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last && threadIdx.x < 32) {
+    __threadfence();
+    pf_plan_warp(a.plan);
+    if (threadIdx.x == 0) *a.ticket = 0;
   }
 }
 
-// ------------------------------------------------------------ permutation
-struct PfPermuteArgs {
+// ------------------------------------------------------------ scatter
+// The token -> expert permutation: a CTA takes 32 (token, rank) entries;
+// warp 0 gives the entries of one expert (__match_any_sync) consecutive slot
+// rows with one atomic on the expert's cursor; then the 8 warps copy the
+// entries' activation rows into their slots (SW128: 16 B chunk c of row r in
+// K-block c / 8 at chunk position (c ^ r) % 8).
+struct PfScatterArgs {
   const uint8_t* sel;    // [N][k]
   const float* wts;      // [N][k]
-  const float* sgate;    // [N] (shared expert weight)
-  const LayerState* ls;  // this layer's cache state (residency, slots)
-  const unsigned char* slot_base;   // this layer's cache slots
-  const unsigned char* stage_base;  // staging of the non-resident experts (by expert id)
-  const unsigned char* shared_w;    // shared expert (null: none)
-  uint64_t expert_bytes;
-  uint32_t N, k, E, d, F, S;
-  PfItem* items;
-  PfHdr* hdr;
-  int32_t* slot_tok;     // [R] token of each slot row (-1: padding)
-  float* slot_w;         // [R] combine weight of each slot row
-  int32_t* entry_slot;   // [N][k] slot row of each (token, rank)
-  uint32_t R;            // slot rows allocated
+  const uint16_t* u;     // [N][d]
+  uint32_t* cursor;      // [E]
+  float* slot_w;         // [R]
+  int32_t* entry_slot;   // [N][k]
+  unsigned char* xg;     // [d/64][R][128 B]
+  uint32_t N, k, d, R;
 };
 
-__global__ void __launch_bounds__(1024) pf_permute_kernel(const __grid_constant__ PfPermuteArgs a) {
-  __shared__ uint32_t cnt[kMaxE], base[kMaxE];
-  __shared__ uint32_t s_rows;
-  const int lane = lane_id();
-  const uint32_t n = a.N * a.k;
-  for (uint32_t e = threadIdx.x; e < kMaxE; e += blockDim.x) cnt[e] = 0;
-  __syncthreads();
-  // histogram: one shared atomic per distinct expert per warp
-  for (uint32_t i0 = threadIdx.x - lane; i0 < n; i0 += blockDim.x) {
-    const uint32_t i = i0 + lane;
-    const bool live = i < n;
-    const uint32_t e = live ? a.sel[i] : 0xFFu;
-    const uint32_t act = __ballot_sync(0xffffffffu, live);
-    if (live) {
-      const uint32_t peers = __match_any_sync(act, e);
-      if (lane == __ffs(peers) - 1) atomicAdd(&cnt[e], __popc(peers));
-    }
-  }
-  __syncthreads();
-  // segments and the item / unit tables (warp 0, lane-parallel scan)
-  if (threadIdx.x < 32) {
-    const uint32_t nmt = a.d / 128;
-    uint32_t rows = 0, tiles = 0, gu = 0, n_items = 0;
-    if (a.S) {
-      PfItem it{};
-      it.w = a.shared_w;
-      it.F = a.S;
-      it.row0 = 0;
-      it.n = a.N;
-      it.ntile = (a.N + kPfNt - 1) / kPfNt;
-      it.tile0 = 0;
-      it.gu0 = 0;
-      it.expert = 0xFFFFu;
-      if (lane == 0) a.items[0] = it;
-      rows = (a.N + 15) & ~15u;
-      tiles = it.ntile;
-      gu = it.ntile * (a.S / 128);
-      n_items = 1;
-    }
-    const uint64_t mask = a.ls->mask;
-    for (uint32_t e0 = 0; e0 < a.E; e0 += 32) {
-      const uint32_t e = e0 + lane;
-      const uint32_t c = e < a.E ? cnt[e] : 0u;
-      const uint32_t pr = (c + 15) & ~15u, nt = (c + kPfNt - 1) / kPfNt;
-      // exclusive prefix sums over the lanes (experts in ascending order)
-      uint32_t sr = pr, st = nt, sg = nt * (a.F / 128), si = c ? 1u : 0u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t vr = __shfl_up_sync(0xffffffffu, sr, o), vt = __shfl_up_sync(0xffffffffu, st, o);
-        const uint32_t vg = __shfl_up_sync(0xffffffffu, sg, o), vi = __shfl_up_sync(0xffffffffu, si, o);
-        if (lane >= o) { sr += vr; st += vt; sg += vg; si += vi; }
-      }
-      if (c) {
-        PfItem it{};
-        const bool res = (mask >> e) & 1ull;
-        it.w = res ? a.slot_base + (uint64_t)a.ls->slot_of[e] * a.expert_bytes : a.stage_base + (uint64_t)e * a.expert_bytes;
-        it.F = a.F;
-        it.row0 = rows + sr - pr;
-        it.n = c;
-        it.ntile = nt;
-        it.tile0 = tiles + st - nt;
-        it.gu0 = gu + sg - nt * (a.F / 128);
-        it.expert = e;
-        a.items[n_items + si - 1] = it;
-      }
-      if (e < a.E) base[e] = rows + sr - pr;
-      rows += __shfl_sync(0xffffffffu, sr, 31);
-      tiles += __shfl_sync(0xffffffffu, st, 31);
-      gu += __shfl_sync(0xffffffffu, sg, 31);
-      n_items += __shfl_sync(0xffffffffu, si, 31);
-    }
-    __syncwarp();
-    // down units after every gate_up unit, in item order
-    uint32_t dn = gu;
-    for (uint32_t i0 = 0; i0 < n_items; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const uint32_t v = i < n_items ? a.items[i].ntile * nmt : 0u;
-      uint32_t s = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += t;
-      }
-      if (i < n_items) a.items[i].dn0 = dn + s - v;
-      dn += __shfl_sync(0xffffffffu, s, 31);
-    }
-    if (lane == 0) {
-      *a.hdr = PfHdr{n_items, gu, dn - gu, rows, tiles};
-      s_rows = rows;
-    }
-  }
-  __syncthreads();
-  const uint32_t rows = s_rows;
-  // padding rows -1, shared rows = the tokens in order
-  for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) {
-    const bool sh = a.S && r < a.N;
-    a.slot_tok[r] = sh ? (int32_t)r : -1;
-    a.slot_w[r] = sh ? a.sgate[r] : 0.f;
-  }
-  __syncthreads();
-  // scatter: a warp's entries of one expert take consecutive slots (one atomic)
-  for (uint32_t i0 = threadIdx.x - lane; i0 < n; i0 += blockDim.x) {
+__global__ void __launch_bounds__(256) pf_scatter_kernel(const __grid_constant__ PfScatterArgs a) {
+  __shared__ uint32_t s_slot[32];
+  const int lane = lane_id(), warp = warp_id();
+  const uint32_t n = a.N * a.k, nvec = a.d / 8;
+  const uint32_t i0 = blockIdx.x * 32;
+  if (warp == 0) {
     const uint32_t i = i0 + lane;
     const bool live = i < n;
     const uint32_t e = live ? a.sel[i] : 0xFFu;
@@ -365,31 +398,31 @@ __global__ void __launch_bounds__(1024) pf_permute_kernel(const __grid_constant_
       const uint32_t peers = __match_any_sync(act, e);
       const int leader = __ffs(peers) - 1;
       uint32_t b = 0;
-      if (lane == leader) b = atomicAdd(&base[e], __popc(peers));
+      if (lane == leader) b = atomicAdd(&a.cursor[e], __popc(peers));
       b = __shfl_sync(peers, b, leader);
       const uint32_t slot = b + __popc(peers & ((1u << lane) - 1u));
-      a.slot_tok[slot] = (int32_t)(i / a.k);
       a.slot_w[slot] = a.wts[i];
       a.entry_slot[i] = (int32_t)slot;
+      s_slot[lane] = slot;
     }
   }
-}
-
-// ------------------------------------------------------------ gather
-// slot row r <- u[slot_tok[r]] (zero for padding), SW128: 16 B chunk c of
-// row r in K-block c / 8 at chunk position (c ^ r) % 8. One warp per row.
-__global__ void __launch_bounds__(256) pf_gather_kernel(const uint16_t* __restrict__ u, const int32_t* __restrict__ slot_tok,
-                                                        const PfHdr* __restrict__ hdr, unsigned char* __restrict__ xg,
-                                                        uint32_t d, uint32_t R) {
-  const uint32_t rows = hdr->rows, nvec = d / 8;
-  const int lane = lane_id();
-  for (uint32_t r = blockIdx.x * 8 + warp_id(); r < rows; r += gridDim.x * 8) {
-    const int32_t t = slot_tok[r];
-    const uint4* src = reinterpret_cast<const uint4*>(u + (size_t)(t < 0 ? 0 : t) * d);
-    for (uint32_t c = lane; c < nvec; c += 32) {
-      const uint4 v = t >= 0 ? __ldg(src + c) : make_uint4(0, 0, 0, 0);
-      const size_t off = (size_t)(c >> 3) * R * 128u + (r >> 3) * 1024u + (r & 7u) * 128u + (((c ^ r) & 7u) << 4);
-      *reinterpret_cast<uint4*>(xg + off) = v;
+  __syncthreads();
+  for (uint32_t j = warp; j < 32 && i0 + j < n; j += 8) {
+    const uint32_t r = s_slot[j];
+    const uint4* src = reinterpret_cast<const uint4*>(a.u + (size_t)((i0 + j) / a.k) * a.d);
+    for (uint32_t c0 = lane; c0 < nvec; c0 += 8 * 32) {
+      uint4 v[8];  // 8 independent loads in flight per lane
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q)
+        if (c0 + q * 32 < nvec) v[q] = __ldg(src + c0 + q * 32);
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q) {
+        const uint32_t c = c0 + q * 32;
+        if (c < nvec) {
+          const size_t off = (size_t)(c >> 3) * a.R * 128u + (r >> 3) * 1024u + (r & 7u) * 128u + (((c ^ r) & 7u) << 4);
+          *reinterpret_cast<uint4*>(a.xg + off) = v[q];
+        }
+      }
     }
   }
 }
@@ -465,11 +498,11 @@ __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_con
         for (uint32_t j = 1; j < hdr.n_items; ++j)
           if ((gu ? s_items[j].gu0 : s_items[j].dn0) <= unit) i = j;
         const PfItem& it = s_items[i];
-        const uint32_t q = unit - (gu ? it.gu0 : it.dn0), per = gu ? it.F / 128 : nmt;
+        const uint32_t q = unit - (gu ? it.gu0 : it.dn0);
         r.kind = gu ? 0u : 1u;
         r.item = i;
-        r.tile = q / per;
-        r.idx = q % per;
+        r.idx = q / it.ntile;  // token tiles innermost: a weight tile's re-reads hit L2
+        r.tile = q % it.ntile;
         r.nrows = min(kPfNt, it.n - r.tile * kPfNt);
         r.nt = (r.nrows + 15) & ~15u;
         {

@@ -1089,9 +1089,10 @@ struct moeb_stack {
   // one, uploading); a copy stream and its events.
   uint32_t pf_cap = 0, pf_R = 0, pf_tiles = 0;
   DevBuf<uint16_t> pf_u, pf_hid, pf_stage;
-  DevBuf<float> pf_scores, pf_wts, pf_sgate, pf_slot_w, pf_out;
+  DevBuf<float> pf_logits, pf_scores, pf_wts, pf_slot_w, pf_out;
   DevBuf<uint8_t> pf_sel;
-  DevBuf<int32_t> pf_slot_tok, pf_entry;
+  DevBuf<int32_t> pf_entry;
+  DevBuf<uint32_t> pf_cnt, pf_cursor;
   DevBuf<PfItem> pf_items;
   DevBuf<PfHdr> pf_hdr;
   DevBuf<uint32_t> pf_ctr;
@@ -1915,12 +1916,11 @@ static void prefill_alloc(moeb_stack* S, uint32_t N) {
     const uint32_t tiles = (N + kPfNt - 1) / kPfNt + (N * k + kPfNt - 1) / kPfNt + E;
     S->pf_u.alloc((size_t)N * d);
     S->pf_hid.alloc((size_t)2 * N * d);
+    S->pf_logits.alloc((size_t)N * (E + 1));
     S->pf_scores.alloc((size_t)N * E);
     S->pf_wts.alloc((size_t)N * k);
     S->pf_sel.alloc((size_t)N * k);
-    S->pf_sgate.alloc(N);
     S->pf_entry.alloc((size_t)N * k);
-    S->pf_slot_tok.alloc(R);
     S->pf_slot_w.alloc(R);
     S->pf_out.alloc((size_t)R * d);
     S->pf_xg.alloc((size_t)R * d * 2);
@@ -1929,6 +1929,11 @@ static void prefill_alloc(moeb_stack* S, uint32_t N) {
     S->pf_ctr.alloc(2 + tiles);
     S->pf_items.alloc(kMaxItems);
     S->pf_hdr.alloc(1);
+    if (!S->pf_cnt.p) {
+      S->pf_cnt.alloc(kMaxE + 1);  // histogram + the top-k kernel's ticket
+      S->pf_cnt.zero(s);
+      S->pf_cursor.alloc(kMaxE);
+    }
     S->pf_cap = N;
     S->pf_R = R;
     S->pf_tiles = tiles;
@@ -1942,7 +1947,7 @@ static void prefill_alloc(moeb_stack* S, uint32_t N) {
     MOEB_CUDA(cudaFuncSetAttribute(pf_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(kPfStages * kPfStageBytes + 1024)));
     MOEB_CUDA(cudaFuncSetAttribute(pf_router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(kPfRouterTok * (d + 8) * 2 + kPfRouterTok * E * 4)));
+                                   (int)(kPfRouterTok * (d + 8) * 2)));
   }
   if (S->rec_cap && N > S->pf_log_n) {
     const uint32_t L = S->L;
@@ -1962,14 +1967,21 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
   if (N == 0) throw Error(1, "prefill: no tokens");
   if (k > kPfMaxK) throw Error(1, "prefill: top_k > 16");
   prefill_alloc(S, N);
-  // the cache residency each layer's items read (the decode state is not changed)
-  MOEB_CUDA(cudaStreamSynchronize(s));
+  // the cache residency (which experts to upload): read once, unless every
+  // expert fits the cache and the initial fill put them all there (then
+  // nothing is ever evicted: no host sync)
+  const uint64_t all = E == 64 ? ~0ull : ((1ull << E) - 1);
   std::vector<LayerState> ls(L);
-  MOEB_CUDA(cudaMemcpy(ls.data(), S->layers.p, sizeof(LayerState) * L, cudaMemcpyDeviceToHost));
+  if (S->cfg.slots >= E && S->cfg.init_fill != 2) {
+    for (uint32_t l = 0; l < L; ++l) ls[l].mask = all;
+  } else {
+    MOEB_CUDA(cudaStreamSynchronize(s));
+    MOEB_CUDA(cudaMemcpy(ls.data(), S->layers.p, sizeof(LayerState) * L, cudaMemcpyDeviceToHost));
+  }
   const uint64_t eb = S->expert_elems * 2;
   bool any_up = false;
   for (uint32_t l = 0; l < L; ++l)
-    if (ls[l].mask != (E == 64 ? ~0ull : ((1ull << E) - 1))) any_up = true;
+    if (ls[l].mask != all) any_up = true;
   if (any_up && !S->pf_stage.p) S->pf_stage.alloc(2 * (size_t)E * S->expert_elems);
   uint64_t h2d = 0;
   std::vector<char> up(L, 0);
@@ -1993,7 +2005,7 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
   };
   int n_sm = 0;
   MOEB_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, S->device));
-  const size_t r_smem = (size_t)kPfRouterTok * (d + 8) * 2 + (size_t)kPfRouterTok * E * 4;
+  const size_t r_smem = (size_t)kPfRouterTok * (d + 8) * 2;
   const bool log = S->rec_cap != 0;
   if (any_up) upload(0);
   for (uint32_t l = 0; l < L; ++l) {
@@ -2009,46 +2021,60 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     ra.wg = S->gate_w.p + (size_t)l * E * d;
     ra.wsg = S->model.shared_gate ? S->sgate_w.p + (size_t)l * d : nullptr;
     ra.u = S->pf_u.p;
-    ra.scores = S->pf_scores.p;
-    ra.sel = S->pf_sel.p;
-    ra.wts = S->pf_wts.p;
-    ra.sgate = S->pf_sgate.p;
+    ra.xg = Sh ? S->pf_xg.p : nullptr;
+    ra.logits = S->pf_logits.p;
     ra.N = N;
     ra.d = d;
     ra.E = E;
-    ra.k = k;
-    ra.renormalize = S->model.renormalize;
-    ra.routed_scale = S->model.routed_scale;
-    pf_router_kernel<<<(N + kPfRouterTok - 1) / kPfRouterTok, 256, r_smem, s>>>(ra);
+    ra.R = S->pf_R;
+    pf_router_kernel<<<dim3((N + kPfRouterTok - 1) / kPfRouterTok, (E + 15) / 16), 256, r_smem, s>>>(ra);
     MOEB_CUDA(cudaGetLastError());
-    PfPermuteArgs pa{};
-    pa.sel = S->pf_sel.p;
-    pa.wts = S->pf_wts.p;
-    pa.sgate = S->pf_sgate.p;
-    pa.ls = S->layers.p + l;
-    pa.slot_base = reinterpret_cast<const unsigned char*>(S->slots.p + (size_t)l * S->slots_alloc * S->expert_elems);
-    pa.stage_base = S->pf_stage.p ? reinterpret_cast<const unsigned char*>(S->pf_stage.p) + (size_t)(l % 2) * E * eb
+    PfTopkArgs ta{};
+    ta.logits = S->pf_logits.p;
+    ta.scores = S->pf_scores.p;
+    ta.sel = S->pf_sel.p;
+    ta.wts = S->pf_wts.p;
+    ta.slot_w = Sh ? S->pf_slot_w.p : nullptr;
+    ta.cnt = S->pf_cnt.p;
+    ta.N = N;
+    ta.E = E;
+    ta.k = k;
+    ta.renormalize = S->model.renormalize;
+    ta.shared_gate = S->model.shared_gate;
+    ta.routed_scale = S->model.routed_scale;
+    ta.plan.cnt = S->pf_cnt.p;
+    ta.plan.cursor = S->pf_cursor.p;
+    ta.plan.ls = S->layers.p + l;
+    ta.plan.slot_base = reinterpret_cast<const unsigned char*>(S->slots.p + (size_t)l * S->slots_alloc * S->expert_elems);
+    ta.plan.stage_base = S->pf_stage.p ? reinterpret_cast<const unsigned char*>(S->pf_stage.p) + (size_t)(l % 2) * E * eb
                                   : nullptr;
-    pa.shared_w = Sh ? reinterpret_cast<const unsigned char*>(S->shared_w.p + (size_t)l * 3 * Sh * d) : nullptr;
-    pa.expert_bytes = eb;
-    pa.N = N;
-    pa.k = k;
-    pa.E = E;
-    pa.d = d;
-    pa.F = F;
-    pa.S = Sh;
-    pa.items = S->pf_items.p;
-    pa.hdr = S->pf_hdr.p;
-    pa.slot_tok = S->pf_slot_tok.p;
-    pa.slot_w = S->pf_slot_w.p;
-    pa.entry_slot = S->pf_entry.p;
-    pa.R = S->pf_R;
-    pf_permute_kernel<<<1, 1024, 0, s>>>(pa);
+    ta.plan.shared_w = Sh ? reinterpret_cast<const unsigned char*>(S->shared_w.p + (size_t)l * 3 * Sh * d) : nullptr;
+    ta.plan.expert_bytes = eb;
+    ta.plan.N = N;
+    ta.plan.E = E;
+    ta.plan.d = d;
+    ta.plan.F = F;
+    ta.plan.S = Sh;
+    ta.plan.items = S->pf_items.p;
+    ta.plan.hdr = S->pf_hdr.p;
+    ta.ticket = S->pf_cnt.p + kMaxE;
+    pf_topk_kernel<<<(N + 7) / 8, 256, 0, s>>>(ta);
+    MOEB_CUDA(cudaGetLastError());
+    PfScatterArgs sa{};
+    sa.sel = S->pf_sel.p;
+    sa.wts = S->pf_wts.p;
+    sa.u = S->pf_u.p;
+    sa.cursor = S->pf_cursor.p;
+    sa.slot_w = S->pf_slot_w.p;
+    sa.entry_slot = S->pf_entry.p;
+    sa.xg = S->pf_xg.p;
+    sa.N = N;
+    sa.k = k;
+    sa.d = d;
+    sa.R = S->pf_R;
+    pf_scatter_kernel<<<(N * k + 31) / 32, 256, 0, s>>>(sa);
     MOEB_CUDA(cudaGetLastError());
     MOEB_CUDA(cudaMemsetAsync(S->pf_ctr.p, 0, S->pf_ctr.n * sizeof(uint32_t), s));
-    pf_gather_kernel<<<(unsigned)std::min<uint64_t>((S->pf_R + 7) / 8, (uint64_t)n_sm * 16), 256, 0, s>>>(
-        S->pf_u.p, S->pf_slot_tok.p, S->pf_hdr.p, S->pf_xg.p, d, S->pf_R);
-    MOEB_CUDA(cudaGetLastError());
     PfGemmArgs ga{};
     ga.items = S->pf_items.p;
     ga.hdr = S->pf_hdr.p;
