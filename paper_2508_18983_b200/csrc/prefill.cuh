@@ -199,6 +199,7 @@ struct PfPlanArgs {
   const unsigned char* slot_base;   // this layer's cache slots
   const unsigned char* stage_base;  // staging of the non-resident experts (by expert id)
   const unsigned char* shared_w;    // shared expert (null: none)
+  const unsigned char* tiled_base;  // non-null: every routed expert re-tiled here (by expert id)
   uint64_t expert_bytes;
   uint32_t N, E, d, F, S;
   PfItem* items;
@@ -240,7 +241,9 @@ __device__ void pf_plan_warp(const PfPlanArgs& a) {
     if (c) {
       PfItem it{};
       const bool res = (mask >> e) & 1ull;
-      it.w = res ? a.slot_base + (uint64_t)a.ls->slot_of[e] * a.expert_bytes : a.stage_base + (uint64_t)e * a.expert_bytes;
+      it.w = a.tiled_base ? a.tiled_base + (uint64_t)e * a.expert_bytes
+             : res        ? a.slot_base + (uint64_t)a.ls->slot_of[e] * a.expert_bytes
+                          : a.stage_base + (uint64_t)e * a.expert_bytes;
       it.F = a.F;
       it.row0 = rows + sr - pr;
       it.n = c;
@@ -423,6 +426,68 @@ __global__ void __launch_bounds__(256) pf_scatter_kernel(const __grid_constant__
           *reinterpret_cast<uint4*>(a.xg + off) = v[q];
         }
       }
+    }
+  }
+}
+
+// ------------------------------------------------------------ re-tiling
+// Batch-1 stacks keep experts row-interleaved ([F][3][d], the split-K GEMV's
+// layout); prefill re-tiles each layer's experts into the UMMA layout
+// (weights.cuh tiled_coords) through HBM first. One CTA per 16 KB tile:
+// gate / up tiles are row copies with the SW128 chunk swizzle; down tiles
+// (128 outputs x 64 intermediate rows, K = intermediate) are transposed
+// through shared memory. blockIdx.y = expert (gridDim.y - 1 = the shared
+// expert when shared_src is set); a routed expert's source is its cache slot
+// when resident, else the staging area.
+struct PfRetileArgs {
+  const LayerState* ls;
+  const unsigned char* slot_base;
+  const unsigned char* stage_base;
+  const unsigned char* shared_src;  // shared expert (rows layout) or null
+  unsigned char* dst;               // [E][expert_bytes] then the shared expert
+  uint64_t expert_bytes;
+  uint32_t E, d, F, S;
+};
+
+__global__ void __launch_bounds__(256) pf_retile_kernel(const __grid_constant__ PfRetileArgs a) {
+  __shared__ __align__(16) uint16_t tr[64][128 + 8];
+  const uint32_t e = blockIdx.y, d = a.d;
+  const bool sh = a.shared_src && e == a.E;
+  const uint32_t F = sh ? a.S : a.F;
+  const uint32_t n_gu = (F / 128) * (d / 64) * 2, n_dn = (d / 128) * (F / 64);
+  if (blockIdx.x >= n_gu + n_dn) return;
+  const unsigned char* src;
+  if (sh) {
+    src = a.shared_src;
+  } else {
+    const bool res = (a.ls->mask >> e) & 1ull;
+    src = res ? a.slot_base + (uint64_t)a.ls->slot_of[e] * a.expert_bytes : a.stage_base + (uint64_t)e * a.expert_bytes;
+  }
+  const uint16_t* w = reinterpret_cast<const uint16_t*>(src);
+  unsigned char* dst = a.dst + (uint64_t)e * a.expert_bytes + (uint64_t)blockIdx.x * kUmBlk;
+  if (blockIdx.x < n_gu) {
+    // gate_up tile (unit u, K-block kb, gate|up): out row rr = F-row u*128 + rr
+    const uint32_t t = blockIdx.x, which = t & 1, kb = (t >> 1) % (d / 64), u = (t >> 1) / (d / 64);
+    for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) {
+      const uint32_t rr = i >> 3, j = i & 7;
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(w + (size_t)(u * 128 + rr) * 3 * d + which * d + kb * 64 + 8 * j));
+      *reinterpret_cast<uint4*>(dst + sw128_off(rr, 8 * j)) = v;
+    }
+  } else {
+    // down tile (output unit mt, K-block kb): element (m, r) = down column r, entry m
+    const uint32_t t = blockIdx.x - n_gu, kb = t % (F / 64), mt = t / (F / 64);
+    for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) {
+      const uint32_t r = i >> 4, j = i & 15;
+      *reinterpret_cast<uint4*>(&tr[r][8 * j]) =
+          __ldg(reinterpret_cast<const uint4*>(w + (size_t)(kb * 64 + r) * 3 * d + 2 * d + mt * 128 + 8 * j));
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < 1024; i += blockDim.x) {
+      const uint32_t m = i >> 3, j = i & 7;
+      uint32_t o[4];
+#pragma unroll
+      for (uint32_t q = 0; q < 4; ++q) o[q] = (uint32_t)tr[8 * j + 2 * q][m] | ((uint32_t)tr[8 * j + 2 * q + 1][m] << 16);
+      *reinterpret_cast<uint4*>(dst + sw128_off(m, 8 * j)) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }

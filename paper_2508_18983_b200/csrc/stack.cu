@@ -1088,7 +1088,7 @@ struct moeb_stack {
   // non-resident experts of two layers (the layer being computed and the next
   // one, uploading); a copy stream and its events.
   uint32_t pf_cap = 0, pf_R = 0, pf_tiles = 0;
-  DevBuf<uint16_t> pf_u, pf_hid, pf_stage;
+  DevBuf<uint16_t> pf_u, pf_hid, pf_stage, pf_tiled;
   DevBuf<float> pf_logits, pf_scores, pf_wts, pf_slot_w, pf_out;
   DevBuf<uint8_t> pf_sel;
   DevBuf<int32_t> pf_entry;
@@ -1961,9 +1961,9 @@ static void prefill_alloc(moeb_stack* S, uint32_t N) {
 
 static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N, cudaStream_t s) {
   const uint32_t L = S->L, E = S->E, k = S->cfg.top_k, d = S->d, F = S->F, Sh = S->S;
-  if (!S->umma)
-    throw Error(1, "prefill needs the UMMA-tiled expert layout (a stack with max_batch 2..32, ffn and "
-                   "shared_ffn multiples of 128)");
+  if (!S->umma && !(S->splitk && F % 128 == 0 && Sh % 128 == 0))
+    throw Error(1, "prefill needs the UMMA-tiled expert layout (max_batch 2..32) or the row-interleaved one "
+                   "(batch 1, d_model <= 2048), with ffn and shared_ffn multiples of 128");
   if (N == 0) throw Error(1, "prefill: no tokens");
   if (k > kPfMaxK) throw Error(1, "prefill: top_k > 16");
   prefill_alloc(S, N);
@@ -1983,6 +1983,10 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
   for (uint32_t l = 0; l < L; ++l)
     if (ls[l].mask != all) any_up = true;
   if (any_up && !S->pf_stage.p) S->pf_stage.alloc(2 * (size_t)E * S->expert_elems);
+  // batch-1 stacks: experts are row-interleaved; every layer is re-tiled
+  // into one buffer (routed experts by id, then the shared expert)
+  const bool retile = !S->umma;
+  if (retile && !S->pf_tiled.p) S->pf_tiled.alloc((size_t)E * S->expert_elems + (size_t)3 * Sh * d);
   uint64_t h2d = 0;
   std::vector<char> up(L, 0);
   auto upload = [&](uint32_t l) {
@@ -2049,6 +2053,8 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     ta.plan.stage_base = S->pf_stage.p ? reinterpret_cast<const unsigned char*>(S->pf_stage.p) + (size_t)(l % 2) * E * eb
                                   : nullptr;
     ta.plan.shared_w = Sh ? reinterpret_cast<const unsigned char*>(S->shared_w.p + (size_t)l * 3 * Sh * d) : nullptr;
+    ta.plan.tiled_base = retile ? reinterpret_cast<const unsigned char*>(S->pf_tiled.p) : nullptr;
+    if (retile && Sh) ta.plan.shared_w = reinterpret_cast<const unsigned char*>(S->pf_tiled.p + (size_t)E * S->expert_elems);
     ta.plan.expert_bytes = eb;
     ta.plan.N = N;
     ta.plan.E = E;
@@ -2075,6 +2081,22 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     pf_scatter_kernel<<<(N * k + 31) / 32, 256, 0, s>>>(sa);
     MOEB_CUDA(cudaGetLastError());
     MOEB_CUDA(cudaMemsetAsync(S->pf_ctr.p, 0, S->pf_ctr.n * sizeof(uint32_t), s));
+    if (retile) {
+      PfRetileArgs rt{};
+      rt.ls = S->layers.p + l;
+      rt.slot_base = ta.plan.slot_base;
+      rt.stage_base = ta.plan.stage_base;
+      rt.shared_src = Sh ? reinterpret_cast<const unsigned char*>(S->shared_w.p + (size_t)l * 3 * Sh * d) : nullptr;
+      rt.dst = reinterpret_cast<unsigned char*>(S->pf_tiled.p);
+      rt.expert_bytes = eb;
+      rt.E = E;
+      rt.d = d;
+      rt.F = F;
+      rt.S = Sh;
+      const uint32_t Fm = std::max(F, Sh), tiles = (Fm / 128) * (d / 64) * 2 + (d / 128) * (Fm / 64);
+      pf_retile_kernel<<<dim3(tiles, E + (Sh ? 1 : 0)), 256, 0, s>>>(rt);
+      MOEB_CUDA(cudaGetLastError());
+    }
     PfGemmArgs ga{};
     ga.items = S->pf_items.p;
     ga.hdr = S->pf_hdr.p;

@@ -13,7 +13,8 @@ Per layer, from the prefill log:
   * the residual chain: layer l+1's input = bf16(x_l + y_l) bit-exact, and
     the returned hidden is the last layer's.
 Also: bitwise-reproducible outputs, the decode state untouched, uploads of
-exactly the non-resident experts, and the tiled-layout requirement.
+exactly the non-resident experts, batch-1 (row-interleaved) stacks through
+the re-tiling pass, and the shape requirement.
 """
 import numpy as np
 import pytest
@@ -76,6 +77,9 @@ CASES = {
     "mixtral_like_renorm_no_shared": (2, 8, 2, 2, 256, 256, 0, 2, 200, 0, 1),
     "all_resident": (2, 16, 4, 2, 256, 128, 256, 16, 64, 0, 0),
     "zero_slots": (1, 16, 4, 2, 256, 128, 256, 0, 50, 0, 0),
+    # batch-1 stacks keep experts row-interleaved (split-K decode): prefill re-tiles them
+    "dsv2_like_b1_rows": (2, 16, 4, 1, 256, 128, 256, 4, 77, 0, 0),
+    "qwen_like_b1_rows": (2, 60, 4, 1, 512, 128, 512, 15, 40, 1, 0),
 }
 
 
@@ -103,12 +107,14 @@ def test_prefill_reproducible_and_decode_state_untouched(gpu):
     st.close()
 
 
-def test_prefill_dsv2_lite_full_width(gpu):
+@pytest.mark.parametrize("B", [1, 2])
+def test_prefill_dsv2_lite_full_width(gpu, B):
     """DeepSeek-V2-Lite widths (64 experts top-6, 2 shared, d 2048, ffn 1408),
-    2 layers, a 512-token prompt, cache 16/64: every layer's scores and
-    selections for all tokens, outputs of 48 tokens against the oracle."""
+    2 layers, a 512-token prompt, cache 16/64, on a batch-1 (re-tiled) and a
+    batched stack: every layer's scores and selections for all tokens,
+    outputs of 48 tokens against the oracle."""
     import torch
-    L, E, k, B, d, F, S, slots, N = 2, 64, 6, 2, 2048, 1408, 2816, 16, 512
+    L, E, k, d, F, S, slots, N = 2, 64, 6, 2048, 1408, 2816, 16, 512
     st, x, y, up = _run(gpu, torch, L, E, k, B, d, F, S, slots, N)
     assert up == L * 48 * 3 * F * d * 2
     rng = np.random.default_rng(0)
@@ -116,10 +122,10 @@ def test_prefill_dsv2_lite_full_width(gpu):
     st.close()
 
 
-def test_prefill_needs_tiled_layout(gpu):
+def test_prefill_needs_128_multiple_ffn(gpu):
     import torch
     cfg = gpu.Config.make(num_layers=1, experts=16, top_k=4, batch=1, slots=4)
-    st = gpu.Stack(cfg, 256, 128, 256, weight_seed=1)  # batch 1: row-interleaved experts (split-K)
+    st = gpu.Stack(cfg, 256, 64, 256, weight_seed=1)  # ffn 64: no tensor-core tiling
     x = torch.zeros(4, 256, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(gpu.MoebError) as ei:
         st.prefill(x.data_ptr(), x.data_ptr(), 4)

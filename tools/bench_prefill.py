@@ -115,6 +115,8 @@ def main():
     ap.add_argument("--capped-tokens", default="512")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cpu-tokens", type=int, default=512)
+    ap.add_argument("--rows", type=int, default=512, help="also time a batch-1 (row-interleaved, re-tiled) "
+                    "capped stack at this N (0: skip)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     import torch
@@ -161,6 +163,21 @@ def main():
         print(json.dumps({f"capped N{N}": out["capped"][f"N{N}"]}), flush=True)
     full.close()
     capped.close()
+    if args.rows:
+        # the headline decode stack (batch 1: split-K layout), prefill through the re-tiling pass
+        N = args.rows
+        rows = capi.Stack(capi.Config.make(num_layers=L, experts=E, top_k=K, batch=1, slots=16), weight_seed=7,
+                          **model)
+        ms, up = time_prefill(torch, rows, xall[:N], y[:N], N, 2)
+        wb, fl, t_hbm, t_tc = roofline(N, L * E, hbm, tflops)
+        t_pcie = up / (bw_pcie * 1e9) * 1e3
+        t_roof = max(t_hbm, t_tc, t_pcie)
+        out["capped_batch1_stack"] = {
+            "N": N, "ttft_ms": round(ms, 3), "tokens_per_s": round(N / (ms * 1e-3), 1), "upload_gb": round(up / 1e9, 3),
+            "roofline": {"t_roof_ms": round(t_roof, 3), "bound": "pcie" if t_pcie >= max(t_hbm, t_tc) else "hbm",
+                         "frac": round(t_roof / ms, 4)}}
+        print(json.dumps({"capped_batch1_stack": out["capped_batch1_stack"]}), flush=True)
+        rows.close()
     if args.cpu_tokens:
         nthreads = os.cpu_count() or 1
         ms, gbs = cpu_prefill_ms(args.cpu_tokens, nthreads)
