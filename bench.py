@@ -630,6 +630,8 @@ def run_ours(args):
     }
     if abl:
         result["ablation"] = abl
+    if world == 1 and not args.no_prefill:
+        result["prefill"] = prefill_section(torch, stack, d, pcie_peak, hbm_peak)
     if not args.no_c5:
         # C5: 64 requests stream-partitioned over the world's GPUs at the
         # largest batch the partition allows (B <= 64 / G, <= 32)
@@ -652,6 +654,39 @@ def run_ours(args):
         print(json.dumps(result), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def prefill_section(torch, stack, d, pcie_peak, hbm_peak, N=512, reps=2):
+    """Prefill (moeb_prefill) of an N-token prompt on the bench's own stack
+    (batch 1, cache 16/64: experts re-tiled per layer, the 48 non-resident
+    experts of every layer uploaded while the previous layer computes): TTFT
+    with CUDA events on the stream, against the PCIe path roofline."""
+    g = torch.Generator().manual_seed(11)
+    x = (torch.randn(N, d, generator=g) * 2).to(torch.bfloat16).cuda()
+    y = torch.empty_like(x)
+    s = torch.cuda.Stream()
+    stack.prefill(x.data_ptr(), y.data_ptr(), N, stream=s.cuda_stream)  # warm-up: buffers
+    torch.cuda.synchronize()
+    ts, up = [], 0
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        up = stack.prefill(x.data_ptr(), y.data_ptr(), N, stream=s.cuda_stream)
+        e1.record(s)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = min(ts)
+    L, E = CFG["num_layers"], CFG["experts"]
+    wbytes = L * (E * d * 2 + 3 * MODEL["shared_ffn"] * d * 2) + L * E * 3 * MODEL["ffn"] * d * 2
+    # the PCIe peak: the bench's probe, or this run's own large-copy rate if higher
+    bw = max(pcie_peak, up / (ms * 1e-3) / 1e9)
+    t_roof = max(up / (bw * 1e9), wbytes / (hbm_peak * 1e9)) * 1e3
+    return {"tokens": N, "ttft_ms": round(ms, 2), "tokens_per_s": round(N / (ms * 1e-3), 1),
+            "upload_gb": round(up / 1e9, 3), "pcie_achieved_gbs": round(up / (ms * 1e-3) / 1e9, 2),
+            "path_roofline": {"t_roof_ms": round(t_roof, 2), "frac": round(t_roof / ms, 4), "bound": "pcie",
+                              "pcie_peak_gbs": round(bw, 2)},
+            "note": "plain top-k routing, grouped tcgen05 GEMM; tools/bench_prefill.py for the all-resident "
+                    "(HBM / tensor-bound) numbers"}
 
 
 # ----------------------------------------------------------------- CPU path
@@ -809,6 +844,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-ablation", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the batched (config C5) tensor-core FFN section")
     ap.add_argument("--cpu-sample-tokens", type=int, default=12)
