@@ -71,6 +71,10 @@ public:
     // Asynchronous on `stream` (a cudaStream_t; nullptr = the stack's own).
     void step(const void* x, void* y, std::uint32_t batch, void* stream = nullptr);
     void sync();
+    // Prefill (prompt pass) of n_tokens tokens through all layers: x, y device
+    // bf16 [n_tokens][d_model]. Plain top-k routing, the decode state is not
+    // changed (moeb_prefill). Returns the bytes uploaded from the pinned pool.
+    std::uint64_t prefill(const void* x, void* y, std::uint32_t n_tokens, void* stream = nullptr);
     void reset();
 
     Metrics metrics() const;

@@ -57,6 +57,12 @@ void MoeStack::step(const void* x, void* y, std::uint32_t batch, void* stream) {
 
 void MoeStack::sync() { throw_status(moeb_sync(h_)); }
 
+std::uint64_t MoeStack::prefill(const void* x, void* y, std::uint32_t n_tokens, void* stream) {
+    std::uint64_t bytes = 0;
+    throw_status(moeb_prefill(h_, x, y, n_tokens, stream, &bytes));
+    return bytes;
+}
+
 void MoeStack::reset() { throw_status(moeb_reset(h_)); }
 
 Metrics MoeStack::metrics() const {

@@ -9,6 +9,7 @@
 //   moe_stack_main L E k B d F S slots T [er] [ba]
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -108,6 +109,35 @@ int main(int argc, char** argv) {
                     (unsigned long long)m.total_time, m.stage.c_str());
         cudaFree(x);
         cudaFree(y);
+        // prefill of a 40-token prompt: the uploads of the non-resident
+        // experts, bitwise-reproducible hidden outputs, decisions unchanged
+        if (F % 128 == 0 && S % 128 == 0) {
+            const std::uint32_t N = 40;
+            void *px = nullptr, *py0 = nullptr, *py1 = nullptr;
+            cudaMalloc(&px, (size_t)N * d * 2);
+            cudaMalloc(&py0, (size_t)N * d * 2);
+            cudaMalloc(&py1, (size_t)N * d * 2);
+            std::vector<std::uint16_t> hx((size_t)N * d);
+            for (size_t i = 0; i < hx.size(); ++i) hx[i] = (std::uint16_t)(0x3c00u + (i * 2654435761u >> 20) % 512u);
+            cudaMemcpy(px, hx.data(), hx.size() * 2, cudaMemcpyHostToDevice);
+            const std::uint64_t up = st.prefill(px, py0, N);
+            st.prefill(px, py1, N);
+            st.sync();
+            std::vector<std::uint16_t> a(hx.size()), b(hx.size());
+            cudaMemcpy(a.data(), py0, a.size() * 2, cudaMemcpyDeviceToHost);
+            cudaMemcpy(b.data(), py1, b.size() * 2, cudaMemcpyDeviceToHost);
+            const bool same = a == b, decisions_kept = st.decisions().size() == dec.size();
+            std::fprintf(stderr, "prefill h2d %llu reproducible %d decisions_kept %d\n", (unsigned long long)up,
+                         (int)same, (int)decisions_kept);
+            cudaFree(px);
+            cudaFree(py0);
+            cudaFree(py1);
+            const std::uint64_t want = (std::uint64_t)L * (E - std::min(slots, E)) * 3ull * F * d * 2;
+            if (up != want || !same || !decisions_kept) {
+                std::fprintf(stderr, "prefill check failed (want %llu)\n", (unsigned long long)want);
+                return 1;
+            }
+        }
         // the reference's exception types come back through the wrapper
         try {
             SimConfig bad = cfg;

@@ -5,7 +5,9 @@ decisions it returns in the reference's RouteResult / load-list vocabulary,
 replayed by the oracle on the router scores the device used, are bit-exact;
 Metrics agree; pending is the reference's kept-low-and-not-resident set
 (router.cpp:150, 250-258); a bad config raises ConfigError through the
-wrapper (the program checks that itself)."""
+wrapper, and MoeStack::prefill uploads exactly the non-resident experts and
+returns bitwise-reproducible outputs without touching the decisions (the
+program checks these itself)."""
 import json
 import os
 import subprocess
