@@ -1,5 +1,6 @@
 """A small stack (B = 1 split-K and B = 2 tcgen05 FFN) for compute-sanitizer runs
-(tools/gpu_sanitize.sh): the stack detects the tool and runs in serial mode."""
+(tools/gpu_sanitize.sh): the stack detects the tool and runs in serial mode.
+Each stack also runs a prefill of 150 tokens (re-tiled for B = 1)."""
 import sys, torch
 sys.path.insert(0, ".")
 from paper_2508_18983_b200 import capi
@@ -12,5 +13,9 @@ for B, F, S in ((1, 128, 256), (2, 128, 256)):
     for i in range(6):
         st.step(x[i].data_ptr(), y.data_ptr(), B)
     st.sync()
-    print("B", B, "ok", st.metrics()["hits"])
+    xp = torch.randn(150, 256).to(torch.bfloat16).cuda()
+    yp = torch.empty_like(xp)
+    up = st.prefill(xp.data_ptr(), yp.data_ptr(), 150)
+    st.sync()
+    print("B", B, "ok", st.metrics()["hits"], "prefill uploaded", up)
     st.close()
