@@ -247,6 +247,17 @@ int moeb_step(moeb_stack* s, const void* x, void* y, uint32_t B, void* stream);
  * h2d_bytes (nullable) = bytes uploaded. */
 int moeb_prefill(moeb_stack* s, const void* x, void* y, uint32_t n_tokens, void* stream,
                  uint64_t* h2d_bytes);
+/* Expert tier: upload each (layer, expert) from a
+ * device pointer — a peer GPU's HBM over NVLink (peer access is enabled
+ * here; across processes, map the peer's allocation with CUDA IPC first), or
+ * this GPU's — instead of the pinned host pool. ptrs: [L*E], each pointing to
+ * that expert's weights in this stack's pool layout (moeb_host_pool_flags);
+ * NULL restores the host pool. Call between steps (synchronises the device).
+ * Decisions are unchanged; only where the upload bytes come from. Copies
+ * between device memories run as SM kernels, which cannot start beside the
+ * persistent FFN grid, so a device tier puts the stack's uploads in serial
+ * mode (the compute stream waits for each step's uploads before its FFN). */
+int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n);
 /* MOEB_MODEL_LOG_STEPS: the last prefill's layer `layer`: input hidden
  * (bf16 [N][d]), router scores (fp32 [N][E]), selections in rank order
  * (uint8 [N][k]) and fp32 layer output before the residual ([N][d]); every

@@ -348,6 +348,15 @@ class Stack:
                                  C.c_void_p(stream), C.byref(b)))
         return b.value
 
+    def set_expert_sources(self, ptrs):
+        """Upload each (layer, expert) from a device pointer (a peer GPU's HBM or
+        this one's) instead of the pinned host pool; None restores the pool."""
+        if ptrs is None:
+            check(lib().moeb_set_expert_sources(self.h, None, C.c_size_t(0)))
+            return
+        arr = (C.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+        check(lib().moeb_set_expert_sources(self.h, arr, C.c_size_t(len(ptrs))))
+
     def prefill_log(self, layer):
         """The last prefill's layer `layer` (MOEB_MODEL_LOG_STEPS): input hidden (bf16 bits
         [N, d]), router scores [N, E], selections [N, k] and the fp32 layer output [N, d]."""

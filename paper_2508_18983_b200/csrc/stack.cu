@@ -1105,7 +1105,7 @@ struct moeb_stack {
   DevBuf<uint16_t> pf_log_x;
   DevBuf<float> pf_log_scores, pf_log_y;
   DevBuf<uint8_t> pf_log_sel;
-  bool serial = false;
+  bool serial = false, serial_at_create = false;
   uint32_t serial_need = 0;  // highest upload id the next FFN may depend on
   uint64_t n_launch_layers = 0;        // (gate+decide, FFN) launch pairs
   std::mutex io_mu;
@@ -1175,6 +1175,15 @@ struct moeb_stack {
   }
 
   // one upload: the copy, then copies_done := id (the FFN waits on it)
+  // Expert sources (moeb_set_expert_sources): per (layer, expert) a device
+  // pointer to the expert's weights in some GPU's HBM (a peer GPU's over
+  // NVLink, or this one's) instead of the pinned host pool. Empty: host pool.
+  std::vector<const char*> src_tab;
+  const char* upload_src(uint64_t src_off) const {
+    if (src_tab.empty()) return reinterpret_cast<const char*>(pool) + src_off;
+    const uint64_t eb = expert_elems * 2;
+    return src_tab[src_off / eb] + src_off % eb;
+  }
   void issue_upload(const MailCmd& c, CUdeviceptr done_ptr) {
     // submit first, account after: the copy's start is what the GPU waits for
     const int ei = ev_next;
@@ -1184,9 +1193,8 @@ struct moeb_stack {
       harvest(ei);
     }
     cudaEventRecord(ev_a[ei], copy_stream);
-    const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(c.dst),
-                                           reinterpret_cast<const char*>(pool) + c.src_off, c.bytes,
-                                           cudaMemcpyHostToDevice, copy_stream);
+    const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(c.dst), upload_src(c.src_off), c.bytes,
+                                           cudaMemcpyDefault, copy_stream);
     if (p_write32(copy_stream, done_ptr, c.id, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
       copier_msg = "cuStreamWriteValue32 failed";
       copier_error = 5;
@@ -1218,9 +1226,8 @@ struct moeb_stack {
       harvest(ei);
     }
     cudaEventRecord(ev_a[ei], copy_stream);
-    const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(j.dst + off),
-                                           reinterpret_cast<const char*>(pool) + j.src_off + off, n,
-                                           cudaMemcpyHostToDevice, copy_stream);
+    const cudaError_t ce = cudaMemcpyAsync(reinterpret_cast<void*>(j.dst + off), upload_src(j.src_off + off), n,
+                                           cudaMemcpyDefault, copy_stream);
     cudaEventRecord(ev_b[ei], copy_stream);
     if (ce != cudaSuccess) {
       copier_msg = std::string("speculative upload failed: ") + cudaGetErrorString(ce);
@@ -1652,7 +1659,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   // the speculative start the FFN runs beside the deciding CTA, so one SM
   // is left to it
   S->ffn_grid = S->spec ? sms - 1 : sms;
-  S->serial = serial_mode_requested();
+  S->serial = S->serial_at_create = serial_mode_requested();
   // speculative uploads (opt-in, MOEB_SPEC_UPLOAD=1): the split-K (batch-1)
   // path with stage Pre and a capped cache; not in serial (profiler) mode.
   // Measured on the bench workload: 9.91 vs 7.86 ms/token without — half the
@@ -1998,9 +2005,12 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
         continue;
       }
       uint32_t e1 = e;
-      while (e1 < E && !((ls[l].mask >> e1) & 1ull)) ++e1;  // a run of non-resident experts: one copy
-      MOEB_CUDA(cudaMemcpyAsync(dst + (size_t)e * eb, src + (size_t)e * eb, (size_t)(e1 - e) * eb,
-                                cudaMemcpyHostToDevice, S->pf_copy));
+      // a run of non-resident experts: one copy from the host pool (per expert
+      // from a device tier, moeb_set_expert_sources)
+      while (e1 < E && !((ls[l].mask >> e1) & 1ull) && (e1 == e || S->src_tab.empty())) ++e1;
+      MOEB_CUDA(cudaMemcpyAsync(dst + (size_t)e * eb, S->src_tab.empty() ? static_cast<const void*>(src + (size_t)e * eb)
+                                                                         : S->upload_src(((uint64_t)l * E + e) * eb),
+                                (size_t)(e1 - e) * eb, cudaMemcpyDefault, S->pf_copy));
       h2d += (uint64_t)(e1 - e) * eb;
       up[l] = 1;
       e = e1;
@@ -2410,6 +2420,44 @@ int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n) {
     const size_t have = (size_t)std::min<uint64_t>(s->host_seq, 16384) * kTlWords;
     *n = have;
     if (out) MOEB_CUDA(cudaMemcpy(out, s->timeline.p, std::min(cap, have) * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n) {
+  return guarded([&] {
+    MOEB_CUDA(cudaSetDevice(s->device));
+    MOEB_CUDA(cudaDeviceSynchronize());  // no upload in flight while the table changes
+    if (!ptrs) {
+      std::lock_guard<std::mutex> g(s->io_mu);
+      s->src_tab.clear();
+      s->serial = s->serial_at_create;
+      return;
+    }
+    if (n != (size_t)s->L * s->E) throw Error(1, "expert sources: need one pointer per (layer, expert)");
+    std::vector<const char*> tab(n);
+    for (size_t i = 0; i < n; ++i) {
+      cudaPointerAttributes at{};
+      MOEB_CUDA(cudaPointerGetAttributes(&at, ptrs[i]));
+      if (at.type != cudaMemoryTypeDevice) throw Error(1, "expert sources: every pointer must be device memory");
+      if (at.device != s->device) {
+        int ok = 0;
+        MOEB_CUDA(cudaDeviceCanAccessPeer(&ok, s->device, at.device));
+        if (!ok) throw Error(1, "expert sources: no peer access to device " + std::to_string(at.device));
+        const cudaError_t pe = cudaDeviceEnablePeerAccess(at.device, 0);
+        if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) MOEB_CUDA(pe);
+        cudaGetLastError();
+      }
+      tab[i] = static_cast<const char*>(ptrs[i]);
+    }
+    std::lock_guard<std::mutex> g(s->io_mu);
+    s->src_tab = std::move(tab);
+    // Copies between device memories run as SM copy kernels (measured: a
+    // device-to-device cudaMemcpyAsync does not progress beside the persistent
+    // FFN grid, which leaves no room on any SM), so an FFN spinning on such an
+    // upload would wait for a copy that cannot start: with a device tier the
+    // stack orders uploads on the host (serial mode: the compute stream waits
+    // for the copy before the FFN launch).
+    s->serial = true;
   });
 }
 

@@ -49,8 +49,9 @@ def split(shape):
     return cfg, model
 
 
-def run_case(capi, torch, cfg_d, model_d, T, K, hbm_peak, pcie_peak, pool=None, seed=7):
-    """Decode a T-token stream, time its last K steps. Returns (row, stack)."""
+def run_case(capi, torch, cfg_d, model_d, T, K, hbm_peak, pcie_peak, pool=None, seed=7, setup=None):
+    """Decode a T-token stream, time its last K steps. Returns (row, stack).
+    setup(stack), if given, runs before the first step."""
     L, E, B, d = cfg_d["num_layers"], cfg_d["experts"], cfg_d["batch"], model_d["d_model"]
     scores = capi.generate_trace(L, E, B, T, seed)
     x = torch.from_numpy(bench.ar1_hidden(T, B, d, seed)).to(torch.bfloat16).cuda()
@@ -63,6 +64,7 @@ def run_case(capi, torch, cfg_d, model_d, T, K, hbm_peak, pcie_peak, pool=None, 
     st = capi.Stack(cfg, weight_seed=7, **kw, **model_d)
     create_s = time.time() - t0
     st.set_logits_trace(capi.trace_logits(scores), T)
+    keep = setup(st) if setup else None
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for i in range(T - K):
@@ -216,6 +218,44 @@ def c2_predictor(capi, torch, hbm, pcie, cpu):
     return out
 
 
+def c2_tier(capi, torch, hbm, pcie, cpu):
+    """The headline workload with the HBM expert tier (moeb_set_expert_sources;
+    SURVEY §8(f) rank 4): misses uploaded from a device-resident copy of the
+    pool (LocalTier: this GPU's HBM — on one GPU the stand-in for a peer GPU's
+    HBM over NVLink 5) instead of pinned host memory. A device tier runs the
+    uploads in serial mode, so the host-pool serial run is the like-for-like
+    comparison; decisions are identical in all three."""
+    from paper_2508_18983_b200.tier import LocalTier
+    cfg, model = split(DSV2)
+    cfg_d = dict(cfg, num_layers=26, batch=1, slots=16, alpha=0.25, seed=7)
+    T, K = 64, 48
+    out = {"workload": "DeepSeek-V2-Lite 26 L, batch 1, cache 16/64, trace-driven, CE+ER+Pre+BA"}
+    row, pool, _ = run_case(capi, torch, cfg_d, model, T, K, hbm, pcie)
+    out["host_pool_pipelined"] = row
+    os.environ["MOEB_SERIAL"] = "1"
+    row, st, _ = run_case(capi, torch, cfg_d, model, T, K, hbm, pcie, pool=pool)
+    st.close()
+    out["host_pool_serial"] = row
+    os.environ.pop("MOEB_SERIAL")
+    tiers = []
+    row, st, _ = run_case(capi, torch, cfg_d, model, T, K, hbm, pcie, pool=pool,
+                          setup=lambda s: tiers.append(LocalTier(torch, s, 26 * 64)))
+    st.close()
+    tiers.clear()
+    pool.close()
+    up = row["path_roofline"]["pcie_mb_per_step"] * 1e6
+    b_hbm = row["path_roofline"]["hbm_mb_per_step"] * 1e6
+    # the tier copies read and write HBM: the bound is HBM, not PCIe
+    t_roof = (b_hbm + 2 * up) / (hbm * 1e9) * 1e3
+    row["path_roofline"] = {"t_roof_ms": round(t_roof, 4), "frac": round(t_roof / row["ms_per_token"], 4),
+                            "hbm_mb_per_step": round(b_hbm / 1e6, 1), "tier_mb_per_step": round(up / 1e6, 1),
+                            "bound": "hbm"}
+    # a peer GPU's HBM over NVLink 5 (900 GB/s per direction) instead of this GPU's
+    row["nvlink5_projection_ms"] = round(max(b_hbm / (hbm * 1e9), up / 900e9) * 1e3, 4)
+    out["device_tier_serial"] = row
+    return out
+
+
 def c5(capi, torch, hbm, pcie, cpu):
     from paper_2508_18983_b200 import partition
     out = {"workload": "64 DeepSeek-V2-Lite requests x 16 tokens, stream-partitioned, cache 16/64, 1 GPU", "batch": {}}
@@ -227,7 +267,7 @@ def c5(capi, torch, hbm, pcie, cpu):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="C1,C2P,C3,C4,C5")
+    ap.add_argument("--only", default="C1,C2P,C2T,C3,C4,C5")
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -239,7 +279,7 @@ def main():
     res = {"hbm_peak_gbs": hbm, "pcie_peak_gbs": round(pcie, 2), "gpu": torch.cuda.get_device_name(0)}
     for name in args.only.split(","):
         t0 = time.time()
-        res[name] = {"C1": c1, "C2P": c2_predictor, "C3": c3, "C4": c4, "C5": c5}[name](capi, torch, hbm, pcie,
+        res[name] = {"C1": c1, "C2P": c2_predictor, "C2T": c2_tier, "C3": c3, "C4": c4, "C5": c5}[name](capi, torch, hbm, pcie,
                                                                                      not args.no_cpu)
         res[name]["wall_s"] = round(time.time() - t0, 1)
         print(f"{name} done in {res[name]['wall_s']} s", file=sys.stderr, flush=True)
