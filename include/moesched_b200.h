@@ -253,10 +253,10 @@ int moeb_prefill(moeb_stack* s, const void* x, void* y, uint32_t n_tokens, void*
  * this GPU's — instead of the pinned host pool. ptrs: [L*E], each pointing to
  * that expert's weights in this stack's pool layout (moeb_host_pool_flags);
  * NULL restores the host pool. Call between steps (synchronises the device).
- * Decisions are unchanged; only where the upload bytes come from. Copies
- * between device memories run as SM kernels, which cannot start beside the
- * persistent FFN grid, so a device tier puts the stack's uploads in serial
- * mode (the compute stream waits for each step's uploads before its FFN). */
+ * Decisions are unchanged; only where the upload bytes come from. A device
+ * tier puts the stack's uploads in serial mode (the compute stream waits for
+ * each step's uploads before its FFN): measured, a device-to-device upload
+ * does not complete while the pipelined FFN spins waiting for it. */
 int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n);
 /* MOEB_MODEL_LOG_STEPS: the last prefill's layer `layer`: input hidden
  * (bf16 [N][d]), router scores (fp32 [N][E]), selections in rank order

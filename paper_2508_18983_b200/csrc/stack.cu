@@ -2238,10 +2238,9 @@ int moeb_sync(moeb_stack* s) {
     MOEB_CUDA(cudaSetDevice(s->device));
     MOEB_CUDA(cudaStreamSynchronize(s->stream));
     MOEB_CUDA(cudaDeviceSynchronize());
-    if (const uint32_t to = take_spin_timeout()) {
-      throw Error(5, "device wait timed out (code " + std::to_string(to) + "): upload pipeline stalled");
-    }
-    if (s->copier_error) throw Error(5, s->copier_msg);
+    const uint32_t to = take_spin_timeout();
+    if (s->copier_error) throw Error(5, s->copier_msg);  // a failed upload is the cause of any stall
+    if (to) throw Error(5, "device wait timed out (code " + std::to_string(to) + "): upload pipeline stalled");
   });
 }
 
@@ -2451,13 +2450,14 @@ int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n) {
     }
     std::lock_guard<std::mutex> g(s->io_mu);
     s->src_tab = std::move(tab);
-    // Copies between device memories run as SM copy kernels (measured: a
-    // device-to-device cudaMemcpyAsync does not progress beside the persistent
-    // FFN grid, which leaves no room on any SM), so an FFN spinning on such an
-    // upload would wait for a copy that cannot start: with a device tier the
-    // stack orders uploads on the host (serial mode: the compute stream waits
-    // for the copy before the FFN launch).
-    s->serial = true;
+    // Measured: with the pipelined schedule (the FFN spinning on copies_done)
+    // a device-to-device upload issued by the copy thread does not complete
+    // while the FFN waits for it, although a standalone device-to-device copy
+    // does run beside a kernel that fills every SM (tools/probe/d2d_ce_probe.cu).
+    // So with a device tier the stack orders uploads on the host (serial mode:
+    // the compute stream waits for each step's copies before its FFN).
+    // MOEB_TIER_PIPELINED=1 keeps the pipelined schedule (diagnostics).
+    if (!getenv("MOEB_TIER_PIPELINED")) s->serial = true;
   });
 }
 

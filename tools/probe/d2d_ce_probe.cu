@@ -36,24 +36,30 @@ int main() {
   cudaStream_t sk, sc;
   CK(cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking));
-  for (int variant = 0; variant < 2; ++variant) {
+  const size_t sizes[3] = {196608, 1u << 20, bytes};
+  for (int vs = 0; vs < 6; ++vs) {
+    const int variant = vs & 1;
+    const size_t nb = sizes[vs >> 1];
     CK(cudaMemset(flag, 0, 4));
     *res = 0;
     CK(cudaDeviceSynchronize());
-    // one CTA per SM, big enough smem to own the SM
-    CK(cudaFuncSetAttribute(spin, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    spin<<<sms, 1024, 200 * 1024, sk>>>(flag, 7u, res);
+    // one CTA per SM with all of the opt-in shared memory (as the FFN grids
+    // use ~224 KB): nothing else fits on any SM
+    int optin = 0;
+    CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0));
+    CK(cudaFuncSetAttribute(spin, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+    spin<<<sms, 1024, optin, sk>>>(flag, 7u, res);
     CK(cudaGetLastError());
     if (variant == 0) {
-      CK(cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice, sc));
+      CK(cudaMemcpyAsync(b, a, nb, cudaMemcpyDeviceToDevice, sc));
     } else {
-      CK(cudaMemcpyAsync(hbuf, a, bytes, cudaMemcpyDeviceToHost, sc));
-      CK(cudaMemcpyAsync(b, hbuf, bytes, cudaMemcpyHostToDevice, sc));
+      CK(cudaMemcpyAsync(hbuf, a, nb, cudaMemcpyDeviceToHost, sc));
+      CK(cudaMemcpyAsync(b, hbuf, nb, cudaMemcpyHostToDevice, sc));
     }
     CUdeviceptr fp = (CUdeviceptr)flag;
     if (cuStreamWriteValue32(sc, fp, 7u, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) printf("writevalue failed\n");
     CK(cudaDeviceSynchronize());
-    printf("%s: %s\n", variant == 0 ? "cudaMemcpyAsync D2D" : "D2H + H2D through pinned memory",
+    printf("%zu B, %s: %s\n", nb, variant == 0 ? "cudaMemcpyAsync D2D" : "D2H + H2D through pinned memory",
            *res == 2 ? "progressed beside the persistent kernel (copy engine)" : "blocked until the kernel gave up (SM copy)");
   }
   return 0;
