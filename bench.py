@@ -294,7 +294,8 @@ def c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, B, t
     m = st.metrics()
     io = st.io_stats()
     st.close()
-    pcie = measure_pcie_gbs(torch)  # this GPU's link, for the path roofline
+    # this GPU's link for the path roofline: the probe, or the run's own copy rate if higher
+    pcie = max(measure_pcie_gbs(torch), io["h2d_bytes"] / max(io["copy_ms"], 1e-9) / 1e6)
     # the uploads the decisions call for (speculative chunks excluded)
     eb = 3 * MODEL["ffn"] * d * 2
     up = float(io["h2d_bytes"] - io["spec_bytes"] + io["spec_promoted"] * eb)

@@ -101,6 +101,17 @@ def pool_owner(keys: list, rank: int) -> int:
     return min(pool_groups(keys)[keys[rank]])
 
 
+def bind_to_device_node(device: int) -> int:
+    """Bind this process to the cores of its GPU's NUMA node (so pinned pools
+    it allocates are first-touched in the memory next to the GPU's PCIe root);
+    returns the node (-1: unknown, no binding)."""
+    node = device_numa_node(device)
+    cpus = node_cpus(node)
+    if cpus:
+        os.sched_setaffinity(0, cpus)
+    return node
+
+
 class NodePools:
     """One pinned expert pool replica per (host, NUMA node), shared by the
     ranks whose GPUs sit on that node. Setup-time collectives only (gloo):
@@ -117,10 +128,7 @@ class NodePools:
         self.dist = dist
         self.world = dist.get_world_size() if dist is not None else 1
         self.rank = dist.get_rank() if dist is not None else 0
-        self.node = device_numa_node(device)
-        cpus = node_cpus(self.node)
-        if cpus:
-            os.sched_setaffinity(0, cpus)
+        self.node = bind_to_device_node(device)
         me = (socket.gethostname(), self.node)
         if dist is not None:
             everyone = [None] * self.world

@@ -271,6 +271,8 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    from paper_2508_18983_b200 import partition
+    partition.bind_to_device_node(0)  # pinned pools first-touched on the GPU's NUMA node
     import torch
     from paper_2508_18983_b200 import capi
     torch.cuda.set_device(0)

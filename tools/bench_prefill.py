@@ -119,6 +119,8 @@ def main():
                     "capped stack at this N (0: skip)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
+    from paper_2508_18983_b200 import partition
+    partition.bind_to_device_node(0)  # pinned pools first-touched on the GPU's NUMA node
     import torch
     from paper_2508_18983_b200 import capi
     hbm, tflops = peaks()
