@@ -83,6 +83,12 @@ def main():
         print("ffn CTA0 entry rel. decide entry", us(tl[:, 7] - tl[:, 3]), "spec plan seen rel. decide entry",
               us((tl[:, 6] - tl[:, 3])[tl[:, 6] != 0]) if (tl[:, 6] != 0).any() else None)
         print("ffn start->end (no uploads)", us((tl[:, 2] - tl[:, 0])[~miss]))
+        if (tl[:, 13] != 0).all() and (tl[:, 14] != 0).all():
+            print("ffn phases (no uploads): CTA0 entry->plan", us((tl[:, 0] - tl[:, 7])[~miss]),
+                  "plan->last CTA done streaming", us((tl[:, 13] - tl[:, 0])[~miss]),
+                  "CTA0 done->last CTA done", us((tl[:, 13] - tl[:, 11])[~miss]),
+                  "last done->CTA0 past barrier", us((tl[:, 14] - tl[:, 13])[~miss]),
+                  "barrier->end (final sum)", us((tl[:, 2] - tl[:, 14])[~miss]))
         # algorithmic weight bytes per layer-step: distinct experts selected by
         # the batch (after substitution) + the shared expert
         dec = st.decisions()
