@@ -94,6 +94,26 @@ __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ 
   const uint32_t t0 = blockIdx.x * kPfRouterTok, e0 = blockIdx.y * 16;
   const uint32_t nt = min(kPfRouterTok, a.N - t0), nvec = d / 8;
   const bool first = blockIdx.y == 0;
+  // router B fragments (Wg rows e0 + lane/4 and e0 + 8 + lane/4, k pairs
+  // 2 (lane % 4) and + 8) of 8 k-steps of this warp's K eighth; the first
+  // chunk is in flight while x is staged and normalised
+  const uint32_t ea = e0 + (lane >> 2), eb = e0 + 8 + (lane >> 2);
+  const uint32_t* w0 = ea < E ? reinterpret_cast<const uint32_t*>(a.wg + (size_t)ea * d) + (lane & 3) : nullptr;
+  const uint32_t* w1 = eb < E ? reinterpret_cast<const uint32_t*>(a.wg + (size_t)eb * d) + (lane & 3) : nullptr;
+  const uint32_t kend_w = (warp + 1) * (d / 8);
+  auto load_b = [&](uint32_t c0, uint32_t (&b)[8][4]) {
+#pragma unroll
+    for (uint32_t i = 0; i < 8; ++i) {
+      const uint32_t k0 = c0 + 16 * i, kw = k0 / 2;
+      const bool in = k0 < kend_w;
+      b[i][0] = in && w0 ? __ldg(w0 + kw) : 0u;
+      b[i][1] = in && w0 ? __ldg(w0 + kw + 4) : 0u;
+      b[i][2] = in && w1 ? __ldg(w1 + kw) : 0u;
+      b[i][3] = in && w1 ? __ldg(w1 + kw + 4) : 0u;
+    }
+  };
+  uint32_t bfr[8][4];
+  load_b(warp * (d / 8), bfr);
   for (uint32_t i0 = threadIdx.x; i0 < kPfRouterTok * nvec; i0 += 8 * blockDim.x) {
     uint4 v[8];  // 8 independent 16 B loads in flight per thread
 #pragma unroll
@@ -145,21 +165,29 @@ __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ 
   }
   __syncthreads();
   {
-    const uint32_t kq = warp, kspan = d / 8;
+    const uint32_t kq = warp, kspan = d / 8, k_beg = kq * kspan, k_end = k_beg + kspan;
     float acc[2][4] = {};
     const uint32_t a_addr = smem_u32(us + (size_t)(lane & 15) * ld + (lane >> 4) * 8);
-    const uint32_t ea = e0 + (lane >> 2), eb = e0 + 8 + (lane >> 2);
-    const uint32_t* w0 = ea < E ? reinterpret_cast<const uint32_t*>(a.wg + (size_t)ea * d) + (lane & 3) : nullptr;
-    const uint32_t* w1 = eb < E ? reinterpret_cast<const uint32_t*>(a.wg + (size_t)eb * d) + (lane & 3) : nullptr;
-#pragma unroll 4
-    for (uint32_t k0 = kq * kspan; k0 < (kq + 1) * kspan; k0 += 16) {
-      const uint32_t kw = k0 / 2;
-      const uint32_t b00 = w0 ? __ldg(w0 + kw) : 0u, b01 = w0 ? __ldg(w0 + kw + 4) : 0u;
-      const uint32_t b10 = w1 ? __ldg(w1 + kw) : 0u, b11 = w1 ? __ldg(w1 + kw + 4) : 0u;
-      uint32_t af[4];
-      ldsm_x4(a_addr + k0 * 2, af);
-      mma16816(acc[0], af, b00, b01);
-      mma16816(acc[1], af, b10, b11);
+    // chunks of 8 k-steps: the B fragments of the next chunk are loaded while
+    // this one's MMAs run (the first chunk was loaded before the RMSNorm)
+    uint32_t bn[8][4];
+    for (uint32_t c0 = k_beg; c0 < k_end; c0 += 128) {
+      uint32_t bc[8][4];
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i)
+#pragma unroll
+        for (uint32_t q = 0; q < 4; ++q) bc[i][q] = c0 == k_beg ? bfr[i][q] : bn[i][q];
+      if (c0 + 128 < k_end) load_b(c0 + 128, bn);
+#pragma unroll
+      for (uint32_t i = 0; i < 8; ++i) {
+        const uint32_t k0 = c0 + 16 * i;
+        if (k0 < k_end) {
+          uint32_t af[4];
+          ldsm_x4(a_addr + k0 * 2, af);
+          mma16816(acc[0], af, bc[i][0], bc[i][1]);
+          mma16816(acc[1], af, bc[i][2], bc[i][3]);
+        }
+      }
     }
 #pragma unroll
     for (uint32_t j = 0; j < 2; ++j) {
