@@ -793,6 +793,19 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     if (threadIdx.x == 0) sm->cfg = a.cfg;
     (void)r_cd;
   }
+  // trace-driven routing: this layer's logits (and the next layer's, for
+  // the predictor) come from the trace, not the gate — staged now, while the
+  // gate CTAs run, and normalised in place after the gate arrivals
+  if (a.trace) {
+    const float* tr = a.trace + ((it % a.trace_steps) * L + layer) * B * E;
+    const float* ntr = a.trace + ((tit % a.trace_steps) * L + tl) * B * E;
+    for (uint32_t i = threadIdx.x; i < B * E; i += blockDim.x) {
+      const float v = __ldg(tr + i);
+      const float nv = want_next ? __ldg(ntr + i) : 0.f;
+      sm->sc[i / E][i % E] = v;
+      if (want_next) sm->nsc[i / E][i % E] = nv;
+    }
+  }
   MOEB_T(t_staged0);
   // the router logits and u of this layer: every gate CTA has arrived
   if (threadIdx.x == 0) {
@@ -809,8 +822,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   for (uint32_t j = warp; j < jobs; j += nw) {
     if (j < B) {
       const uint32_t t = j;
-      const float* lg = a.trace ? a.trace + (((it % a.trace_steps) * L + layer) * B + t) * E
-                                : a.logits + (size_t)t * (E + 1);
+      const float* lg = a.trace ? sm->sc[t] : a.logits + (size_t)t * (E + 1);  // in place for the trace
       softmax_warp(lg, E, sm->sc[t]);
       if (lane == 0 && a.shared_gate) {
         const float z = a.logits[(size_t)t * (E + 1) + E];
@@ -818,7 +830,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
       }
     } else {
       const uint32_t t = j - B;
-      softmax_warp(a.trace + (((tit % a.trace_steps) * L + tl) * B + t) * E, E, sm->nsc[t]);
+      softmax_warp(sm->nsc[t], E, sm->nsc[t]);
     }
   }
   // the shared expert depends on nothing the decision computes: released to
