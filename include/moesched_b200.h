@@ -308,7 +308,9 @@ int moeb_get_decisions(moeb_stack* s, moeb_step_record* steps, moeb_token_record
 /* Upload accounting: bytes and the copy stream's busy time (CUDA events). */
 typedef struct moeb_io_stats {
   uint64_t h2d_bytes, h2d_copies, d2d_copies, steps;
-  double copy_ms; /* sum of per-copy durations on the copy stream */
+  double copy_ms; /* copy-stream busy time: one upload in 8 is timed with CUDA events
+                   * (MOEB_COPY_TIMING_EVERY=n; 1 = every one) and the sum extrapolated
+                   * over all uploads (every upload is one expert) */
   /* speculative uploads (opt-in experiment, MOEB_SPEC_UPLOAD=1; batch-1 stacks
    * with stage Pre and a capped cache): after each decision the first expert of the
    * prefetch queue's ranking that is not resident in the next layer is
@@ -319,8 +321,9 @@ typedef struct moeb_io_stats {
   uint64_t spec_jobs, spec_promoted, spec_chunks, spec_bytes;
 } moeb_io_stats;
 int moeb_get_io_stats(moeb_stack* s, moeb_io_stats* st);
-/* Duration (ms, copy-stream CUDA events) of each expert upload since create or
- * moeb_reset_kernel_stats (first 65536): per-upload PCIe rates. */
+/* Duration (ms, copy-stream CUDA events) of the timed expert uploads (one in
+ * 8 by default, MOEB_COPY_TIMING_EVERY) since create or moeb_reset_kernel_stats
+ * (first 65536): per-upload PCIe rates. */
 int moeb_get_copy_times(moeb_stack* s, float* ms, size_t cap, size_t* n);
 /* Device buffers for tests: fp32 layer outputs of the last step ([L][B][d]) */
 int moeb_get_layer_outputs(moeb_stack* s, float* out, size_t cap);
