@@ -111,6 +111,17 @@ def test_c4_mixtral_shape_ladder(gpu, stages):
     st.close()
 
 
+@pytest.mark.parametrize("B", [2, 4])
+def test_c4_mixtral_shape_batched_tensor_core_ffn(gpu, B):
+    """The Mixtral shape at batch 2 / 4: the tcgen05 FFN over UMMA-tiled
+    experts at d = 4096, ffn = 14336 (112 intermediate tiles, 64 K-blocks) with
+    renormalised combine weights; decisions exact, both layers' outputs."""
+    st, kw, xs, dec, gsc, m = _run(gpu, "mixtral_8x7b", 2, B, 2, 5)
+    s = SHAPES["mixtral_8x7b"]
+    check_outputs(st, kw, xs, dec, gsc, s["d"], s["F"], 0, 0, 1)
+    st.close()
+
+
 def test_c5_independent_streams_concurrent_handles(gpu):
     """Stream partitioning: two decode streams (different trace seeds), each
     with its own handle, cache, copy thread and pinned pool, stepped from two

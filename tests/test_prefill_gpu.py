@@ -122,6 +122,24 @@ def test_prefill_dsv2_lite_full_width(gpu, B):
     st.close()
 
 
+@pytest.mark.parametrize("shape", ["qwen15_moe", "mixtral_8x7b"])
+def test_prefill_full_width_shapes(gpu, shape):
+    """Qwen1.5-MoE (60 experts top-4, 5632-wide sigmoid-gated shared expert)
+    and Mixtral-8x7B (d 4096, ffn 14336, renormalised top-2, no shared expert)
+    at full width, one layer on a batched stack with the capped cache: scores,
+    selections and the residual chain for every token, outputs of 16 tokens
+    against the oracle."""
+    import torch
+    L, E, k, d, F, S, sg, rn, slots, N = {
+        "qwen15_moe": (1, 60, 4, 2048, 1408, 5632, 1, 0, 15, 128),
+        "mixtral_8x7b": (1, 8, 2, 4096, 14336, 0, 0, 1, 2, 48)}[shape]
+    st, x, y, up = _run(gpu, torch, L, E, k, 2, d, F, S, slots, N, sg, rn)
+    assert up == L * (E - slots) * 3 * F * d * 2
+    rng = np.random.default_rng(1)
+    _check(st, x, y, L, E, k, d, F, S, sg, rn, 7, tokens=np.sort(rng.choice(N, 16, replace=False)))
+    st.close()
+
+
 def test_prefill_needs_128_multiple_ffn(gpu):
     import torch
     cfg = gpu.Config.make(num_layers=1, experts=16, top_k=4, batch=1, slots=4)
