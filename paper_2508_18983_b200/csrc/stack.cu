@@ -2023,6 +2023,19 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     for (uint32_t l = 0; l < L; ++l) ls[l].mask = all;
   } else {
     MOEB_CUDA(cudaStreamSynchronize(s));
+    // uploads the last decode steps decided (prefetches into cache slots) may
+    // still be with the copy thread: wait until it has taken every published
+    // mailbox entry, then for its copy stream, so every resident slot holds
+    // its expert before the GEMM reads it
+    const uint64_t want = S->predictor ? (S->host_seq ? 2 * S->host_seq - 1 : 0) : 2 * S->host_seq;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (*reinterpret_cast<volatile uint64_t*>(S->ack) < want) {
+      if (S->copier_error) throw Error(5, S->copier_msg);
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+        throw Error(5, "prefill: the copy thread did not take the decode steps' upload commands");
+      std::this_thread::yield();
+    }
+    MOEB_CUDA(cudaStreamSynchronize(S->copy_stream));
     MOEB_CUDA(cudaMemcpy(ls.data(), S->layers.p, sizeof(LayerState) * L, cudaMemcpyDeviceToHost));
   }
   const uint64_t eb = S->expert_elems * 2;

@@ -107,6 +107,29 @@ def test_prefill_reproducible_and_decode_state_untouched(gpu):
     st.close()
 
 
+def test_prefill_right_after_decode_with_prefetches(gpu):
+    """Decode steps whose stage Pre issues prefetches (copies into cache slots
+    that land after the step), then a prefill at once: it must read every
+    resident slot only after its upload landed, and match the oracle."""
+    import torch
+    L, E, k, B, d, F, S, slots, T, N = 1, 8, 2, 4, 256, 128, 0, 2, 30, 50
+    kw = dict(num_layers=L, experts=E, top_k=k, batch=B, slots=slots, alpha=0.25, seed=7, t_load=3)
+    st = gpu.Stack(gpu.Config.make(**kw), d, F, S, 0, 1, 1.0, weight_seed=7, log_steps=True)
+    st.set_logits_trace(gpu.trace_logits(gpu.generate_trace(L, E, B, T, 7)), T)
+    g = torch.Generator().manual_seed(3)
+    xs = torch.randn(T, B, d, generator=g).to(torch.bfloat16).cuda()
+    yd = torch.empty(B, d, dtype=torch.bfloat16, device="cuda")
+    for i in range(T):
+        st.step(xs[i].data_ptr(), yd.data_ptr(), B)
+    x = (torch.randn(N, d, generator=g) * 2).to(torch.bfloat16).cuda()
+    y = torch.empty_like(x)
+    st.prefill(x.data_ptr(), y.data_ptr(), N)  # no sync in between
+    st.sync()
+    assert st.metrics()["prefetch_loads"] > 0
+    _check(st, x, y, L, E, k, d, F, S, 0, 1, 7)
+    st.close()
+
+
 @pytest.mark.parametrize("B", [1, 2])
 def test_prefill_dsv2_lite_full_width(gpu, B):
     """DeepSeek-V2-Lite widths (64 experts top-6, 2 shared, d 2048, ffn 1408),
