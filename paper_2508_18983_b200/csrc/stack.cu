@@ -1947,6 +1947,22 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
   S->io.steps += 1;
 }
 
+// Uploads the last decode steps decided (prefetches into cache slots) may
+// still be with the copy thread after the compute stream is idle: wait until
+// it has taken every published mailbox entry, then for its copy stream.
+// Callers have synchronised the stream the steps ran on.
+static void drain_uploads(moeb_stack* S) {
+  const uint64_t want = S->predictor ? (S->host_seq ? 2 * S->host_seq - 1 : 0) : 2 * S->host_seq;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*reinterpret_cast<volatile uint64_t*>(S->ack) < want) {
+    if (S->copier_error) throw Error(5, S->copier_msg);
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
+      throw Error(5, "the copy thread did not take the decode steps' upload commands");
+    std::this_thread::yield();
+  }
+  MOEB_CUDA(cudaStreamSynchronize(S->copy_stream));
+}
+
 // ---------------------------------------------------------------- prefill
 // N prompt tokens through all L layers (prefill.cuh). Plain top-k routing
 // (no substitution, no cache admission: the decode state is untouched —
@@ -2023,19 +2039,8 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     for (uint32_t l = 0; l < L; ++l) ls[l].mask = all;
   } else {
     MOEB_CUDA(cudaStreamSynchronize(s));
-    // uploads the last decode steps decided (prefetches into cache slots) may
-    // still be with the copy thread: wait until it has taken every published
-    // mailbox entry, then for its copy stream, so every resident slot holds
-    // its expert before the GEMM reads it
-    const uint64_t want = S->predictor ? (S->host_seq ? 2 * S->host_seq - 1 : 0) : 2 * S->host_seq;
-    const auto t0 = std::chrono::steady_clock::now();
-    while (*reinterpret_cast<volatile uint64_t*>(S->ack) < want) {
-      if (S->copier_error) throw Error(5, S->copier_msg);
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(20))
-        throw Error(5, "prefill: the copy thread did not take the decode steps' upload commands");
-      std::this_thread::yield();
-    }
-    MOEB_CUDA(cudaStreamSynchronize(S->copy_stream));
+    // every resident slot must hold its expert before the GEMM reads it
+    drain_uploads(S);
     MOEB_CUDA(cudaMemcpy(ls.data(), S->layers.p, sizeof(LayerState) * L, cudaMemcpyDeviceToHost));
   }
   const uint64_t eb = S->expert_elems * 2;
@@ -2479,7 +2484,8 @@ int moeb_get_timeline(moeb_stack* s, uint64_t* out, size_t cap, size_t* n) {
 int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n) {
   return guarded([&] {
     MOEB_CUDA(cudaSetDevice(s->device));
-    MOEB_CUDA(cudaDeviceSynchronize());  // no upload in flight while the table changes
+    MOEB_CUDA(cudaDeviceSynchronize());
+    drain_uploads(s);  // no upload issued or in flight while the table changes
     if (!ptrs) {
       std::lock_guard<std::mutex> g(s->io_mu);
       s->src_tab.clear();
