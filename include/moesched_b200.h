@@ -258,6 +258,11 @@ int moeb_prefill(moeb_stack* s, const void* x, void* y, uint32_t n_tokens, void*
  * each step's uploads before its FFN): measured, a device-to-device upload
  * does not complete while the pipelined FFN spins waiting for it. */
 int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n);
+/* Diagnostics (MOEB_FFN_TSTAMP=1 at create, batch-1 split-K FFN): device-clock
+ * stamps [CTA][8] of the last FFN launch — entry, shared expert issued, certain
+ * experts released, certain experts issued, final plan in hand, every row
+ * issued, consumers done, end (0: phase not reached). n = words available. */
+int moeb_debug_ffn_tstamps(moeb_stack* s, uint64_t* out, size_t cap, size_t* n);
 /* MOEB_MODEL_LOG_STEPS: the last prefill's layer `layer`: input hidden
  * (bf16 [N][d]), router scores (fp32 [N][E]), selections in rank order
  * (uint8 [N][k]) and fp32 layer output before the residual ([N][d]); every

@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
   const uint32_t G = gridDim.x, c = blockIdx.x;
+  // MOEB_FFN_TSTAMP: per-CTA phase stamps [G][8] of the launch (diagnostics)
+  uint64_t* const ts = a.tstamp ? a.tstamp + (size_t)c * 8 : nullptr;
+  if (ts && threadIdx.x == 0) ts[0] = globaltimer_ns();
   const uint32_t d = a.d, S = a.stages, SB = a.stage_bytes;
   const int warp = warp_id(), lane = lane_id();
   unsigned char* ring = smem_raw;
@@ -246,8 +249,10 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         load_u();
         fetch(a.spec_plan, hdr, hdr + iw);
         stream(0, 1, kFfnSpecGuCtr, false);
+        if (ts && lane == 0) ts[1] = globaltimer_ns();
         n0 = 1;
         wait_flag(a.spec_flag, 9);
+        if (ts && lane == 0) ts[2] = globaltimer_ns();
       } else {
         wait_flag(a.spec_flag, 6);
         load_u();
@@ -256,8 +261,10 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       n_spec = ld_acquire_u32(&a.spec_plan->n_spec);
       fetch(a.spec_plan, hdr + n0 * iw, hdr + n_spec * iw);
       stream(n0, n_spec, kFfnSpecGuCtr, false);
+      if (ts && lane == 0) ts[3] = globaltimer_ns();
       // the final plan: its first n_spec items are the speculative ones
       wait_flag(a.spec_flag + 1, 0);
+      if (ts && lane == 0) ts[4] = globaltimer_ns();
       const uint32_t hdr_words = (uint32_t)(offsetof(Plan, items) / 8);
       fetch(a.plan, 0, hdr_words);
       fetch(a.plan, hdr_words + n_spec * (uint32_t)(sizeof(Item) / 8), a.plan_smem / 8);
@@ -306,6 +313,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       __syncwarp();
       stream(ii, ii + 1, ii, true);
     }
+    if (ts && lane == 0) ts[5] = globaltimer_ns();
     if (lane == 0) {
       for (int w = 0; w < NC; ++w) {  // one end marker per consumer warp
         const uint32_t st = acquire();
@@ -410,6 +418,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       }
   }
   __syncthreads();
+  if (ts && threadIdx.x == 0) ts[6] = globaltimer_ns();
   if (a.tl && c == 0 && threadIdx.x == 0) a.tl[11] = globaltimer_ns();
   if (a.tl && threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(&a.tl[13]), (unsigned long long)globaltimer_ns());
   // this CTA's partial y (warps summed in order) -> global partials [G][d]
@@ -526,6 +535,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       }
     }
     if (a.tl && c == 0) a.tl[2] = globaltimer_ns();
+    if (ts) ts[7] = globaltimer_ns();
   }
 }
 

@@ -1071,6 +1071,7 @@ struct moeb_stack {
   uint32_t layout_flags() const { return splitk ? MOEB_MODEL_DOWN_T : umma ? MOEB_MODEL_TILED : 0u; }
   uint32_t unit_rows = 0, ffn_dbg = 0;
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
+  DevBuf<uint64_t> ffn_ts;  // MOEB_FFN_TSTAMP: per-CTA phase stamps of the last split-K FFN launch
   DevBuf<StepRec> recs;
   DevBuf<uint64_t> timeline;  // [rec_cap][kTlWords] (MOEB_MODEL_TRACE_TIMELINE)
   DevBuf<TokRec> toks;
@@ -1622,6 +1623,10 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
     S->spec_flag.alloc(3);  // [0] speculative plan published, [1] final plan published, [2] shared expert released
     S->spec_flag.zero(s);
   }
+  if (getenv("MOEB_FFN_TSTAMP")) {
+    S->ffn_ts.alloc(8 * 160);
+    S->ffn_ts.zero(s);
+  }
   S->ffn_ctr.alloc(kFfnCtrWords);
   S->ffn_ctr.zero(s);
   S->copies_done.alloc(1);
@@ -1905,6 +1910,7 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     f.acc_rows = S->ffn.acc_rows;
     f.plan_smem = S->ffn.plan_smem;
     f.tl = a.tl;
+    f.tstamp = S->splitk ? S->ffn_ts.p : nullptr;
     f.spec_plan = a.spec_plan;
     f.spec_flag = S->spec_flag.p;
     f.shared_first = a.shared_first;
@@ -2518,6 +2524,14 @@ int moeb_set_expert_sources(moeb_stack* s, const void* const* ptrs, size_t n) {
     // the compute stream waits for each step's copies before its FFN).
     // MOEB_TIER_PIPELINED=1 keeps the pipelined schedule (diagnostics).
     if (!getenv("MOEB_TIER_PIPELINED")) s->serial = true;
+  });
+}
+
+int moeb_debug_ffn_tstamps(moeb_stack* s, uint64_t* out, size_t cap, size_t* n) {
+  return guarded([&] {
+    MOEB_CUDA(cudaDeviceSynchronize());
+    *n = s->ffn_ts.n;
+    if (out && *n) MOEB_CUDA(cudaMemcpy(out, s->ffn_ts.p, std::min(cap, *n) * 8, cudaMemcpyDeviceToHost));
   });
 }
 
