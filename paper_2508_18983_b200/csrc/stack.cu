@@ -1624,7 +1624,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
     S->spec_flag.zero(s);
   }
   if (getenv("MOEB_FFN_TSTAMP")) {
-    S->ffn_ts.alloc(8 * 160);
+    S->ffn_ts.alloc(8 * (size_t)n_sm);  // [CTA][8]: the split-K grid is at most one CTA per SM
     S->ffn_ts.zero(s);
   }
   S->ffn_ctr.alloc(kFfnCtrWords);

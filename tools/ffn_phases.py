@@ -39,7 +39,7 @@ def main():
         st.step(x[i].data_ptr(), y.data_ptr(), B)
         st.sync()
         n = C.c_size_t(0)
-        buf = np.zeros(8 * 160, dtype=np.uint64)
+        buf = np.zeros(8 * 256, dtype=np.uint64)  # >= 8 words per SM
         capi.check(lib.moeb_debug_ffn_tstamps(st.h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), C.c_size_t(buf.size),
                                               C.byref(n)))
         if i >= T // 3:
