@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmoeb.so")
+LIB_PATH = os.environ.get("MOEB_LIB") or os.path.join(HERE, "libmoeb.so")  # MOEB_LIB: an alternative build (e.g. make PROFILE=1), diagnostics
 
 MAXE, MAXK, MAXB = 64, 16, 32
 
