@@ -444,7 +444,7 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   sp->seq = (uint32_t)sm->seq;
   sm->spec_n = n;
   sm->spec_set = set;
-  __threadfence();
+  // (the release store below orders this lane's plan writes)
   if (uploads) {
     const uint64_t t0 = globaltimer_ns();
     while (!atomicAdd(const_cast<uint32_t*>(&sm->mail_a), 0u) && globaltimer_ns() - t0 < kSpinLimitNs) {}
@@ -749,8 +749,9 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   // the FFN grid counters of this step, zeroed before the FFN kernel (which
   // may already be resident) can see the speculative plan or the final one:
   // fenced before the barrier that precedes both releases
-  if (threadIdx.x == 0) {
-    for (uint32_t i = 0; i < (uint32_t)kFfnCtrWords; ++i) a.ffn_ctr[i] = 0;
+  // (by the last warp: its fence does not delay warp 0's staging loads)
+  if (threadIdx.x >= blockDim.x - 32) {
+    for (uint32_t i = threadIdx.x - (blockDim.x - 32); i < (uint32_t)kFfnCtrWords; i += 32) a.ffn_ctr[i] = 0;
     __threadfence();
   }
   const int warp = warp_id(), lane = lane_id();
@@ -850,8 +851,10 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     }
   }
   // the shared expert depends on nothing the decision computes: released to
-  // the (already resident) FFN right after the gate, before classification
-  if (a.shared_first && threadIdx.x == 0) {
+  // the (already resident) FFN right after the gate, before classification,
+  // by the last warp beside the softmax (batch 1: warp 0). The release store
+  // orders this thread's item writes (no separate fence).
+  if (a.shared_first && threadIdx.x == blockDim.x - 32) {
     Item& it0 = a.spec_plan->items[0];
     it0.w = a.shared_w;
     it0.F = a.S;
@@ -860,8 +863,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     it0.kind = 0;
     it0.expert = 0;
     it0.tok[0] = 0;
-    it0.wt[0] = a.shared_gate ? sm->sg[0] : 1.0f;
-    __threadfence();
+    it0.wt[0] = a.shared_gate ? __fdiv_rn(1.0f, 1.0f + expf(-a.logits[E])) : 1.0f;  // = sg[0]
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag + 2), "r"((uint32_t)a.seq) : "memory");
   }
   const bool run_pending = a.predictor && sm->st.pf_pending && sm->st.pf_layer == layer && sm->st.pf_it == it;
