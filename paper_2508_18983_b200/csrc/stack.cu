@@ -91,20 +91,20 @@ struct MailCmd {
 // once every word shows the entry's tag — no system-scope fence on the
 // device's publish path (measured ~1.5-2.5 us per upload layer), and a
 // word left over from the entry kRing sequences earlier carries another tag.
-struct WireCmd {
+struct __align__(16) WireCmd {
   uint64_t w[6];  // src_off | dst | bytes, kind, buf | id | wait_ffn | gen  (payload <= 48 bits each)
 };
 static_assert(sizeof(WireCmd) == sizeof(MailCmd), "wire command size");
 __host__ __device__ inline uint64_t wire_tag(uint64_t mseq) { return (mseq & 0xffffull) << 48; }
 __device__ __forceinline__ void put_wire(WireCmd* wc, const MailCmd& c, uint64_t mseq) {
   const uint64_t t = wire_tag(mseq), m = (1ull << 48) - 1;
-  volatile uint64_t* w = wc->w;
-  w[0] = (c.src_off & m) | t;
-  w[1] = (c.dst & m) | t;
-  w[2] = (c.bytes & ((1ull << 40) - 1)) | ((uint64_t)(c.kind & 15u) << 40) | ((uint64_t)(c.buf & 15u) << 44) | t;
-  w[3] = (uint64_t)c.id | t;
-  w[4] = (uint64_t)c.wait_ffn | t;
-  w[5] = (uint64_t)c.gen | t;
+  const uint64_t w0 = (c.src_off & m) | t, w1 = (c.dst & m) | t;
+  const uint64_t w2 = (c.bytes & ((1ull << 40) - 1)) | ((uint64_t)(c.kind & 15u) << 40) | ((uint64_t)(c.buf & 15u) << 44) | t;
+  const uint64_t w3 = (uint64_t)c.id | t, w4 = (uint64_t)c.wait_ffn | t, w5 = (uint64_t)c.gen | t;
+  // three 16-byte stores to the mapped ring (each 8-byte half arrives whole)
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(wc->w), "l"(w0), "l"(w1) : "memory");
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(wc->w + 2), "l"(w2), "l"(w3) : "memory");
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(wc->w + 4), "l"(w4), "l"(w5) : "memory");
 }
 // seq word = (sequence << 8) | command count, one 64-bit store
 struct MailEntry {
