@@ -381,6 +381,55 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
       }
       const float wt = __uint_as_float(s_hdr[st][2]);
       const uint16_t* base = reinterpret_cast<const uint16_t*>(ring + st * SB);
+      if constexpr (XREG) {
+        if (!(a.dbg & 1)) {
+          // the down column to registers and the gate/up MMAs, then the
+          // stage goes back to the producer (the arrive's release orders
+          // the reads) before the reduction, silu and the down FMAs
+          const uint4* wd = reinterpret_cast<const uint4*>(base + 2 * d);
+          uint4 wdr[kSkMaxYChunks];
+#pragma unroll
+          for (int j = 0; j < kSkMaxYChunks; ++j)
+            if ((uint32_t)j < ych) wdr[j] = wd[j * 32 + lane];
+          float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
+          const uint32_t dbase = diag_addr(smem_u32(base), smem_u32(base + d));
+          const uint32_t nb = d / 128;
+#pragma unroll
+          for (int b = 0; b < 16; b += 2) {
+            if ((uint32_t)b < nb) {
+              uint32_t f[4];
+              ldsm_x4(dbase + b * 256, f);
+              mma16816(acc, f, xb[b][0], xb[b][1]);
+            }
+            if ((uint32_t)b + 1 < nb) {
+              uint32_t f[4];
+              ldsm_x4(dbase + (b + 1) * 256, f);
+              mma16816(acc2, f, xb[b + 1][0], xb[b + 1][1]);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty_bar[st]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += acc2[q];
+          const float2 gu = diag_reduce(acc);
+          const float s = wt * (__fdiv_rn(gu.x, 1.0f + expf(-gu.x)) * gu.y);
+#pragma unroll
+          for (int j = 0; j < kSkMaxYChunks; ++j) {
+            if ((uint32_t)j < ych) {
+              const uint4 w = wdr[j];
+              y[j][0] = fmaf(s, __uint_as_float(w.x << 16), y[j][0]);
+              y[j][1] = fmaf(s, __uint_as_float(w.x & 0xffff0000u), y[j][1]);
+              y[j][2] = fmaf(s, __uint_as_float(w.y << 16), y[j][2]);
+              y[j][3] = fmaf(s, __uint_as_float(w.y & 0xffff0000u), y[j][3]);
+              y[j][4] = fmaf(s, __uint_as_float(w.z << 16), y[j][4]);
+              y[j][5] = fmaf(s, __uint_as_float(w.z & 0xffff0000u), y[j][5]);
+              y[j][6] = fmaf(s, __uint_as_float(w.w << 16), y[j][6]);
+              y[j][7] = fmaf(s, __uint_as_float(w.w & 0xffff0000u), y[j][7]);
+            }
+          }
+          continue;
+        }
+      }
       if (!(a.dbg & 1)) {
         float hv;
         if constexpr (XREG) hv = sk_h(base, base + d, xb, d);
