@@ -730,6 +730,7 @@ __device__ inline void deferred_prefetch(const StepCtx& cx, DecideSmem* sm, uint
 struct NoHook {
   __device__ void operator()(DecideSmem*, uint32_t, uint32_t) const {}
   __device__ void classified(DecideSmem*, uint64_t) const {}
+  __device__ void classified_early(DecideSmem*, uint64_t) const {}
   __device__ void plan_ready(DecideSmem*) const {}
   __device__ void prefetched(DecideSmem*) const {}
 };
@@ -821,6 +822,16 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
   const uint64_t mask = cx.ls->mask;  // snapshot the router sees (pipeline.cpp:154-155)
   __syncthreads();
   mark(4);
+  // the speculative plan needs only the classification and the snapshot:
+  // built by the last warp beside route pass 2 when that warp routes no
+  // token; the route barrier below then leaves that warp out (it hands its
+  // result to warp 2 on named barrier 7), so route -> loads -> mailbox A on
+  // warp 0 never waits for it
+  const bool early_spec = B < nw && nw >= 5;
+  if (early_spec && warp == (int)nw - 1) {
+    on_loads.classified_early(sm, mask);
+    asm volatile("bar.arrive 7, 64;" ::: "memory");
+  }
   // route pass 2 (router.cpp:114-149), one warp per token; C (the union of
   // the batch's top-score experts, router.cpp:105-112) computed by every warp
   if (cfg.er) {
@@ -839,7 +850,11 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
       }
     }
   }
-  __syncthreads();
+  if (early_spec) {
+    if (warp != (int)nw - 1) asm volatile("bar.sync 6, %0;" ::"r"((nw - 1) * 32) : "memory");
+  } else {
+    __syncthreads();
+  }
   mark(17);
 
   // ---- fork. warp 0 routes and runs the order-dependent rest; alongside it
@@ -872,6 +887,7 @@ __device__ inline void decide_step(const StepCtx& cx, DecideSmem* sm, NextSmem* 
     return;
   }
   if (warp == 2) {
+    if (early_spec) asm volatile("bar.sync 7, 64;" ::: "memory");  // the last warp's speculative plan
     on_loads.classified(sm, mask);
     asm volatile("bar.arrive 3, 64;" ::: "memory");
     return;

@@ -30,6 +30,7 @@ constexpr int kSkMaxStages = 24;
 constexpr int kSkStages = 16;        // a multiple of the consumer warps (2 stages each); 192 KB at d = 2048
 constexpr int kSkMaxYChunks = 8;     // d <= 2048: 8 columns x 8 chunks per lane
 constexpr uint32_t kSkStaticUnitRows = 4;  // rows per unit when dealt round-robin (default)
+constexpr uint32_t kSkWtShared = 0xffffffffu;  // stage header: combine weight = s_wt_shared (a NaN pattern)
 constexpr uint32_t kSkUnitRows = 16;  // rows per grab in the first tier (same-address atomics serialise: keep grabs few)
 
 // silu(g.u) * (u_r.u) for one gate/up row pair in shared memory; every lane
@@ -102,6 +103,11 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   __shared__ float s_yloc[2048];
   __shared__ volatile uint32_t s_turn;
   __shared__ uint32_t s_snap;
+  // shared-expert rows prefetched before the gate has run: consumers wait
+  // for s_uready (u written, shared expert released) and take the combine
+  // weight of stages marked kSkWtShared from s_wt_shared
+  __shared__ volatile uint32_t s_uready;
+  __shared__ float s_wt_shared;
   asm volatile("griddepcontrol.launch_dependents;");
   if (a.tl && blockIdx.x == 0 && threadIdx.x == 0) a.tl[7] = globaltimer_ns();
   const uint32_t G = gridDim.x, c = blockIdx.x;
@@ -117,6 +123,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
   if (threadIdx.x == 0) {
     s_turn = 0;
     s_snap = 0;
+    s_uready = 0;
     for (uint32_t s = 0; s < S; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -243,9 +250,39 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
     if (spec) {
       const uint32_t hdr = (uint32_t)(offsetof(Plan, items) / 8), iw = (uint32_t)(sizeof(Item) / 8);
       uint32_t n0 = 0;
-      if (a.shared_first) {
+      if (a.shared_first && XREG && a.shared_w && a.deterministic && !a.unit_rows) {
+        // the shared expert's weights do not depend on the gate: this CTA's
+        // first ring-full of its rows is issued at once (HBM is idle while
+        // the gate and the classification run), the rest after the release
+        // (same rows, same ring steps as stream(): bitwise-identical sums)
+        const uint32_t rows = a.shared_F;
+        const uint32_t r0 = (uint32_t)((uint64_t)rows * c / G), r1 = (uint32_t)((uint64_t)rows * (c + 1) / G);
+        const uint32_t pre = min(r1 - r0, S);
+        if (lane == 0) {
+          Item& it0 = p->items[0];
+          it0.w = a.shared_w;
+          it0.F = rows;
+          it0.wt[0] = __uint_as_float(kSkWtShared);
+          for (uint32_t r = r0; r < r0 + pre; ++r) issue_row(0, r);
+        }
+        __syncwarp();
+        wait_flag(a.spec_flag + 2, 6);
+        fetch(a.spec_plan, hdr, hdr + iw);
+        if (lane == 0) {
+          s_wt_shared = p->items[0].wt[0];
+          __threadfence_block();
+          s_uready = 1;
+          for (uint32_t r = r0 + pre; r < r1; ++r) issue_row(0, r);
+        }
+        __syncwarp();
+        if (ts && lane == 0) ts[1] = globaltimer_ns();
+        n0 = 1;
+        wait_flag(a.spec_flag, 9);
+        if (ts && lane == 0) ts[2] = globaltimer_ns();
+      } else if (a.shared_first) {
         // the shared expert, released right after the gate
         wait_flag(a.spec_flag + 2, 6);
+        if (lane == 0) s_uready = 1;
         load_u();
         fetch(a.spec_plan, hdr, hdr + iw);
         stream(0, 1, kFfnSpecGuCtr, false);
@@ -370,6 +407,14 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         break;
       }
       if (XREG && !have_x) {  // u: the gate phase wrote it before either plan was released
+        if (a.shared_first) {  // (rows may have been issued before the release)
+          const uint64_t t0 = globaltimer_ns();
+          while (!s_uready) {
+            __nanosleep(20);
+            if (globaltimer_ns() - t0 > kSpinLimitNs) { atomicExch(&g_spin_timeout, 9u); break; }
+          }
+          __threadfence_block();
+        }
         const uint32_t* u32w = reinterpret_cast<const uint32_t*>(a.u);
 #pragma unroll
         for (int b = 0; b < (XREG ? kXrBlocks : 1); ++b) {
@@ -379,7 +424,7 @@ __global__ void __launch_bounds__(32 * (NC + 1), 1) ffn_splitk_kernel(FfnTArgs a
         }
         have_x = true;
       }
-      const float wt = __uint_as_float(s_hdr[st][2]);
+      const float wt = s_hdr[st][2] == kSkWtShared ? s_wt_shared : __uint_as_float(s_hdr[st][2]);
       const uint16_t* base = reinterpret_cast<const uint16_t*>(ring + st * SB);
       if constexpr (XREG) {
         if (!(a.dbg & 1)) {

@@ -114,6 +114,8 @@ struct FfnTArgs {
   uint32_t unit_rows;      // split-K kernel: intermediate rows per grid-counter grab (0: default)
   uint32_t deterministic;  // split-K kernel: static row -> (CTA, warp) assignment (bitwise-reproducible sums)
   uint32_t shared_first;   // split-K kernel: item 0 (shared expert) of spec_plan released alone by spec_flag[2]
+  const uint16_t* shared_w;  // split-K kernel with shared_first: the layer's shared expert (rows prefetched
+  uint32_t shared_F;         //   into the ring before the release), its intermediate rows
   const uint32_t* spec_done;  // split-K kernel: speculative upload generations landed, per buffer [2]
 };
 

@@ -185,6 +185,7 @@ struct DecideKSmem {
   uint32_t n_cmds;
   uint32_t landed;            // copies_done when the step's state was staged
   volatile uint32_t mail_a;   // mailbox entry A is out (warp 0 -> warp 2)
+  uint32_t spec_stage;        // speculative plan: 0 not built, 1 built (release after mailbox A), 2 released
   uint32_t spec_n;            // items in the speculative plan (0: none published)
   uint64_t spec_set;          // routed experts in it
   uint64_t it, seq;
@@ -267,12 +268,13 @@ __device__ __forceinline__ void wait_ring_slot(const DecideArgs& a, uint64_t mse
 // Mailbox entry A of a layer-step (sequence 2*seq-1): the demand loads and
 // BA-streamed experts, published from inside the decision step the moment
 // the lists are final. Entry B (2*seq) carries the prefetches later.
-__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d, uint64_t mask);
+__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d, uint64_t mask, bool early);
 
 struct EarlyPublish {
   const DecideArgs* a;
   DecideKSmem* sm;
-  __device__ void classified(DecideSmem* d, uint64_t mask) const { publish_spec(*a, sm, d, mask); }
+  __device__ void classified(DecideSmem* d, uint64_t mask) const { publish_spec(*a, sm, d, mask, false); }
+  __device__ void classified_early(DecideSmem* d, uint64_t mask) const { publish_spec(*a, sm, d, mask, true); }
   __device__ void plan_ready(DecideSmem* d) const;
   __device__ void prefetched(DecideSmem* d) const;
   __device__ void operator()(DecideSmem* d, uint32_t n_load, uint32_t n_cpu) const {
@@ -395,8 +397,20 @@ struct EarlyPublish {
 // landed is final: hits are shielded (pipeline.cpp:196-201), so its slot
 // cannot change in this step. Publishing these lets the FFN kernel (already
 // resident via PDL) stream them while the rest of the decision runs.
-__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d, uint64_t mask) {
-  if (lane_id() != 0) return;  // one lane of warp 2, beside the routing on warp 0
+// early: called by the last warp right after classification (beside route
+// pass 2, batch < warps); the plan is built and, unless it must wait for the
+// step's uploads to be handed off, released there. Otherwise (or if it was
+// not called early) warp 2 finishes it after the fork.
+__device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideSmem* d, uint64_t mask, bool early) {
+  if (lane_id() != 0) return;  // one lane of warp 2 (or the last warp), beside the routing on warp 0
+  if (!early && sm->spec_stage == 2) return;
+  if (!early && sm->spec_stage == 1) {
+    const uint64_t t0 = globaltimer_ns();
+    while (!atomicAdd(const_cast<uint32_t*>(&sm->mail_a), 0u) && globaltimer_ns() - t0 < kSpinLimitNs) {}
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
+    sm->spec_stage = 2;
+    return;
+  }
   sm->spec_n = 0;
   sm->spec_set = 0;
   if (!a.spec_plan) return;
@@ -445,11 +459,16 @@ __device__ void publish_spec(const DecideArgs& a, DecideKSmem* sm, const DecideS
   sm->spec_n = n;
   sm->spec_set = set;
   // (the release store below orders this lane's plan writes)
+  if (uploads && early) {
+    sm->spec_stage = 1;  // warp 2 releases it once mailbox A is out
+    return;
+  }
   if (uploads) {
     const uint64_t t0 = globaltimer_ns();
     while (!atomicAdd(const_cast<uint32_t*>(&sm->mail_a), 0u) && globaltimer_ns() - t0 < kSpinLimitNs) {}
   }
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.spec_flag), "r"((uint32_t)sm->seq) : "memory");
+  sm->spec_stage = 2;
 }
 
 // Warp 0 builds the FFN plan in shared memory as soon as the loads and
@@ -873,6 +892,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
     sm->it = it;
     sm->seq = a.seq;
     sm->mail_a = 0;
+    sm->spec_stage = 0;
     sm->d.next_has_pred = run_pending ? (B >= 64 ? ~0ull : (1ull << B) - 1ull) : 0ull;
   }
   __syncthreads();
@@ -1085,6 +1105,7 @@ struct moeb_stack {
   DevBuf<uint32_t> gcnt;
   uint32_t layout_flags() const { return splitk ? MOEB_MODEL_DOWN_T : umma ? MOEB_MODEL_TILED : 0u; }
   uint32_t unit_rows = 0, ffn_dbg = 0;
+  bool sk_shared_prefetch = true;  // split-K: shared-expert rows issued before the release (MOEB_NO_SHARED_PREFETCH=1: off)
   DevBuf<uint32_t> ffn_ctr, copies_done, ffn_done;
   DevBuf<uint64_t> ffn_ts;  // MOEB_FFN_TSTAMP: per-CTA phase stamps of the last split-K FFN launch
   DevBuf<StepRec> recs;
@@ -1577,6 +1598,7 @@ static void build_stack(moeb_stack* S, const moeb_config& cfg, const moeb_model&
   S->splitk = B == 1 && d <= 2048 && d <= 16u * (uint32_t)(n_sm - 1) && getenv("MOEB_NO_SPLITK") == nullptr;
   if (const char* ur = getenv("MOEB_SK_UNIT")) S->unit_rows = (uint32_t)atoi(ur);
   if (const char* fd = getenv("MOEB_FFN_DBG")) S->ffn_dbg = (uint32_t)atoi(fd);  // microbenchmark knob
+  S->sk_shared_prefetch = getenv("MOEB_NO_SHARED_PREFETCH") == nullptr;
   // batch 2..32: tensor-core FFN over UMMA-tiled experts, when the shapes
   // tile (ffn, shared_ffn multiples of 128) and the pool is ours to lay out
   // (or a caller pool declares the tiled layout). MOEB_NO_UMMA=1 selects the
@@ -1978,6 +2000,8 @@ static void step_stack_locked(moeb_stack* S, const void* x, void* y, uint32_t B,
     f.spec_plan = a.spec_plan;
     f.spec_flag = S->spec_flag.p;
     f.shared_first = a.shared_first;
+    f.shared_w = S->sk_shared_prefetch ? a.shared_w : nullptr;
+    f.shared_F = a.S;
     f.spec_done = S->spec_done.p;
     f.seq = (uint32_t)a.seq;
     f.unit_rows = S->unit_rows;
