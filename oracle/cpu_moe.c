@@ -24,9 +24,13 @@
  * cpu_bytes_touched() reports the weight bytes read, so bench.py can state the
  * achieved host GB/s next to the baseline.
  */
+#ifndef _POSIX_C_SOURCE
+#define _POSIX_C_SOURCE 200809L /* nanosleep */
+#endif
 #include <immintrin.h>
 #include <math.h>
 #include <pthread.h>
+#include <time.h>
 #include <sched.h>
 #include <stdatomic.h>
 #include <stdint.h>
@@ -74,8 +78,14 @@ static void* worker(void* arg) {
     uint64_t g;
     unsigned spins = 0;
     while ((g = atomic_load_explicit(&g_pool.gen, memory_order_acquire)) == seen) {
+      /* spin through the short gaps between phases; park once idle (a
+       * yielding worker would keep all cores busy and slow the GPU runs'
+       * host threads that follow a CPU baseline) */
       if (++spins < (1u << 16)) _mm_pause();
-      else sched_yield();
+      else {
+        struct timespec ts = {0, 100000};
+        nanosleep(&ts, NULL);
+      }
     }
     seen = g;
     g_pool.fn(g_pool.ctx, tid, g_pool.n);
