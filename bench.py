@@ -228,6 +228,8 @@ def batched_section(capi, torch, local, hbm_peak, batches=(8, 32), n_warm=8, n_t
                 e0.record(s)
                 for i in range(n_warm, T):
                     st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+                if not allhit:
+                    st.sync()  # every upload the timed steps published has landed
                 e1.record(s)
                 e1.synchronize()
                 st.sync()
@@ -283,6 +285,7 @@ def c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, B, t
             st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
         st.sync()
         st.reset()
+        io0 = st.io_stats()  # the warm-up's uploads are not part of the timed job
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -290,12 +293,12 @@ def c5_partitioned(capi, partition, torch, dist, pools, world, rank, local, B, t
         e0.record(s)
         for i in range(T):
             st.step(x[i].data_ptr(), y.data_ptr(), B, stream=s.cuda_stream)
+        st.sync()  # every upload the timed steps published has landed (they are counted)
         e1.record(s)
         e1.synchronize()
-        st.sync()
     ms = e0.elapsed_time(e1)
     m = st.metrics()
-    io = st.io_stats()
+    io = {k: v - io0.get(k, 0) if isinstance(v, (int, float)) else v for k, v in st.io_stats().items()}
     st.close()
     # this GPU's link for the path roofline: the probe, or the run's own copy rate if higher
     pcie = max(measure_pcie_gbs(torch), io["h2d_bytes"] / max(io["copy_ms"], 1e-9) / 1e6)

@@ -84,7 +84,17 @@ struct PfRouterArgs {
 // layer.cuh gate_phase), then logits of 16 experts on mma.sync m16n8k16:
 // warp w takes the K eighth w; the eighths are summed in a fixed order
 // (fp32 accumulation).
+// Programmatic dependent launch between the per-layer prefill kernels: each
+// waits for its predecessor grid (complete, memory visible) before touching
+// anything, and lets its own dependent start launching at once, so the
+// launch and CTA rasterisation of the next kernel overlap this one's tail.
+__device__ __forceinline__ void pf_pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
 __global__ void __launch_bounds__(256) pf_router_kernel(const __grid_constant__ PfRouterArgs a) {
+  pf_pdl_entry();
   extern __shared__ __align__(16) unsigned char pf_rsm[];
   const uint32_t d = a.d, E = a.E, ld = d + 8;
   uint16_t* us = reinterpret_cast<uint16_t*>(pf_rsm);
@@ -327,6 +337,7 @@ struct PfTopkArgs {
 // aggregated per CTA in shared memory, one global atomic per expert per CTA;
 // the last CTA to finish builds the plan (pf_plan_warp).
 __global__ void __launch_bounds__(256) pf_topk_kernel(const __grid_constant__ PfTopkArgs a) {
+  pf_pdl_entry();
   __shared__ uint32_t hist[kMaxE];
   const int lane = lane_id();
   const uint32_t E = a.E, k = a.k;
@@ -413,12 +424,17 @@ struct PfScatterArgs {
   int32_t* entry_slot;   // [N][k]
   unsigned char* xg;     // [d/64][R][128 B]
   uint32_t N, k, d, R;
+  uint32_t* ctr_zero;    // the GEMM's unit / tile counters, zeroed here (the previous GEMM is complete)
+  uint32_t n_ctr;
 };
 
 __global__ void __launch_bounds__(256) pf_scatter_kernel(const __grid_constant__ PfScatterArgs a) {
+  pf_pdl_entry();
   __shared__ uint32_t s_slot[32];
   const int lane = lane_id(), warp = warp_id();
   const uint32_t n = a.N * a.k, nvec = a.d / 8;
+  if (blockIdx.x == 0)
+    for (uint32_t i = threadIdx.x; i < a.n_ctr; i += blockDim.x) a.ctr_zero[i] = 0;
   const uint32_t i0 = blockIdx.x * 32;
   if (warp == 0) {
     const uint32_t i = i0 + lane;
@@ -478,6 +494,7 @@ struct PfRetileArgs {
 };
 
 __global__ void __launch_bounds__(256) pf_retile_kernel(const __grid_constant__ PfRetileArgs a) {
+  pf_pdl_entry();
   __shared__ __align__(16) uint16_t tr[64][128 + 8];
   const uint32_t e = blockIdx.y, d = a.d;
   const bool sh = a.shared_src && e == a.E;
@@ -538,6 +555,7 @@ struct PfRec {
 };
 
 __global__ void __launch_bounds__(kPfThreads, 1) pf_gemm_kernel(const __grid_constant__ PfGemmArgs a) {
+  pf_pdl_entry();
   extern __shared__ unsigned char pf_smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kPfStages], empty_bar[kPfStages];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
@@ -753,6 +771,7 @@ __global__ void __launch_bounds__(256) pf_combine_kernel(const uint16_t* __restr
                                                          const int32_t* __restrict__ entry_slot, uint16_t* __restrict__ xo,
                                                          float* __restrict__ y, uint32_t N, uint32_t d, uint32_t k,
                                                          uint32_t shared) {
+  pf_pdl_entry();
   const uint32_t per = d / 4;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N * per; i += gridDim.x * blockDim.x) {
     const uint32_t t = i / per, c = (i % per) * 4;

@@ -2193,7 +2193,8 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     ra.d = d;
     ra.E = E;
     ra.R = S->pf_R;
-    pf_router_kernel<<<dim3((N + kPfRouterTok - 1) / kPfRouterTok, (E + 15) / 16), 256, r_smem, s>>>(ra);
+    launch_pdl(reinterpret_cast<const void*>(pf_router_kernel), dim3((N + kPfRouterTok - 1) / kPfRouterTok, (E + 15) / 16),
+               dim3(256), r_smem, s, &ra);
     MOEB_CUDA(cudaGetLastError());
     PfTopkArgs ta{};
     ta.logits = S->pf_logits.p;
@@ -2226,7 +2227,7 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     ta.plan.items = S->pf_items.p;
     ta.plan.hdr = S->pf_hdr.p;
     ta.ticket = S->pf_cnt.p + kMaxE;
-    pf_topk_kernel<<<(N + 7) / 8, 256, 0, s>>>(ta);
+    launch_pdl(reinterpret_cast<const void*>(pf_topk_kernel), dim3((N + 7) / 8), dim3(256), 0, s, &ta);
     MOEB_CUDA(cudaGetLastError());
     PfScatterArgs sa{};
     sa.sel = S->pf_sel.p;
@@ -2240,9 +2241,10 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     sa.k = k;
     sa.d = d;
     sa.R = S->pf_R;
-    pf_scatter_kernel<<<(N * k + 31) / 32, 256, 0, s>>>(sa);
+    sa.ctr_zero = S->pf_ctr.p;
+    sa.n_ctr = (uint32_t)S->pf_ctr.n;
+    launch_pdl(reinterpret_cast<const void*>(pf_scatter_kernel), dim3((N * k + 31) / 32), dim3(256), 0, s, &sa);
     MOEB_CUDA(cudaGetLastError());
-    MOEB_CUDA(cudaMemsetAsync(S->pf_ctr.p, 0, S->pf_ctr.n * sizeof(uint32_t), s));
     if (retile) {
       PfRetileArgs rt{};
       rt.ls = S->layers.p + l;
@@ -2256,7 +2258,7 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
       rt.F = F;
       rt.S = Sh;
       const uint32_t Fm = std::max(F, Sh), tiles = (Fm / 128) * (d / 64) * 2 + (d / 128) * (Fm / 64);
-      pf_retile_kernel<<<dim3(tiles, E + (Sh ? 1 : 0)), 256, 0, s>>>(rt);
+      launch_pdl(reinterpret_cast<const void*>(pf_retile_kernel), dim3(tiles, E + (Sh ? 1 : 0)), dim3(256), 0, s, &rt);
       MOEB_CUDA(cudaGetLastError());
     }
     PfGemmArgs ga{};
@@ -2269,12 +2271,25 @@ static uint64_t prefill_stack(moeb_stack* S, const void* x, void* y, uint32_t N,
     ga.ctr = S->pf_ctr.p;
     ga.d = d;
     ga.R = S->pf_R;
-    pf_gemm_kernel<<<n_sm, kPfThreads, kPfStages * kPfStageBytes + 1024, s>>>(ga);
+    launch_pdl(reinterpret_cast<const void*>(pf_gemm_kernel), dim3(n_sm), dim3(kPfThreads), kPfStages * kPfStageBytes + 1024, s,
+               &ga);
     MOEB_CUDA(cudaGetLastError());
     if (any_up) MOEB_CUDA(cudaEventRecord(S->pf_free[l % 2], s));
     float* ylog = log && N <= S->pf_log_n ? S->pf_log_y.p + (size_t)l * N * d : nullptr;
-    pf_combine_kernel<<<(unsigned)std::min<uint64_t>(((uint64_t)N * d / 4 + 255) / 256, (uint64_t)n_sm * 16), 256, 0,
-                        s>>>(xin, S->pf_out.p, S->pf_entry.p, xout, ylog, N, d, k, Sh ? 1u : 0u);
+    {
+      cudaLaunchConfig_t cc{};
+      cc.gridDim = dim3((unsigned)std::min<uint64_t>(((uint64_t)N * d / 4 + 255) / 256, (uint64_t)n_sm * 16));
+      cc.blockDim = dim3(256);
+      cc.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = kUsePdl ? 1 : 0;
+      cc.attrs = at;
+      cc.numAttrs = 1;
+      const float* pout = S->pf_out.p;
+      const int32_t* pent = S->pf_entry.p;
+      MOEB_CUDA(cudaLaunchKernelEx(&cc, pf_combine_kernel, xin, pout, pent, xout, ylog, N, d, k, Sh ? 1u : 0u));
+    }
     MOEB_CUDA(cudaGetLastError());
     if (ylog) {
       MOEB_CUDA(cudaMemcpyAsync(S->pf_log_x.p + (size_t)l * N * d, xin, (size_t)N * d * 2, cudaMemcpyDeviceToDevice, s));
@@ -2390,6 +2405,9 @@ int moeb_sync(moeb_stack* s) {
     MOEB_CUDA(cudaSetDevice(s->device));
     MOEB_CUDA(cudaStreamSynchronize(s->stream));
     MOEB_CUDA(cudaDeviceSynchronize());
+    // and every upload the steps published (prefetches for later steps
+    // included) has been issued by the copy thread and has landed
+    if (s->host_seq) drain_uploads(s);
     const uint32_t to = take_spin_timeout();
     if (s->copier_error) throw Error(5, s->copier_msg);  // a failed upload is the cause of any stall
     if (to) throw Error(5, "device wait timed out (code " + std::to_string(to) + "): upload pipeline stalled");
