@@ -139,8 +139,32 @@ struct GateArgs {
 // ng = ceil(rows / 2) gate CTAs with rows = E (+1 for the shared gate), gi the
 // CTA's index among them; 8 warps: warp w -> row 2*gi + (w & 1), quarter (w >> 1) of d.
 // us: [B][d] bf16 scratch in shared memory.
+// This warp's chunk of its router row (d <= 4096: <= 4 x 16 B per lane),
+// loaded by the gate CTAs BEFORE the programmatic-dependency wait: the router
+// weights do not depend on the previous layer, so the load overlaps its FFN's
+// tail (gate_decide_kernel).
+constexpr uint32_t kGateWPre = 4;
+struct GateWPre {
+  uint4 w[kGateWPre];
+  bool ok;
+};
+__device__ __forceinline__ GateWPre gate_w_prefetch(const GateArgs& a, uint32_t gi) {
+  GateWPre r;
+  const int lane = lane_id(), warp = warp_id();
+  const uint32_t rows = a.E + (a.wsg ? 1u : 0u), row = 2 * gi + (warp & 1), q = warp >> 1;
+  const uint32_t per_q = a.d / 32, c0 = q * per_q;  // (d / 8) / 4 vectors per quarter
+  r.ok = row < rows && per_q % 32 == 0 && per_q / 32 <= kGateWPre;
+  if (r.ok) {
+    const uint4* wv = reinterpret_cast<const uint4*>(row < a.E ? a.wg + (size_t)row * a.d : a.wsg);
+#pragma unroll
+    for (uint32_t j = 0; j < kGateWPre; ++j)
+      if (j < per_q / 32) r.w[j] = __ldg(wv + c0 + j * 32 + lane);
+  }
+  return r;
+}
+
 __device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, uint32_t ng, const uint16_t* xsrc,
-                                  float* logits_out, bool write_u) {
+                                  float* logits_out, bool write_u, const GateWPre* wp = nullptr) {
   __shared__ float part[4][2][kMaxB];
   __shared__ float inv_rms[kMaxB];
   const int lane = lane_id(), warp = warp_id();
@@ -215,7 +239,13 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, 
       for (uint32_t t = 0; t < B; ++t) {
         const uint4* uv = reinterpret_cast<const uint4*>(us + (size_t)t * d);
         float s = 0.f;
-        for (uint32_t c = c0 + lane; c < c1; c += 32) s += dot8(__ldg(wv + c), uv[c]);
+        if (wp && wp->ok) {  // same order as the loop below: c = c0 + lane + 32 j
+#pragma unroll
+          for (uint32_t j = 0; j < kGateWPre; ++j)
+            if (j < nvec / 4 / 32) s += dot8(wp->w[j], uv[c0 + j * 32 + lane]);
+        } else {
+          for (uint32_t c = c0 + lane; c < c1; c += 32) s += dot8(__ldg(wv + c), uv[c]);
+        }
         s = warp_sum(s);
         if (lane == 0) part[q][warp & 1][t] = s;
       }
@@ -224,7 +254,8 @@ __device__ inline void gate_phase(const GateArgs& a, uint16_t* us, uint32_t gi, 
       // partial dots of all tokens, then one transposed butterfly (31
       // shuffles for 32 tokens instead of 5 per token): lane t ends with
       // token t's sum
-      const uint4 w0 = __ldg(wv + c0 + lane), w1 = __ldg(wv + c0 + 32 + lane);
+      const bool pre = wp && wp->ok;
+      const uint4 w0 = pre ? wp->w[0] : __ldg(wv + c0 + lane), w1 = pre ? wp->w[1] : __ldg(wv + c0 + 32 + lane);
       float p[32];
 #pragma unroll
       for (uint32_t t = 0; t < 32; ++t) {

@@ -730,8 +730,12 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
 #else
 #define MOEB_T(x) const uint64_t x = 0
 #endif
-  // PDL: wait for the previous layer's FFN (x, plan buffers), then let the
-  // next kernel's CTAs start launching as ours retire
+  // the gate CTAs' router rows first (static weights: the load overlaps the
+  // previous layer's FFN tail); then PDL: wait for the previous layer's FFN
+  // (x, plan buffers), and let the next kernel's CTAs start launching as ours retire
+  GateWPre wpre;
+  wpre.ok = false;
+  if (blockIdx.x != 0) wpre = gate_w_prefetch(ga.g, blockIdx.x - 1);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;");
   MOEB_T(t_entry);
@@ -747,7 +751,7 @@ __global__ void __launch_bounds__(kGdThreads, 1) gate_decide_kernel(GateDecideAr
   const uint32_t n_gate = gridDim.x - 1;
   if (blockIdx.x != 0) {
     // us [B][d] bf16 aliases the decision workspace
-    gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw), blockIdx.x - 1, n_gate, ga.g.x, ga.g.logits, true);
+    gate_phase(ga.g, reinterpret_cast<uint16_t*>(smem_raw), blockIdx.x - 1, n_gate, ga.g.x, ga.g.logits, true, &wpre);
     if (ga.g.x_pred) {
       // the predictor: this layer's router on the previous layer's partial
       // forward (shared expert + resident hits)
